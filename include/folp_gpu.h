@@ -1,0 +1,219 @@
+/*
+ * folp_gpu.h -- the thin C ABI between the host C++ solve driver
+ * (paper_2106_04756_b200/csrc/host/solver.cpp, which keeps folp::solve's
+ * C++ signature, /root/reference/proj/include/folp/solver.hpp:226-228) and
+ * the sm_100a CUDA engine (paper_2106_04756_b200/csrc/engine/engine.cu).
+ *
+ * One folp_gpu_ctx owns one presolved LP resident in HBM (CSR + CSC with
+ * int32 indices, original and scaled fp64 values), every iterate buffer of
+ * the PDLP loop and its own CUDA stream, so concurrent solves on one GPU
+ * are independent (the reentrancy the reference bench harness relies on,
+ * proj/src/bench.cpp:46-73).  Host arrays are caller-owned and copied;
+ * device buffers are context-owned.  No C++ exception crosses this ABI:
+ * every call returns FOLP_OK or a FOLP_E_* code from folp_c.h and
+ * folp_gpu_last_error() holds the message.
+ *
+ * Points live in the working (scaled) space unless stated otherwise.
+ */
+#ifndef FOLP_GPU_H_
+#define FOLP_GPU_H_
+
+#include <stdint.h>
+
+#include "folp_c.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct folp_gpu_ctx folp_gpu_ctx;
+
+/* Point slots held by a context. */
+enum {
+  FOLP_PT_CURRENT = 0,  /* z_k of the loop (SolveDriver::current_)        */
+  FOLP_PT_AVERAGE = 1,  /* materialized running average                  */
+  FOLP_PT_LAST = 2,     /* last restart point (SolveDriver::last_restart_) */
+  FOLP_PT_AUX = 3       /* free slot for one-shot operations              */
+};
+
+/* Chunk exit status. */
+enum {
+  FOLP_CHUNK_RUNNING = 0,
+  FOLP_CHUNK_DONE = 1,        /* target accepted iterations reached        */
+  FOLP_CHUNK_LIMIT = 2,       /* iteration or KKT-pass limit hit mid-chunk */
+  FOLP_CHUNK_NONFINITE = 3,   /* pdhg_trial produced NaN/inf (solver.cpp:91-93) */
+  FOLP_CHUNK_UNDERFLOW = 4    /* adaptive eta < 1e-300 (solver.cpp:196-198) */
+};
+
+/* The presolved LP (two-block form, inequality rows first).  CSR is
+ * required; CSC may be NULL (then it is built from the CSR on the host,
+ * columns in increasing row order like SparseMatrix::from_triplets).
+ * NULL vectors are read as zeros (matrix-only contexts). */
+typedef struct folp_gpu_problem {
+  int64_t num_rows;
+  int64_t num_cols;
+  int64_t num_inequality_rows;
+  int64_t nnz;
+  const int64_t* row_start;
+  const int64_t* row_cols;
+  const double* row_values;
+  const int64_t* col_start;
+  const int64_t* col_rows;
+  const double* col_values;
+  const double* objective;
+  const double* right_hand_side;
+  const double* variable_lower;
+  const double* variable_upper;
+  double objective_constant;
+} folp_gpu_problem;
+
+/* Loop state mirrored between host and device at chunk boundaries. */
+typedef struct folp_gpu_loop {
+  int32_t policy;            /* FOLP_STEP_ADAPTIVE or FOLP_STEP_CONSTANT  */
+  int32_t status;            /* out: FOLP_CHUNK_*                         */
+  int64_t target;            /* in: accepted iterations wanted            */
+  int64_t accepted;          /* out                                        */
+  int64_t k_total;           /* in/out: SolveDriver::k_total_              */
+  int64_t t_inner;           /* in/out: SolveDriver::t_inner_              */
+  int64_t step_trials;       /* in/out                                     */
+  int64_t violations;        /* in/out: step_condition_violations          */
+  int64_t ledger_k;          /* in/out: KktPassLedger::k_multiplies        */
+  int64_t ledger_kt;         /* in/out: KktPassLedger::kt_multiplies       */
+  int64_t iteration_limit;   /* in                                         */
+  double kkt_pass_limit;     /* in                                         */
+  double omega;              /* in: primal weight                          */
+  double eta;                /* in/out: eta_hat (adaptive) or eta (const)  */
+  double last_eta_used;      /* out                                        */
+  double avg_weight;         /* out: sum of eta over the running average   */
+  double last_movement;      /* out: ||z'-z||_omega^2 of the last trial    */
+  double last_cross;         /* out: (y-y')'K(x'-x) of the last trial      */
+  int64_t slots;             /* out: trial slots executed                  */
+  const double* reduction;   /* in: [target] 1-(k+1)^-0.3 per iteration    */
+  const double* growth;      /* in: [target] 1+(k+1)^-0.6 per iteration    */
+} folp_gpu_loop;
+
+/* Convergence quantities (termination.cpp:23-73) as partial sums, so the
+ * host forms ConvergenceInfo with the reference's final arithmetic. */
+typedef struct folp_gpu_eval {
+  double c_dot_x;            /* c'x                                       */
+  double q_dot_y;            /* q'y                                       */
+  double bound_terms;        /* sum l_i lambda_i^+ + u_i lambda_i^-       */
+  double primal_sq;          /* ||(q-Kx) with (.)^+ on >= rows||^2        */
+  double dual_sq;            /* ||c - K'y - lambda||^2                    */
+  double norm_q;             /* ||q||_2                                   */
+  double norm_c;             /* ||c||_2                                   */
+  int32_t nonfinite;         /* point had NaN/inf (NonFiniteIterate)      */
+  int32_t infinite_product;  /* lambda outside its cone (InfiniteProduct) */
+} folp_gpu_eval;
+
+/* Context lifetime. device < 0 picks $FOLP_DEVICE (default 0). */
+int folp_gpu_create(const folp_gpu_problem* problem, int device,
+                    folp_gpu_ctx** out);
+void folp_gpu_destroy(folp_gpu_ctx* ctx);
+
+/* rescale_problem (scaling.cpp:48-96) on device: ruiz_iterations Ruiz
+ * (inf-norm) steps then optionally one Pock-Chambolle step; builds
+ * K~ = D1 K D2, c~, q~, l~, u~.  D1/D2 are downloaded when non-NULL. */
+int folp_gpu_rescale(folp_gpu_ctx* ctx, int64_t ruiz_iterations,
+                     int32_t pock_chambolle, double alpha, double* row_scale,
+                     double* col_scale);
+
+/* Working-problem statistics: max|K~| (sparse_matrix.cpp:149-154) and the
+ * norms used by initialize_primal_weight (solver.cpp:421-427). */
+int folp_gpu_working_stats(folp_gpu_ctx* ctx, double* max_abs_entry,
+                           double* norm_c, double* norm_q);
+
+/* Scaled values and vectors of the working problem (for parity tests). */
+int folp_gpu_get_working(folp_gpu_ctx* ctx, double* csr_values,
+                         double* csc_values, double* objective, double* rhs,
+                         double* lower, double* upper);
+
+/* Start point in the presolved (unscaled) space: z/D then projected
+ * (solver.cpp:853-865); sets CURRENT = LAST = z and clears the average. */
+int folp_gpu_set_start(folp_gpu_ctx* ctx, const double* x, const double* y);
+
+/* Raw working-space upload/download of a point slot. */
+int folp_gpu_set_point(folp_gpu_ctx* ctx, int32_t which, const double* x,
+                       const double* y);
+int folp_gpu_get_point(folp_gpu_ctx* ctx, int32_t which, double* x,
+                       double* y);
+
+/* reduced_point (solver.cpp:495-502): unscale and clamp into the presolved
+ * bounds, downloaded to x [n], y [m]. */
+int folp_gpu_get_reduced_point(folp_gpu_ctx* ctx, int32_t which, double* x,
+                               double* y);
+
+/* Flush the pending averaging weight and materialize AVERAGE
+ * (materialize_average, solver.cpp:509-528).  *weight = sum of etas. */
+int folp_gpu_materialize_average(folp_gpu_ctx* ctx, double* weight);
+
+/* convergence_info of a slot after reduced_point (solver.cpp:504-507).
+ * raw != 0 evaluates the slot as given (already in the presolved space,
+ * no unscaling or clamping), i.e. the standalone convergence_info. */
+int folp_gpu_evaluate(folp_gpu_ctx* ctx, int32_t which, int32_t raw,
+                      folp_gpu_eval* out);
+
+/* linalg::all_finite of both halves of a slot (solver.cpp:731-734). */
+int folp_gpu_all_finite(folp_gpu_ctx* ctx, int32_t which, int32_t* finite);
+
+/* SparseMatrix::axis_norms (sparse_matrix.cpp:156-186) of the original
+ * (working == 0) or working values; axis 0 = rows, 1 = columns. */
+int folp_gpu_axis_norms(folp_gpu_ctx* ctx, int32_t axis, double p,
+                        int32_t working, double* out);
+
+/* SparseMatrix::max_abs_entry (sparse_matrix.cpp:149-154). */
+int folp_gpu_max_abs_entry(folp_gpu_ctx* ctx, int32_t working, double* out);
+
+/* Squared distances sum (x_a-x_b)^2, sum (y_a-y_b)^2 (weighted_norm and
+ * diff_norm2 inputs, lp_model.cpp:167-173, linalg.hpp:47-54). */
+int folp_gpu_distance(folp_gpu_ctx* ctx, int32_t a, int32_t b, double* sx,
+                      double* sy);
+
+/* normalized_duality_gap (solver.cpp:277-370) of a slot. */
+int folp_gpu_ndg(folp_gpu_ctx* ctx, int32_t which, double radius,
+                 double omega, double* gap);
+
+/* Restart bookkeeping (solver.cpp:810-815): LAST = CURRENT = slot; when
+ * reset_average the running average is cleared. */
+int folp_gpu_restart_to(folp_gpu_ctx* ctx, int32_t which,
+                        int32_t reset_average);
+
+/* Sets LAST = CURRENT without touching the average (kNone schedule,
+ * solver.cpp:771-781). */
+int folp_gpu_mark_last(folp_gpu_ctx* ctx);
+
+/* Runs PDHG iterations on device until loop->target steps were accepted
+ * or the loop stopped (limit, non-finite, underflow).  Trials, step-size
+ * decisions, the ledger and the averaging all stay on device; the host
+ * sees one synchronisation per chunk. */
+int folp_gpu_run_chunk(folp_gpu_ctx* ctx, folp_gpu_loop* loop);
+
+/* Power iteration on K~'K~ (sparse_matrix.cpp:188-220) from a host start
+ * vector v0 [n] (already normalised by the caller). */
+int folp_gpu_spectral_norm(folp_gpu_ctx* ctx, const double* v0,
+                           double relative_tol, int64_t max_iterations,
+                           double* norm, int64_t* multiplies);
+
+/* K x / K'y on the original (unscaled) or working values of the context.
+ * Host vectors in, host vectors out. */
+int folp_gpu_multiply(folp_gpu_ctx* ctx, int32_t working, const double* x,
+                      double* out);
+int folp_gpu_multiply_transpose(folp_gpu_ctx* ctx, int32_t working,
+                                const double* y, double* out);
+
+/* Kernel launches issued by this context so far (for bench accounting). */
+int64_t folp_gpu_launch_count(const folp_gpu_ctx* ctx);
+
+/* Timing of the two fused step kernels inside the last chunk (ms),
+ * measured with CUDA events on the context stream when enabled. */
+int folp_gpu_set_profiling(folp_gpu_ctx* ctx, int32_t enabled);
+int folp_gpu_chunk_timing(folp_gpu_ctx* ctx, double* chunk_ms,
+                          int64_t* slots);
+
+const char* folp_gpu_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FOLP_GPU_H_ */

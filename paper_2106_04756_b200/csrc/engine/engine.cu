@@ -1,0 +1,1319 @@
+// engine.cu -- the sm_100a PDLP engine behind include/folp_gpu.h.
+//
+// Data layout in HBM (one context = one presolved LP):
+//   CSR  : int32 row_ptr[m+1], int32 col[nnz], fp64 val_orig[nnz], val_work[nnz]
+//   CSC  : int32 col_ptr[n+1], int32 row[nnz], fp64 val_orig[nnz], val_work[nnz]
+//          (CSC = CSR of K', columns in increasing row order, so K'y is the
+//           same row-dot kernel as Kx; indices shared by both value sets)
+//   vectors: presolved c,q,l,u and scaled c~,q~,l~,u~, D1, D2; iterate
+//          double buffers x[2], y[2], Kx[2]; average sums; AVERAGE, LAST,
+//          AUX points; evaluation / duality-gap scratch.
+// All fp64, structure-of-arrays, 256-byte aligned by cudaMalloc.
+//
+// Compiled with -fmad=false (see Makefile): every a*b+c is two IEEE
+// roundings like the reference's x86-64 build.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "folp_gpu.h"
+#include "ops.cuh"
+
+using namespace folpgpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct EngineError : std::runtime_error {
+  int code;
+  EngineError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) {                                                  \
+      throw EngineError(e_ == cudaErrorMemoryAllocation ? FOLP_E_NOMEM        \
+                                                        : FOLP_E_CUDA,        \
+                        std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    }                                                                         \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return FOLP_OK;
+  } catch (const EngineError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return FOLP_E_NOMEM;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return FOLP_E_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FOLP_E_RUNTIME;
+  }
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+// ---------------------------------------------------------------------
+// Scaling kernels (rescale_problem, scaling.cpp:48-96; axis_norms,
+// sparse_matrix.cpp:156-186).
+__global__ void k_axis_absmax(const int* __restrict__ ptr, const double* __restrict__ val,
+                              int S, double* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int s = warp; s < S; s += nwarps) {
+    double a = 0.0;
+    for (int k = ptr[s] + lane; k < ptr[s + 1]; k += 32) a = fmax(a, fabs(val[k]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a = fmax(a, __shfl_down_sync(0xffffffffu, a, off));
+    if (lane == 0) out[s] = a;  // max is order-independent: bit-exact
+  }
+}
+
+// Sequential per-segment p-norm in increasing index order: bit-identical to
+// the reference's loop for p = 0, 1, 2 (pow for other p is CUDA's).
+__global__ void k_axis_pnorm_seq(const int* __restrict__ ptr, const double* __restrict__ val,
+                                 int S, double p, double* __restrict__ out) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int k = ptr[s]; k < ptr[s + 1]; ++k) {
+      const double a = fabs(val[k]);
+      if (p == 0.0) {
+        acc += 1.0;
+      } else if (p == 1.0) {
+        acc += a;
+      } else if (p == 2.0) {
+        acc += a * a;
+      } else {
+        acc += pow(a, p);
+      }
+    }
+    if (p == 2.0) {
+      acc = sqrt(acc);
+    } else if (isfinite(p) && p > 1.0 && p != 2.0) {
+      acc = pow(acc, 1.0 / p);
+    }
+    out[s] = acc;
+  }
+}
+
+// reciprocal_sqrt (scaling.cpp:23-28) fused with the cumulative product
+// (scaling.cpp:58-65): d = v > 0 ? 1/sqrt(v) : 1; cum *= d.
+__global__ void k_recip_sqrt_cum(double* __restrict__ v, double* __restrict__ cum, int S) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    const double x = v[s];
+    const double d = x > 0.0 ? 1.0 / sqrt(x) : 1.0;
+    v[s] = d;
+    cum[s] *= d;
+  }
+}
+
+// SparseMatrix::scaled (sparse_matrix.cpp:222-242): out = src * (dseg*didx).
+__global__ void k_scale_values(const int* __restrict__ ptr, const int* __restrict__ idx,
+                               const double* __restrict__ src, double* __restrict__ dst,
+                               int S, const double* __restrict__ dseg,
+                               const double* __restrict__ didx) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int s = warp; s < S; s += nwarps) {
+    const double ds = dseg[s];
+    for (int k = ptr[s] + lane; k < ptr[s + 1]; k += 32) dst[k] = src[k] * (ds * didx[idx[k]]);
+  }
+}
+
+// Scaled vectors (scaling.cpp:82-94).
+__global__ void k_scale_vectors(int64_t n, int64_t m, const double* c, const double* l,
+                                const double* u, const double* q, const double* d1,
+                                const double* d2, double* cw, double* lw, double* uw,
+                                double* qw) {
+  const int64_t total = n + m;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) {
+      const double s = d2[i];
+      cw[i] = c[i] * s;
+      lw[i] = l[i] / s;
+      uw[i] = u[i] / s;
+    } else {
+      const int64_t j = i - n;
+      qw[j] = q[j] * d1[j];
+    }
+  }
+}
+
+__global__ void k_fill(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_narrow(const int64_t* __restrict__ src, int* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = static_cast<int>(src[i]);
+}
+
+// Start point (solver.cpp:853-865): z/D then projected.
+__global__ void k_start_point(int64_t n, int64_t m, int64_t m1, const double* x0,
+                              const double* y0, const double* d1, const double* d2,
+                              const double* lw, const double* uw, double* x, double* y,
+                              double* lx, double* ly) {
+  const int64_t total = n + m;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) {
+      const double v = ref_min(ref_max(x0[i] / d2[i], lw[i]), uw[i]);
+      x[i] = v;
+      lx[i] = v;
+    } else {
+      const int64_t j = i - n;
+      double v = y0[j] / d1[j];
+      if (j < m1) v = ref_max(v, 0.0);
+      y[j] = v;
+      ly[j] = v;
+    }
+  }
+}
+
+// reduced_point (solver.cpp:495-502).
+__global__ void k_reduced_point(int64_t n, int64_t m, const double* xs, const double* ys,
+                                const double* d1, const double* d2, const double* l,
+                                const double* u, double* xr, double* yr) {
+  const int64_t total = n + m;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) {
+      xr[i] = ref_min(ref_max(xs[i] * d2[i], l[i]), u[i]);
+    } else {
+      const int64_t j = i - n;
+      yr[j] = ys[j] * d1[j];
+    }
+  }
+}
+
+__global__ void k_div_scalar(double* __restrict__ dst, const double* __restrict__ src,
+                             int64_t n, const double* __restrict__ denom_sq) {
+  const double snorm = sqrt(denom_sq[0]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] / snorm;  // sparse_matrix.cpp:213
+}
+
+__global__ void k_absmax_all(const double* __restrict__ v, int64_t n, double* out) {
+  __shared__ double s[kWarps];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a = fmax(a, fabs(v[i]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) a = fmax(a, __shfl_down_sync(0xffffffffu, a, off));
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < kWarps; ++w) r = fmax(r, s[w]);
+    *out = r;
+  }
+}
+
+struct OpCountNonFinite {
+  static constexpr int K = 1;
+  static constexpr bool kReduce = true;
+  int64_t n;
+  const double* x;
+  const double* y;
+  double* result;
+  __device__ bool prepare() { return true; }
+  __device__ void apply(int64_t i, double (&acc)[K]) const {
+    const double v = i < n ? x[i] : y[i - n];
+    if (!isfinite(v)) acc[0] += 1.0;
+  }
+  __device__ void finalize(const double (&tot)[K]) const { result[0] = tot[0]; }
+};
+
+struct OpNormSq {
+  static constexpr int K = 1;
+  static constexpr bool kReduce = true;
+  const double* v;
+  double* result;
+  __device__ bool prepare() { return true; }
+  __device__ void apply(int64_t i, double (&acc)[K]) const { acc[0] += v[i] * v[i]; }
+  __device__ void finalize(const double (&tot)[K]) const { result[0] = tot[0]; }
+};
+
+// ---------------------------------------------------------------------
+struct PlanDev {
+  SegPlan sp{};
+  int L = 1;
+  std::vector<void*> owned;
+};
+
+std::mutex g_occ_mu;
+std::unordered_map<const void*, int> g_occ;
+
+int occupancy(const void* fn) {
+  std::lock_guard<std::mutex> lk(g_occ_mu);
+  auto it = g_occ.find(fn);
+  if (it != g_occ.end()) return it->second;
+  int b = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, 0));
+  if (b < 1) b = 1;
+  g_occ[fn] = b;
+  return b;
+}
+
+constexpr int kResSlots = 64;
+constexpr int kCounters = 16;
+constexpr int kMaxGrid = 148 * 8;
+
+}  // namespace
+
+struct folp_gpu_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t m = 0, n = 0, m1 = 0, nnz = 0;
+  double objective_constant = 0.0;
+
+  int *csr_ptr = nullptr, *csr_col = nullptr, *csc_ptr = nullptr, *csc_row = nullptr;
+  double *csr_orig = nullptr, *csc_orig = nullptr, *csr_work = nullptr, *csc_work = nullptr;
+  PlanDev rows, cols;
+
+  double *c0, *q0, *l0, *u0;
+  double *cw, *qw, *lw, *uw, *d1, *d2;
+  double *x[2], *y[2], *kx[2];
+  double *avg_x, *avg_y;
+  double *avgp_x, *avgp_y, *last_x, *last_y, *aux_x, *aux_y;
+  double *kx_avg;   // K~ x of AVERAGE (filled by the duality gap)
+  double *kx_aux;
+  double *xr, *yr;  // reduced point scratch
+  double *g, *lo, *hi;
+  double *partials;
+  unsigned* counters;
+  double* res;      // small result slots
+  double* res_h;    // pinned mirror
+  DevState* st_d;
+  DevState* st_h;   // pinned
+  NdgState* ndg_d;
+  NdgState* ndg_h;  // pinned
+  double *red_d, *grow_d;
+  double *red_h, *grow_h;  // pinned
+  int64_t table_cap = 0;
+  bool kx_valid = false;
+  bool norms_ready = false;
+  double norm_q_sq = 0.0, norm_c_sq = 0.0;
+  int max_giant = 0;
+
+  cudaGraphExec_t chunk_exec = nullptr;
+  bool graph_tried = false;
+  bool graph_ok = false;
+  int64_t launches = 0;
+  bool profiling = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_chunk_ms = 0.0;
+  int64_t last_chunk_slots = 0;
+
+  std::vector<void*> owned;
+
+  template <class T>
+  T* alloc(size_t count) {
+    T* p = dalloc<T>(count);
+    owned.push_back(p);
+    return p;
+  }
+
+  double* cur_x() { return x[st_h->cur]; }
+  double* cur_y() { return y[st_h->cur]; }
+  double* slot_x(int which) {
+    switch (which) {
+      case FOLP_PT_CURRENT: return cur_x();
+      case FOLP_PT_AVERAGE: return avgp_x;
+      case FOLP_PT_LAST: return last_x;
+      case FOLP_PT_AUX: return aux_x;
+    }
+    throw std::invalid_argument("unknown point slot");
+  }
+  double* slot_y(int which) {
+    switch (which) {
+      case FOLP_PT_CURRENT: return cur_y();
+      case FOLP_PT_AVERAGE: return avgp_y;
+      case FOLP_PT_LAST: return last_y;
+      case FOLP_PT_AUX: return aux_y;
+    }
+    throw std::invalid_argument("unknown point slot");
+  }
+
+  int ew_grid(int64_t count, const void* fn) {
+    const int64_t need = (count + kBlock - 1) / kBlock;
+    const int64_t cap = static_cast<int64_t>(sms) * occupancy(fn);
+    return static_cast<int>(std::max<int64_t>(1, std::min(need, std::min<int64_t>(cap, kMaxGrid))));
+  }
+  int simple_grid(int64_t count) {
+    const int64_t need = (count + kBlock - 1) / kBlock;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, sms * 8)));
+  }
+  RedBuf red(int counter) { return RedBuf{partials, counters + counter}; }
+
+  template <int L, class Epi>
+  void seg_L(const PlanDev& p, const double* val, const Epi& epi, int counter) {
+    auto fn = segdot_kernel<L, Epi>;
+    const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(p.sp.total_tiles, std::min<int64_t>(cap, kMaxGrid))));
+    fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, red(counter));
+    ++launches;
+    CK(cudaGetLastError());
+  }
+
+  template <class Epi>
+  void seg(const PlanDev& p, const double* val, const Epi& epi, int counter) {
+    switch (p.L) {
+      case 1: seg_L<1>(p, val, epi, counter); break;
+      case 2: seg_L<2>(p, val, epi, counter); break;
+      case 4: seg_L<4>(p, val, epi, counter); break;
+      case 8: seg_L<8>(p, val, epi, counter); break;
+      case 16: seg_L<16>(p, val, epi, counter); break;
+      default: seg_L<32>(p, val, epi, counter); break;
+    }
+  }
+
+  template <class Op>
+  void ew(int64_t count, const Op& op, int counter) {
+    auto fn = elementwise_kernel<Op>;
+    const int grid = ew_grid(count, reinterpret_cast<const void*>(fn));
+    fn<<<grid, kBlock, 0, stream>>>(count, op, red(counter));
+    ++launches;
+    CK(cudaGetLastError());
+  }
+
+  void fetch_res(int count) {
+    CK(cudaMemcpyAsync(res_h, res, count * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+  void push_state() {
+    CK(cudaMemcpyAsync(st_d, st_h, sizeof(DevState), cudaMemcpyHostToDevice, stream));
+  }
+  void pull_state() {
+    CK(cudaMemcpyAsync(st_h, st_d, sizeof(DevState), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+  LoopBufs loop_bufs(cudaGraphConditionalHandle h, int use_cond) {
+    LoopBufs b{};
+    b.x[0] = x[0];
+    b.x[1] = x[1];
+    b.y[0] = y[0];
+    b.y[1] = y[1];
+    b.kx[0] = kx[0];
+    b.kx[1] = kx[1];
+    b.avg_x = avg_x;
+    b.avg_y = avg_y;
+    b.c = cw;
+    b.l = lw;
+    b.u = uw;
+    b.q = qw;
+    b.m1 = m1;
+    b.st = st_d;
+    b.red = red_d;
+    b.grow = grow_d;
+    b.cond = h;
+    b.use_cond = use_cond;
+    return b;
+  }
+
+  ~folp_gpu_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    if (chunk_exec) cudaGraphExecDestroy(chunk_exec);
+    for (void* p : owned) cudaFree(p);
+    for (void* p : rows.owned) cudaFree(p);
+    for (void* p : cols.owned) cudaFree(p);
+    if (res_h) cudaFreeHost(res_h);
+    if (st_h) cudaFreeHost(st_h);
+    if (ndg_h) cudaFreeHost(ndg_h);
+    if (red_h) cudaFreeHost(red_h);
+    if (grow_h) cudaFreeHost(grow_h);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// Work classes of one axis (see segdot.cuh).
+void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
+                const int* d_ptr, const int* d_idx, PlanDev& out) {
+  const double mean = S > 0 ? static_cast<double>(nnz) / static_cast<double>(S) : 0.0;
+  int L = 1;
+  while (L < 32 && 2.0 * L <= mean / 2.0) L *= 2;
+  const int bulk_max = std::max(8 * L, 8);
+  std::vector<int> long_ids, huge_ids, giant_ids, giant_first, part_giant, part_beg, part_end;
+  for (int64_t s = 0; s < S; ++s) {
+    const int64_t len = ptr[s + 1] - ptr[s];
+    if (len <= bulk_max) continue;
+    if (len <= kLongMax) {
+      long_ids.push_back(static_cast<int>(s));
+    } else if (len <= kHugeMax) {
+      huge_ids.push_back(static_cast<int>(s));
+    } else {
+      const int gi = static_cast<int>(giant_ids.size());
+      giant_ids.push_back(static_cast<int>(s));
+      giant_first.push_back(static_cast<int>(part_beg.size()));
+      for (int64_t b = ptr[s]; b < ptr[s + 1]; b += kGiantPart) {
+        part_giant.push_back(gi);
+        part_beg.push_back(static_cast<int>(b));
+        part_end.push_back(static_cast<int>(std::min<int64_t>(b + kGiantPart, ptr[s + 1])));
+      }
+    }
+  }
+  giant_first.push_back(static_cast<int>(part_beg.size()));
+  auto up = [&](const std::vector<int>& v) -> int* {
+    int* d = dalloc<int>(v.size());
+    out.owned.push_back(d);
+    if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    return d;
+  };
+  SegPlan& p = out.sp;
+  p.ptr = d_ptr;
+  p.idx = d_idx;
+  p.S = static_cast<int>(S);
+  p.bulk_max = bulk_max;
+  p.n_bulk_tiles = static_cast<int>((S + (kBlock / L) - 1) / (kBlock / L));
+  p.long_ids = up(long_ids);
+  p.n_long = static_cast<int>(long_ids.size());
+  p.n_long_tiles = (p.n_long + kWarps - 1) / kWarps;
+  p.huge_ids = up(huge_ids);
+  p.n_huge = static_cast<int>(huge_ids.size());
+  p.giant_ids = up(giant_ids);
+  p.giant_first = up(giant_first);
+  p.n_giant = static_cast<int>(giant_ids.size());
+  p.part_giant = up(part_giant);
+  p.part_beg = up(part_beg);
+  p.part_end = up(part_end);
+  p.n_parts = static_cast<int>(part_beg.size());
+  p.part_sums = dalloc<double>(part_beg.size());
+  out.owned.push_back(p.part_sums);
+  p.giant_arrivals = dalloc<unsigned>(giant_ids.size());
+  out.owned.push_back(p.giant_arrivals);
+  CK(cudaMemset(p.giant_arrivals, 0, std::max<size_t>(1, giant_ids.size()) * sizeof(unsigned)));
+  p.total_tiles = p.n_parts + p.n_huge + p.n_long_tiles + p.n_bulk_tiles;
+  out.L = L;
+  c->max_giant = std::max(c->max_giant, p.n_giant);
+}
+
+// Host-side CSR -> CSC (counting sort), columns in increasing row order
+// (sparse_matrix.cpp:82-102 layout).
+void transpose_host(int64_t m, int64_t n, const int64_t* rs, const int64_t* rc, const double* rv,
+                    std::vector<int64_t>& cs, std::vector<int64_t>& cr, std::vector<double>& cv) {
+  const int64_t nnz = rs[m];
+  cs.assign(static_cast<size_t>(n) + 1, 0);
+  cr.resize(static_cast<size_t>(nnz));
+  cv.resize(static_cast<size_t>(nnz));
+  for (int64_t k = 0; k < nnz; ++k) cs[rc[k] + 1]++;
+  for (int64_t j = 0; j < n; ++j) cs[j + 1] += cs[j];
+  std::vector<int64_t> cursor(cs.begin(), cs.end() - 1);
+  for (int64_t r = 0; r < m; ++r) {
+    for (int64_t k = rs[r]; k < rs[r + 1]; ++k) {
+      const int64_t slot = cursor[rc[k]]++;
+      cr[slot] = r;
+      cv[slot] = rv[k];
+    }
+  }
+}
+
+void upload_index(folp_gpu_ctx* c, const int64_t* src, int* dst, int64_t count, int64_t* stage,
+                  int64_t stage_cap) {
+  for (int64_t off = 0; off < count; off += stage_cap) {
+    const int64_t len = std::min(stage_cap, count - off);
+    CK(cudaMemcpyAsync(stage, src + off, len * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    k_narrow<<<c->simple_grid(len), kBlock, 0, c->stream>>>(stage, dst + off, len);
+    ++c->launches;
+    CK(cudaGetLastError());
+  }
+}
+
+void upload(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
+  if (count <= 0) return;
+  if (src == nullptr) {
+    CK(cudaMemsetAsync(dst, 0, count * sizeof(double), c->stream));
+  } else {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+}
+void download(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
+  if (count > 0 && dst != nullptr) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+}
+void copy_d2d(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
+  if (count > 0 && dst != src) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  }
+}
+
+int pick_device(int device) {
+  if (device >= 0) return device;
+  const char* env = std::getenv("FOLP_DEVICE");
+  return env ? std::atoi(env) : 0;
+}
+
+void set_device(folp_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+// K x of the CURRENT point into kx[cur] (after a start or a restart).
+void refresh_kx(folp_gpu_ctx* c) {
+  EpiStore e{c->cur_x(), c->kx[c->st_h->cur]};
+  c->seg(c->rows, c->csr_work, e, 0);
+  c->kx_valid = true;
+}
+
+// Product with the context matrix into device memory.
+void product(folp_gpu_ctx* c, bool transpose, bool working, const double* v, double* out) {
+  EpiStore e{v, out};
+  if (transpose) {
+    c->seg(c->cols, working ? c->csc_work : c->csc_orig, e, 1);
+  } else {
+    c->seg(c->rows, working ? c->csr_work : c->csr_orig, e, 1);
+  }
+}
+
+void zero_average(folp_gpu_ctx* c) {
+  if (c->n) CK(cudaMemsetAsync(c->avg_x, 0, c->n * sizeof(double), c->stream));
+  if (c->m) CK(cudaMemsetAsync(c->avg_y, 0, c->m * sizeof(double), c->stream));
+  c->st_h->avg_weight = 0.0;
+  c->st_h->pending = 0.0;
+}
+
+// Builds the chunk graph: WHILE(running) { kernel A ; kernel B }.
+void build_chunk_graph(folp_gpu_ctx* c) {
+  c->graph_tried = true;
+  if (std::getenv("FOLP_NO_GRAPH") != nullptr) return;
+  cudaGraph_t graph = nullptr;
+  if (cudaGraphCreate(&graph, 0) != cudaSuccess) return;
+  cudaGraphConditionalHandle handle;
+  bool ok = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault) ==
+            cudaSuccess;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t node;
+  if (ok) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    ok = cudaGraphAddNode(&node, graph, nullptr, 0, &cp) == cudaSuccess;
+  }
+  if (ok) {
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ok = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      const LoopBufs b = c->loop_bufs(handle, 1);
+      try {
+        c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2);
+        c->seg(c->rows, c->csr_work, EpiDual{b}, 3);
+        c->launches -= 2;
+      } catch (...) {
+        ok = false;
+      }
+      cudaGraph_t captured = nullptr;
+      ok = (cudaStreamEndCapture(c->stream, &captured) == cudaSuccess) && ok;
+    }
+  }
+  if (ok) ok = cudaGraphInstantiate(&c->chunk_exec, graph, 0) == cudaSuccess;
+  cudaGetLastError();  // clear a failed optional path
+  if (graph) cudaGraphDestroy(graph);
+  c->graph_ok = ok;
+  if (!ok && c->chunk_exec) {
+    cudaGraphExecDestroy(c->chunk_exec);
+    c->chunk_exec = nullptr;
+  }
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+const char* folp_gpu_last_error(void) { return g_err.c_str(); }
+
+int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (p->num_rows < 0 || p->num_cols < 0 || p->nnz < 0 ||
+        p->num_inequality_rows < 0 || p->num_inequality_rows > p->num_rows) {
+      throw EngineError(FOLP_E_DIMENSION_MISMATCH, "folp_gpu_create: bad dimensions");
+    }
+    if (p->nnz >= (int64_t(1) << 31) || p->num_rows >= (int64_t(1) << 31) ||
+        p->num_cols >= (int64_t(1) << 31)) {
+      throw EngineError(FOLP_E_INVALID_ARGUMENT, "folp_gpu_create: sizes exceed int32 indexing");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw EngineError(FOLP_E_NO_DEVICE, "folp_gpu_create: no CUDA device visible");
+    }
+    std::unique_ptr<folp_gpu_ctx> c(new folp_gpu_ctx());
+    c->device = pick_device(device);
+    set_device(c.get());
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    c->sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    const int64_t m = p->num_rows, n = p->num_cols, nnz = p->nnz;
+    c->m = m;
+    c->n = n;
+    c->m1 = p->num_inequality_rows;
+    c->nnz = nnz;
+    c->objective_constant = p->objective_constant;
+
+    std::vector<int64_t> cs, cr;
+    std::vector<double> cv;
+    const int64_t *col_start = p->col_start, *col_rows = p->col_rows;
+    const double* col_values = p->col_values;
+    if (col_start == nullptr || col_rows == nullptr || col_values == nullptr) {
+      transpose_host(m, n, p->row_start, p->row_cols, p->row_values, cs, cr, cv);
+      col_start = cs.data();
+      col_rows = cr.data();
+      col_values = cv.data();
+    }
+
+    c->csr_ptr = c->alloc<int>(m + 1);
+    c->csr_col = c->alloc<int>(nnz);
+    c->csc_ptr = c->alloc<int>(n + 1);
+    c->csc_row = c->alloc<int>(nnz);
+    c->csr_orig = c->alloc<double>(nnz);
+    c->csc_orig = c->alloc<double>(nnz);
+    c->csr_work = c->alloc<double>(nnz);
+    c->csc_work = c->alloc<double>(nnz);
+    {
+      const int64_t cap = std::min<int64_t>(std::max<int64_t>({m + 1, n + 1, nnz}), int64_t(1) << 26);
+      int64_t* stage = dalloc<int64_t>(cap);
+      try {
+        upload_index(c.get(), p->row_start, c->csr_ptr, m + 1, stage, cap);
+        upload_index(c.get(), p->row_cols, c->csr_col, nnz, stage, cap);
+        upload_index(c.get(), col_start, c->csc_ptr, n + 1, stage, cap);
+        upload_index(c.get(), col_rows, c->csc_row, nnz, stage, cap);
+        CK(cudaStreamSynchronize(c->stream));
+      } catch (...) {
+        cudaFree(stage);
+        throw;
+      }
+      cudaFree(stage);
+    }
+    upload(c.get(), c->csr_orig, p->row_values, nnz);
+    upload(c.get(), c->csc_orig, col_values, nnz);
+    copy_d2d(c.get(), c->csr_work, c->csr_orig, nnz);
+    copy_d2d(c.get(), c->csc_work, c->csc_orig, nnz);
+
+    build_plan(c.get(), p->row_start, m, nnz, c->csr_ptr, c->csr_col, c->rows);
+    build_plan(c.get(), col_start, n, nnz, c->csc_ptr, c->csc_row, c->cols);
+
+    auto vn = [&] { return c->alloc<double>(n); };
+    auto vm = [&] { return c->alloc<double>(m); };
+    c->c0 = vn(); c->l0 = vn(); c->u0 = vn(); c->q0 = vm();
+    c->cw = vn(); c->lw = vn(); c->uw = vn(); c->qw = vm();
+    c->d1 = vm(); c->d2 = vn();
+    c->x[0] = vn(); c->x[1] = vn();
+    c->y[0] = vm(); c->y[1] = vm();
+    c->kx[0] = vm(); c->kx[1] = vm();
+    c->avg_x = vn(); c->avg_y = vm();
+    c->avgp_x = vn(); c->avgp_y = vm();
+    c->last_x = vn(); c->last_y = vm();
+    c->aux_x = vn(); c->aux_y = vm();
+    c->kx_avg = vm(); c->kx_aux = vm();
+    c->xr = vn(); c->yr = vm();
+    c->g = c->alloc<double>(n + m);
+    c->lo = c->alloc<double>(n + m);
+    c->hi = vn();
+    c->partials = c->alloc<double>(static_cast<size_t>(kMaxGrid + c->max_giant + 8) * kMaxAcc);
+    c->counters = c->alloc<unsigned>(kCounters);
+    CK(cudaMemsetAsync(c->counters, 0, kCounters * sizeof(unsigned), c->stream));
+    c->res = c->alloc<double>(kResSlots);
+    CK(cudaMallocHost(&c->res_h, kResSlots * sizeof(double)));
+    c->st_d = c->alloc<DevState>(1);
+    CK(cudaMallocHost(&c->st_h, sizeof(DevState)));
+    std::memset(c->st_h, 0, sizeof(DevState));
+    c->ndg_d = c->alloc<NdgState>(1);
+    CK(cudaMallocHost(&c->ndg_h, sizeof(NdgState)));
+    c->table_cap = 4096;
+    c->red_d = c->alloc<double>(c->table_cap);
+    c->grow_d = c->alloc<double>(c->table_cap);
+    CK(cudaMallocHost(&c->red_h, c->table_cap * sizeof(double)));
+    CK(cudaMallocHost(&c->grow_h, c->table_cap * sizeof(double)));
+
+    upload(c.get(), c->c0, p->objective, n);
+    upload(c.get(), c->l0, p->variable_lower, n);
+    upload(c.get(), c->u0, p->variable_upper, n);
+    upload(c.get(), c->q0, p->right_hand_side, m);
+    // Identity scaling until folp_gpu_rescale: working problem = presolved.
+    copy_d2d(c.get(), c->cw, c->c0, n);
+    copy_d2d(c.get(), c->lw, c->l0, n);
+    copy_d2d(c.get(), c->uw, c->u0, n);
+    copy_d2d(c.get(), c->qw, c->q0, m);
+    k_fill<<<c->simple_grid(m), kBlock, 0, c->stream>>>(c->d1, m, 1.0);
+    k_fill<<<c->simple_grid(n), kBlock, 0, c->stream>>>(c->d2, n, 1.0);
+    c->launches += 2;
+    for (int i = 0; i < 2; ++i) {
+      if (n) CK(cudaMemsetAsync(c->x[i], 0, n * sizeof(double), c->stream));
+      if (m) CK(cudaMemsetAsync(c->y[i], 0, m * sizeof(double), c->stream));
+      if (m) CK(cudaMemsetAsync(c->kx[i], 0, m * sizeof(double), c->stream));
+    }
+    zero_average(c.get());
+    CK(cudaStreamSynchronize(c->stream));
+    *out = c.release();
+  });
+}
+
+void folp_gpu_destroy(folp_gpu_ctx* ctx) { delete ctx; }
+
+int folp_gpu_rescale(folp_gpu_ctx* c, int64_t ruiz_iterations, int32_t pock_chambolle,
+                     double alpha, double* row_scale, double* col_scale) {
+  return guarded([&] {
+    set_device(c);
+    const int64_t m = c->m, n = c->n, nnz = c->nnz;
+    double* cum1 = c->d1;
+    double* cum2 = c->d2;
+    k_fill<<<c->simple_grid(m), kBlock, 0, c->stream>>>(cum1, m, 1.0);
+    k_fill<<<c->simple_grid(n), kBlock, 0, c->stream>>>(cum2, n, 1.0);
+    c->launches += 2;
+    copy_d2d(c, c->csr_work, c->csr_orig, nnz);
+    copy_d2d(c, c->csc_work, c->csc_orig, nnz);
+    double* step1 = c->yr;  // scratch m
+    double* step2 = c->xr;  // scratch n
+    auto apply_step = [&] {
+      k_recip_sqrt_cum<<<c->simple_grid(m), kBlock, 0, c->stream>>>(step1, cum1, (int)m);
+      k_recip_sqrt_cum<<<c->simple_grid(n), kBlock, 0, c->stream>>>(step2, cum2, (int)n);
+      // working = working.scaled(step1, step2)   (scaling.cpp:57)
+      k_scale_values<<<c->simple_grid(m * 32), kBlock, 0, c->stream>>>(
+          c->csr_ptr, c->csr_col, c->csr_work, c->csr_work, (int)m, step1, step2);
+      k_scale_values<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(
+          c->csc_ptr, c->csc_row, c->csc_work, c->csc_work, (int)n, step2, step1);
+      c->launches += 4;
+      CK(cudaGetLastError());
+    };
+    for (int64_t it = 0; it < ruiz_iterations; ++it) {
+      // ruiz_step (scaling.cpp:32-36): inf-norms of the running matrix.
+      k_axis_absmax<<<c->simple_grid(m * 32), kBlock, 0, c->stream>>>(c->csr_ptr, c->csr_work,
+                                                                     (int)m, step1);
+      k_axis_absmax<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(c->csc_ptr, c->csc_work,
+                                                                     (int)n, step2);
+      c->launches += 2;
+      apply_step();
+    }
+    if (pock_chambolle) {
+      // pock_chambolle_step (scaling.cpp:38-46)
+      const double row_p = 2.0 - alpha;
+      k_axis_pnorm_seq<<<c->simple_grid(m), kBlock, 0, c->stream>>>(c->csr_ptr, c->csr_work,
+                                                                   (int)m, row_p, step1);
+      if (std::isinf(alpha)) {
+        k_axis_absmax<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(c->csc_ptr, c->csc_work,
+                                                                       (int)n, step2);
+      } else {
+        k_axis_pnorm_seq<<<c->simple_grid(n), kBlock, 0, c->stream>>>(c->csc_ptr, c->csc_work,
+                                                                     (int)n, alpha, step2);
+      }
+      c->launches += 2;
+      apply_step();
+    }
+    // K~ = K .scaled(D1, D2) from the original values in one shot (scaling.cpp:75-76)
+    k_scale_values<<<c->simple_grid(m * 32), kBlock, 0, c->stream>>>(
+        c->csr_ptr, c->csr_col, c->csr_orig, c->csr_work, (int)m, cum1, cum2);
+    k_scale_values<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(
+        c->csc_ptr, c->csc_row, c->csc_orig, c->csc_work, (int)n, cum2, cum1);
+    k_scale_vectors<<<c->simple_grid(n + m), kBlock, 0, c->stream>>>(
+        n, m, c->c0, c->l0, c->u0, c->q0, cum1, cum2, c->cw, c->lw, c->uw, c->qw);
+    c->launches += 3;
+    CK(cudaGetLastError());
+    download(c, row_scale, cum1, m);
+    download(c, col_scale, cum2, n);
+    CK(cudaStreamSynchronize(c->stream));
+    c->kx_valid = false;
+  });
+}
+
+int folp_gpu_working_stats(folp_gpu_ctx* c, double* max_abs_entry, double* norm_c,
+                           double* norm_q) {
+  return guarded([&] {
+    set_device(c);
+    k_absmax_all<<<1, kBlock, 0, c->stream>>>(c->csr_work, c->nnz, c->res + 0);
+    ++c->launches;
+    c->ew(c->n, OpNormSq{c->cw, c->res + 1}, 4);
+    c->ew(c->m, OpNormSq{c->qw, c->res + 2}, 5);
+    c->fetch_res(3);
+    if (max_abs_entry) *max_abs_entry = c->res_h[0];
+    if (norm_c) *norm_c = std::sqrt(c->res_h[1]);
+    if (norm_q) *norm_q = std::sqrt(c->res_h[2]);
+  });
+}
+
+int folp_gpu_get_working(folp_gpu_ctx* c, double* csr_values, double* csc_values,
+                         double* objective, double* rhs, double* lower, double* upper) {
+  return guarded([&] {
+    set_device(c);
+    download(c, csr_values, c->csr_work, c->nnz);
+    download(c, csc_values, c->csc_work, c->nnz);
+    download(c, objective, c->cw, c->n);
+    download(c, rhs, c->qw, c->m);
+    download(c, lower, c->lw, c->n);
+    download(c, upper, c->uw, c->n);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_set_start(folp_gpu_ctx* c, const double* x0, const double* y0) {
+  return guarded([&] {
+    set_device(c);
+    upload(c, c->aux_x, x0, c->n);
+    upload(c, c->aux_y, y0, c->m);
+    k_start_point<<<c->simple_grid(c->n + c->m), kBlock, 0, c->stream>>>(
+        c->n, c->m, c->m1, c->aux_x, c->aux_y, c->d1, c->d2, c->lw, c->uw, c->cur_x(),
+        c->cur_y(), c->last_x, c->last_y);
+    ++c->launches;
+    CK(cudaGetLastError());
+    zero_average(c);
+    refresh_kx(c);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_set_point(folp_gpu_ctx* c, int32_t which, const double* x, const double* y) {
+  return guarded([&] {
+    set_device(c);
+    upload(c, c->slot_x(which), x, c->n);
+    upload(c, c->slot_y(which), y, c->m);
+    if (which == FOLP_PT_CURRENT) refresh_kx(c);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_get_point(folp_gpu_ctx* c, int32_t which, double* x, double* y) {
+  return guarded([&] {
+    set_device(c);
+    download(c, x, c->slot_x(which), c->n);
+    download(c, y, c->slot_y(which), c->m);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_get_reduced_point(folp_gpu_ctx* c, int32_t which, double* x, double* y) {
+  return guarded([&] {
+    set_device(c);
+    k_reduced_point<<<c->simple_grid(c->n + c->m), kBlock, 0, c->stream>>>(
+        c->n, c->m, c->slot_x(which), c->slot_y(which), c->d1, c->d2, c->l0, c->u0, c->xr,
+        c->yr);
+    ++c->launches;
+    CK(cudaGetLastError());
+    download(c, x, c->xr, c->n);
+    download(c, y, c->yr, c->m);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_materialize_average(folp_gpu_ctx* c, double* weight) {
+  return guarded([&] {
+    set_device(c);
+    DevState* st = c->st_h;
+    OpAverage op{};
+    op.n = c->n;
+    op.m1 = c->m1;
+    op.x = c->cur_x();
+    op.y = c->cur_y();
+    op.ax = c->avg_x;
+    op.ay = c->avg_y;
+    op.l = c->lw;
+    op.u = c->uw;
+    op.pending = st->pending;
+    op.copy_current = st->avg_weight <= 0.0 ? 1 : 0;
+    op.inv = st->avg_weight > 0.0 ? 1.0 / st->avg_weight : 0.0;
+    op.out_x = c->avgp_x;
+    op.out_y = c->avgp_y;
+    c->ew(c->n + c->m, op, 6);
+    st->pending = 0.0;
+    c->push_state();
+    CK(cudaStreamSynchronize(c->stream));
+    if (weight) *weight = st->avg_weight;
+  });
+}
+
+int folp_gpu_evaluate(folp_gpu_ctx* c, int32_t which, int32_t raw, folp_gpu_eval* out) {
+  return guarded([&] {
+    set_device(c);
+    OpEvalPoint op{};
+    op.raw = raw != 0 ? 1 : 0;
+    op.n = c->n;
+    op.m = c->m;
+    op.xs = c->slot_x(which);
+    op.ys = c->slot_y(which);
+    op.d1 = c->d1;
+    op.d2 = c->d2;
+    op.l = c->l0;
+    op.u = c->u0;
+    op.c = c->c0;
+    op.q = c->q0;
+    op.xr = c->xr;
+    op.yr = c->yr;
+    op.result = c->res + 8;
+    c->ew(c->n + c->m, op, 7);
+    c->seg(c->rows, c->csr_orig, EpiPrimalResidual{c->xr, c->q0, c->m1, c->res + 11}, 8);
+    c->seg(c->cols, c->csc_orig, EpiDualResidual{c->yr, c->c0, c->l0, c->u0, c->res + 12}, 9);
+    if (!c->norms_ready) {
+      c->ew(c->m, OpNormSq{c->q0, c->res + 15}, 10);
+      c->ew(c->n, OpNormSq{c->c0, c->res + 16}, 11);
+    }
+    c->fetch_res(c->norms_ready ? 15 : 17);
+    if (!c->norms_ready) {
+      c->norm_q_sq = c->res_h[15];
+      c->norm_c_sq = c->res_h[16];
+      c->norms_ready = true;
+    }
+    const double* r = c->res_h;
+    out->c_dot_x = r[8];
+    out->q_dot_y = r[9];
+    out->nonfinite = r[10] != 0.0 ? 1 : 0;
+    out->primal_sq = r[11];
+    out->dual_sq = r[12];
+    out->bound_terms = r[13];
+    out->infinite_product = r[14] != 0.0 ? 1 : 0;
+    out->norm_q = std::sqrt(c->norm_q_sq);
+    out->norm_c = std::sqrt(c->norm_c_sq);
+  });
+}
+
+int folp_gpu_distance(folp_gpu_ctx* c, int32_t a, int32_t b, double* sx, double* sy) {
+  return guarded([&] {
+    set_device(c);
+    OpDistance op{c->n, c->slot_x(a), c->slot_x(b), c->slot_y(a), c->slot_y(b), c->res + 20};
+    c->ew(c->n + c->m, op, 12);
+    c->fetch_res(22);
+    *sx = c->res_h[20];
+    *sy = c->res_h[21];
+  });
+}
+
+int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, double* gap) {
+  return guarded([&] {
+    set_device(c);
+    if (!(radius > 0.0)) {
+      throw EngineError(FOLP_E_NONPOSITIVE_RADIUS, "normalized_duality_gap: radius must be > 0");
+    }
+    if (!(omega > 0.0)) {
+      throw EngineError(FOLP_E_NONPOSITIVE_WEIGHT, "normalized_duality_gap: omega must be > 0");
+    }
+    const int64_t n = c->n, m = c->m;
+    double* px = c->slot_x(which);
+    double* py = c->slot_y(which);
+    // g, lo, hi over the primal coordinates (K~'y)
+    EpiNdgPrimal ep{py, px, c->cw, c->lw, c->uw, omega, c->g, c->lo, c->hi, c->res + 24};
+    c->seg(c->cols, c->csc_work, ep, 13);
+    // ... and the dual ones (K~x; cached for CURRENT)
+    EpiNdgDual ed{};
+    ed.x = px;
+    ed.y = py;
+    ed.q = c->qw;
+    ed.m1 = c->m1;
+    ed.winv = 1.0 / omega;
+    ed.g = c->g + n;
+    ed.lo = c->lo + n;
+    ed.result = c->res + 29;
+    if (which == FOLP_PT_CURRENT && c->kx_valid) {
+      ed.kx_out = nullptr;
+      c->ew(m, OpNdgDualCached{c->kx[c->st_h->cur], ed}, 14);
+    } else {
+      ed.kx_out = which == FOLP_PT_AVERAGE ? c->kx_avg : c->kx_aux;
+      c->seg(c->rows, c->csr_work, ed, 14);
+    }
+    c->fetch_res(34);
+    const double* r = c->res_h;
+    const double any = r[24] + r[29];
+    if (any == 0.0) {
+      *gap = 0.0;  // solver.cpp:324
+      return;
+    }
+    const double gsq = r[25] + r[30];
+    const bool bounded = (r[26] + r[31]) == 0.0;
+    if (bounded) {
+      const double norm_sq = r[27] + r[32];
+      if (std::sqrt(norm_sq) <= radius * (1.0 + 1e-12)) {
+        *gap = (r[28] + r[33]) / radius;  // solver.cpp:339-341
+        return;
+      }
+    }
+    // bisection on nu (solver.cpp:356-368), 4 levels per pass
+    NdgState* h = c->ndg_h;
+    std::memset(h, 0, sizeof(NdgState));
+    h->nu_lo = 0.0;
+    h->nu_hi = std::sqrt(gsq) / radius;
+    h->radius = radius;
+    CK(cudaMemcpyAsync(c->ndg_d, h, sizeof(NdgState), cudaMemcpyHostToDevice, c->stream));
+    OpNdgPass pass{};
+    pass.n = n;
+    pass.total = n + m;
+    pass.g = c->g;
+    pass.lo = c->lo;
+    pass.hi = c->hi;
+    pass.omega = omega;
+    pass.winv = 1.0 / omega;
+    pass.ns = c->ndg_d;
+    int batch = 12;  // 48 levels before the first look
+    for (int round = 0; round < 64; ++round) {
+      for (int i = 0; i < batch; ++i) c->ew(n + m, pass, 15);
+      CK(cudaMemcpyAsync(h, c->ndg_d, sizeof(NdgState), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (h->done) break;
+      batch = 4;
+    }
+    if (!h->done) throw EngineError(FOLP_E_RUNTIME, "normalized_duality_gap: bisection stalled");
+    *gap = h->result;
+  });
+}
+
+int folp_gpu_restart_to(folp_gpu_ctx* c, int32_t which, int32_t reset_average) {
+  return guarded([&] {
+    set_device(c);
+    DevState* st = c->st_h;
+    if (which != FOLP_PT_CURRENT) {
+      copy_d2d(c, c->cur_x(), c->slot_x(which), c->n);
+      copy_d2d(c, c->cur_y(), c->slot_y(which), c->m);
+      if (which == FOLP_PT_AVERAGE) {
+        copy_d2d(c, c->kx[st->cur], c->kx_avg, c->m);
+        c->kx_valid = true;
+      } else {
+        refresh_kx(c);
+      }
+    }
+    copy_d2d(c, c->last_x, c->cur_x(), c->n);
+    copy_d2d(c, c->last_y, c->cur_y(), c->m);
+    if (reset_average) zero_average(c);
+    c->push_state();
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_mark_last(folp_gpu_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    copy_d2d(c, c->last_x, c->cur_x(), c->n);
+    copy_d2d(c, c->last_y, c->cur_y(), c->m);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
+  return guarded([&] {
+    set_device(c);
+    if (loop->target < 1) throw std::invalid_argument("run_chunk: target must be >= 1");
+    if (loop->policy != FOLP_STEP_ADAPTIVE && loop->policy != FOLP_STEP_CONSTANT) {
+      throw std::invalid_argument("run_chunk: policy not handled by the fused loop");
+    }
+    if (!c->kx_valid) refresh_kx(c);
+    if (loop->target > c->table_cap) {
+      throw std::invalid_argument("run_chunk: target above the factor-table capacity");
+    }
+    if (loop->policy == FOLP_STEP_ADAPTIVE) {
+      std::memcpy(c->red_h, loop->reduction, loop->target * sizeof(double));
+      std::memcpy(c->grow_h, loop->growth, loop->target * sizeof(double));
+      CK(cudaMemcpyAsync(c->red_d, c->red_h, loop->target * sizeof(double),
+                         cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->grow_d, c->grow_h, loop->target * sizeof(double),
+                         cudaMemcpyHostToDevice, c->stream));
+    }
+    DevState* st = c->st_h;
+    st->running = 1;
+    st->status = kRunning;
+    st->policy = loop->policy;
+    st->target = loop->target;
+    st->accepted = 0;
+    st->k_total = loop->k_total;
+    st->k_chunk0 = loop->k_total;
+    st->t_inner = loop->t_inner;
+    st->trials_iter = 0;
+    st->step_trials = loop->step_trials;
+    st->violations = loop->violations;
+    st->ledger_k = loop->ledger_k;
+    st->ledger_kt = loop->ledger_kt;
+    st->iteration_limit = loop->iteration_limit;
+    st->kkt_pass_limit = loop->kkt_pass_limit;
+    st->omega = loop->omega;
+    st->eta = loop->eta;
+    st->eta_hat = loop->eta;
+    st->slots = 0;
+    c->push_state();
+    if (!c->graph_tried) build_chunk_graph(c);
+    if (c->profiling) CK(cudaEventRecord(c->ev0, c->stream));
+    if (c->graph_ok) {
+      CK(cudaGraphLaunch(c->chunk_exec, c->stream));
+      c->launches += 2 * 1;  // refined below from the slot count
+    } else {
+      // Plain stream launches: enough slots for the target plus a few
+      // retries, then look at the state and continue if needed.
+      const LoopBufs b = c->loop_bufs(cudaGraphConditionalHandle{}, 0);
+      int64_t remaining = loop->target;
+      for (;;) {
+        for (int64_t s = 0; s < remaining + 2; ++s) {
+          c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2);
+          c->seg(c->rows, c->csr_work, EpiDual{b}, 3);
+        }
+        CK(cudaMemcpyAsync(st, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (!st->running) break;
+        remaining = st->target - st->accepted;
+      }
+    }
+    if (c->profiling) CK(cudaEventRecord(c->ev1, c->stream));
+    c->pull_state();
+    if (c->graph_ok) c->launches += 2 * st->slots - 2;
+    if (c->profiling) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+      c->last_chunk_ms = ms;
+      c->last_chunk_slots = st->slots;
+    }
+    loop->status = st->status;
+    loop->accepted = st->accepted;
+    loop->k_total = st->k_total;
+    loop->t_inner = st->t_inner;
+    loop->step_trials = st->step_trials;
+    loop->violations = st->violations;
+    loop->ledger_k = st->ledger_k;
+    loop->ledger_kt = st->ledger_kt;
+    loop->eta = st->policy == FOLP_STEP_ADAPTIVE ? st->eta_hat : loop->eta;
+    loop->last_eta_used = st->last_eta_used;
+    loop->avg_weight = st->avg_weight;
+    loop->last_movement = st->movement;
+    loop->last_cross = st->cross;
+    loop->slots = st->slots;
+  });
+}
+
+int folp_gpu_spectral_norm(folp_gpu_ctx* c, const double* v0, double relative_tol,
+                           int64_t max_iterations, double* norm, int64_t* multiplies) {
+  return guarded([&] {
+    set_device(c);
+    double* v = c->aux_x;
+    double* w = c->aux_y;
+    double* s = c->xr;
+    upload(c, v, v0, c->n);
+    double lambda = 0.0;
+    for (int64_t it = 0; it < max_iterations; ++it) {
+      product(c, false, true, v, w);
+      EpiStoreDotNorm e{w, v, s, c->res + 40};
+      c->seg(c->cols, c->csc_work, e, 1);
+      if (multiplies) *multiplies += 2;
+      c->fetch_res(42);
+      const double next = c->res_h[40];
+      const double snorm = std::sqrt(c->res_h[41]);
+      if (snorm == 0.0) {
+        *norm = 0.0;
+        return;
+      }
+      k_div_scalar<<<c->simple_grid(c->n), kBlock, 0, c->stream>>>(v, s, c->n, c->res + 41);
+      ++c->launches;
+      const bool converged = it > 0 && std::fabs(next - lambda) <= relative_tol * std::fabs(next);
+      lambda = next;
+      if (converged) break;
+    }
+    *norm = std::sqrt(std::max(lambda, 0.0));
+  });
+}
+
+int folp_gpu_multiply(folp_gpu_ctx* c, int32_t working, const double* xh, double* out) {
+  return guarded([&] {
+    set_device(c);
+    upload(c, c->aux_x, xh, c->n);
+    product(c, false, working != 0, c->aux_x, c->kx_aux);
+    download(c, out, c->kx_aux, c->m);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_multiply_transpose(folp_gpu_ctx* c, int32_t working, const double* yh, double* out) {
+  return guarded([&] {
+    set_device(c);
+    upload(c, c->aux_y, yh, c->m);
+    product(c, true, working != 0, c->aux_y, c->xr);
+    download(c, out, c->xr, c->n);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_all_finite(folp_gpu_ctx* c, int32_t which, int32_t* finite) {
+  return guarded([&] {
+    set_device(c);
+    c->ew(c->n + c->m, OpCountNonFinite{c->n, c->slot_x(which), c->slot_y(which), c->res + 44}, 4);
+    c->fetch_res(45);
+    *finite = c->res_h[44] == 0.0 ? 1 : 0;
+  });
+}
+
+int folp_gpu_axis_norms(folp_gpu_ctx* c, int32_t axis, double p, int32_t working, double* out) {
+  return guarded([&] {
+    set_device(c);
+    const bool rows = axis == 0;
+    const int S = static_cast<int>(rows ? c->m : c->n);
+    const int* ptr = rows ? c->csr_ptr : c->csc_ptr;
+    const double* val = rows ? (working ? c->csr_work : c->csr_orig)
+                             : (working ? c->csc_work : c->csc_orig);
+    double* dst = rows ? c->yr : c->xr;
+    if (std::isinf(p)) {
+      k_axis_absmax<<<c->simple_grid(static_cast<int64_t>(S) * 32), kBlock, 0, c->stream>>>(
+          ptr, val, S, dst);
+    } else {
+      k_axis_pnorm_seq<<<c->simple_grid(S), kBlock, 0, c->stream>>>(ptr, val, S, p, dst);
+    }
+    ++c->launches;
+    CK(cudaGetLastError());
+    download(c, out, dst, S);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int folp_gpu_max_abs_entry(folp_gpu_ctx* c, int32_t working, double* out) {
+  return guarded([&] {
+    set_device(c);
+    k_absmax_all<<<1, kBlock, 0, c->stream>>>(working ? c->csr_work : c->csr_orig, c->nnz,
+                                              c->res + 46);
+    ++c->launches;
+    c->fetch_res(47);
+    *out = c->res_h[46];
+  });
+}
+
+int64_t folp_gpu_launch_count(const folp_gpu_ctx* c) { return c->launches; }
+
+int folp_gpu_set_profiling(folp_gpu_ctx* c, int32_t enabled) {
+  c->profiling = enabled != 0;
+  return FOLP_OK;
+}
+
+int folp_gpu_chunk_timing(folp_gpu_ctx* c, double* chunk_ms, int64_t* slots) {
+  if (chunk_ms) *chunk_ms = c->last_chunk_ms;
+  if (slots) *slots = c->last_chunk_slots;
+  return FOLP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,324 @@
+// capi.cpp -- include/folp_c.h on top of the C++ folp API.
+//
+// Exceptions never cross this boundary: each entry maps the folp exception
+// type to its FOLP_E_* code and keeps the message for folp_last_error().
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "device.hpp"
+#include "folp/lp_model.hpp"
+#include "folp/scaling.hpp"
+#include "folp/solver.hpp"
+#include "folp/termination.hpp"
+#include "folp_c.h"
+#include "sparse_access.hpp"
+
+namespace {
+
+using namespace folp;
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return FOLP_OK;
+  } catch (const DimensionMismatch& e) {
+    g_err = e.what();
+    return FOLP_E_DIMENSION_MISMATCH;
+  } catch (const EmptyMatrix& e) {
+    g_err = e.what();
+    return FOLP_E_EMPTY_MATRIX;
+  } catch (const UnsupportedNorm& e) {
+    g_err = e.what();
+    return FOLP_E_UNSUPPORTED_NORM;
+  } catch (const NonPositiveWeight& e) {
+    g_err = e.what();
+    return FOLP_E_NONPOSITIVE_WEIGHT;
+  } catch (const NonPositiveRadius& e) {
+    g_err = e.what();
+    return FOLP_E_NONPOSITIVE_RADIUS;
+  } catch (const StepSizeUnderflow& e) {
+    g_err = e.what();
+    return FOLP_E_STEP_UNDERFLOW;
+  } catch (const NonFiniteIterate& e) {
+    g_err = e.what();
+    return FOLP_E_NONFINITE;
+  } catch (const InfiniteProduct& e) {
+    g_err = e.what();
+    return FOLP_E_INFINITE_PRODUCT;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return FOLP_E_INVALID_ARGUMENT;
+  } catch (const DeviceError& e) {
+    g_err = e.what();
+    return std::strstr(e.what(), "no CUDA device") ? FOLP_E_NO_DEVICE : FOLP_E_CUDA;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return FOLP_E_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FOLP_E_RUNTIME;
+  }
+}
+
+// Fast ingestion when the CSR is already canonical (strictly increasing
+// columns, in range, finite nonzero values): that is exactly the matrix
+// from_triplets would build, so the O(nnz log nnz) sort is skipped.
+SparseMatrix matrix_from_csr(const folp_lp_c* in) {
+  const int64_t m = in->num_rows, n = in->num_cols, nnz = in->nnz;
+  if (m < 0 || n < 0 || nnz < 0 || in->row_start == nullptr || in->row_start[0] != 0 ||
+      in->row_start[m] != nnz) {
+    throw DimensionMismatch("folp_lp_c: inconsistent row_start");
+  }
+  bool canonical = true;
+  for (int64_t r = 0; r < m && canonical; ++r) {
+    const int64_t b = in->row_start[r], e = in->row_start[r + 1];
+    if (e < b) throw DimensionMismatch("folp_lp_c: decreasing row_start");
+    for (int64_t k = b; k < e; ++k) {
+      const int64_t c = in->row_cols[k];
+      const double v = in->row_values[k];
+      if (c < 0 || c >= n || v == 0.0 || !std::isfinite(v) || (k > b && c <= in->row_cols[k - 1])) {
+        canonical = false;
+        break;
+      }
+    }
+  }
+  if (canonical) {
+    std::vector<Index> start(in->row_start, in->row_start + m + 1);
+    std::vector<Index> cols(in->row_cols, in->row_cols + nnz);
+    std::vector<double> vals(in->row_values, in->row_values + nnz);
+    return SparseMatrixAccess::build(m, n, std::move(start), std::move(cols), std::move(vals));
+  }
+  std::vector<Triplet> t;
+  t.reserve(static_cast<std::size_t>(nnz));
+  for (int64_t r = 0; r < m; ++r) {
+    for (int64_t k = in->row_start[r]; k < in->row_start[r + 1]; ++k) {
+      t.push_back({r, in->row_cols[k], in->row_values[k]});
+    }
+  }
+  return SparseMatrix::from_triplets(m, n, t);
+}
+
+LinearProgram to_lp(const folp_lp_c* in) {
+  LinearProgram lp;
+  lp.constraint_matrix = matrix_from_csr(in);
+  const std::size_t n = static_cast<std::size_t>(in->num_cols);
+  const std::size_t m = static_cast<std::size_t>(in->num_rows);
+  lp.objective.assign(in->objective, in->objective + n);
+  lp.right_hand_side.assign(in->right_hand_side, in->right_hand_side + m);
+  lp.variable_lower.assign(in->variable_lower, in->variable_lower + n);
+  lp.variable_upper.assign(in->variable_upper, in->variable_upper + n);
+  lp.num_inequality_rows = in->num_inequality_rows;
+  lp.objective_constant = in->objective_constant;
+  return lp;
+}
+
+SolverParams to_params(const folp_params_c* p) {
+  SolverParams s;
+  s.eps_optimal = p->eps_optimal;
+  s.beta_sufficient = p->beta_sufficient;
+  s.beta_necessary = p->beta_necessary;
+  s.beta_artificial = p->beta_artificial;
+  s.restart_scheme = static_cast<RestartSchemeKind>(p->restart_scheme);
+  s.step_policy = static_cast<StepPolicy>(p->step_policy);
+  s.theta_smoothing = p->theta_smoothing;
+  s.eps_zero = p->eps_zero;
+  s.mp_breaking_factor = p->mp_breaking_factor;
+  s.mp_downscaling_factor = p->mp_downscaling_factor;
+  s.mp_interpolation_coefficient = p->mp_interpolation_coefficient;
+  s.evaluation_cadence = p->evaluation_cadence;
+  s.kkt_pass_limit = p->kkt_pass_limit;
+  s.iteration_limit = p->iteration_limit;
+  s.time_limit_seconds = p->time_limit_seconds;
+  s.ruiz_iterations = p->ruiz_iterations;
+  s.use_pock_chambolle = p->use_pock_chambolle != 0;
+  s.pc_alpha = p->pc_alpha;
+  s.scale_invariant_initial_primal_weight = p->scale_invariant_initial_primal_weight != 0;
+  s.use_presolve = p->use_presolve != 0;
+  s.verbosity = p->verbosity;
+  s.log_stream = nullptr;
+  s.record_iterate_trace = p->record_iterate_trace != 0;
+  return s;
+}
+
+folp_info_c to_info(const ConvergenceInfo& i) {
+  return folp_info_c{i.primal_objective,   i.dual_objective,     i.gap_abs,
+                     i.primal_residual_norm, i.dual_residual_norm, i.norm_q,
+                     i.norm_c};
+}
+
+void put(const std::vector<double>& v, double* out) {
+  if (out != nullptr && !v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(double));
+}
+
+PrimalDualPoint point(const folp_lp_c* lp, const double* x, const double* y) {
+  PrimalDualPoint z;
+  z.primal.assign(x, x + lp->num_cols);
+  z.dual.assign(y, y + lp->num_rows);
+  return z;
+}
+
+}  // namespace
+
+extern "C" {
+
+void folp_params_default(folp_params_c* p) {
+  const SolverParams s;
+  std::memset(p, 0, sizeof(*p));
+  p->eps_optimal = s.eps_optimal;
+  p->beta_sufficient = s.beta_sufficient;
+  p->beta_necessary = s.beta_necessary;
+  p->beta_artificial = s.beta_artificial;
+  p->restart_scheme = static_cast<int32_t>(s.restart_scheme);
+  p->step_policy = static_cast<int32_t>(s.step_policy);
+  p->theta_smoothing = s.theta_smoothing;
+  p->eps_zero = s.eps_zero;
+  p->mp_breaking_factor = s.mp_breaking_factor;
+  p->mp_downscaling_factor = s.mp_downscaling_factor;
+  p->mp_interpolation_coefficient = s.mp_interpolation_coefficient;
+  p->evaluation_cadence = s.evaluation_cadence;
+  p->kkt_pass_limit = s.kkt_pass_limit;
+  p->iteration_limit = s.iteration_limit;
+  p->time_limit_seconds = s.time_limit_seconds;
+  p->ruiz_iterations = s.ruiz_iterations;
+  p->use_pock_chambolle = s.use_pock_chambolle ? 1 : 0;
+  p->pc_alpha = s.pc_alpha;
+  p->scale_invariant_initial_primal_weight = s.scale_invariant_initial_primal_weight ? 1 : 0;
+  p->use_presolve = s.use_presolve ? 1 : 0;
+}
+
+int folp_solve(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
+               const double* y0, folp_result_c* out) {
+  return guarded([&] {
+    const LinearProgram lp = to_lp(lp_in);
+    const SolverParams params = to_params(p);
+    PrimalDualPoint z0;
+    z0.primal.assign(static_cast<std::size_t>(lp_in->num_cols), 0.0);
+    z0.dual.assign(static_cast<std::size_t>(lp_in->num_rows), 0.0);
+    if (x0 != nullptr) z0.primal.assign(x0, x0 + lp_in->num_cols);
+    if (y0 != nullptr) z0.dual.assign(y0, y0 + lp_in->num_rows);
+    const SolveResult r = solve(lp, params, z0);
+    put(r.primal_solution, out->primal_solution);
+    put(r.dual_solution, out->dual_solution);
+    put(r.reduced_costs, out->reduced_costs);
+    out->termination_reason = static_cast<int32_t>(r.termination_reason);
+    out->final_info = to_info(r.final_info);
+    out->iterations = r.iterations;
+    out->kkt_passes = r.kkt_passes;
+    out->wall_seconds = r.wall_seconds;
+    out->restarts = r.restarts;
+    out->step_trials = r.step_trials;
+    out->step_condition_violations = r.step_condition_violations;
+    out->num_restart_iterations = static_cast<int64_t>(r.restart_iterations.size());
+    for (int64_t i = 0; i < out->num_restart_iterations && i < out->restart_capacity; ++i) {
+      out->restart_iterations[i] = r.restart_iterations[i];
+    }
+    out->num_trace = static_cast<int64_t>(r.trace.size());
+    for (int64_t i = 0; i < out->num_trace && i < out->trace_capacity; ++i) {
+      const TraceEntry& e = r.trace[static_cast<std::size_t>(i)];
+      if (out->trace_iteration) out->trace_iteration[i] = e.iteration;
+      if (out->trace_kkt_passes) out->trace_kkt_passes[i] = e.kkt_passes;
+      if (out->trace_current) out->trace_current[i] = to_info(e.current);
+      if (out->trace_average) out->trace_average[i] = to_info(e.average);
+    }
+    out->num_iterates = static_cast<int64_t>(r.iterate_trace.size());
+    out->iterate_n = r.iterate_trace.empty()
+                         ? 0
+                         : static_cast<int64_t>(r.iterate_trace[0].point.primal.size());
+    out->iterate_m = r.iterate_trace.empty()
+                         ? 0
+                         : static_cast<int64_t>(r.iterate_trace[0].point.dual.size());
+    for (int64_t i = 0; i < out->num_iterates && i < out->iterate_capacity; ++i) {
+      const IterateRecord& rec = r.iterate_trace[static_cast<std::size_t>(i)];
+      if (out->iterate_iteration) out->iterate_iteration[i] = rec.iteration;
+      if (out->iterate_eta) out->iterate_eta[i] = rec.eta_used;
+      if (out->iterate_primal) put(rec.point.primal, out->iterate_primal + i * out->iterate_n);
+      if (out->iterate_dual) put(rec.point.dual, out->iterate_dual + i * out->iterate_m);
+    }
+  });
+}
+
+int folp_multiply(const folp_lp_c* lp_in, const double* x, double* out) {
+  return guarded([&] {
+    const SparseMatrix k = matrix_from_csr(lp_in);
+    k.multiply(std::span<const double>(x, static_cast<std::size_t>(lp_in->num_cols)),
+               std::span<double>(out, static_cast<std::size_t>(lp_in->num_rows)));
+  });
+}
+
+int folp_multiply_transpose(const folp_lp_c* lp_in, const double* y, double* out) {
+  return guarded([&] {
+    const SparseMatrix k = matrix_from_csr(lp_in);
+    k.multiply_transpose(std::span<const double>(y, static_cast<std::size_t>(lp_in->num_rows)),
+                         std::span<double>(out, static_cast<std::size_t>(lp_in->num_cols)));
+  });
+}
+
+int folp_rescale(const folp_lp_c* lp_in, int64_t ruiz_iterations, int32_t apply_pc,
+                 double alpha, double* row_scale, double* col_scale, double* scaled_values,
+                 double* scaled_objective, double* scaled_rhs, double* scaled_lower,
+                 double* scaled_upper) {
+  return guarded([&] {
+    const LinearProgram lp = to_lp(lp_in);
+    const ScaledProblem s = rescale_problem(lp, ruiz_iterations, apply_pc != 0, alpha);
+    put(s.scaling.row_scale, row_scale);
+    put(s.scaling.col_scale, col_scale);
+    if (scaled_values != nullptr) {
+      const auto v = s.lp.constraint_matrix.row_values();
+      if (!v.empty()) std::memcpy(scaled_values, v.data(), v.size() * sizeof(double));
+    }
+    put(s.lp.objective, scaled_objective);
+    put(s.lp.right_hand_side, scaled_rhs);
+    put(s.lp.variable_lower, scaled_lower);
+    put(s.lp.variable_upper, scaled_upper);
+  });
+}
+
+int folp_convergence_info(const folp_lp_c* lp_in, const double* x, const double* y,
+                          folp_info_c* info) {
+  return guarded([&] {
+    const LinearProgram lp = to_lp(lp_in);
+    *info = to_info(convergence_info(
+        lp, std::span<const double>(x, static_cast<std::size_t>(lp_in->num_cols)),
+        std::span<const double>(y, static_cast<std::size_t>(lp_in->num_rows))));
+  });
+}
+
+int folp_normalized_duality_gap(const folp_lp_c* lp_in, const double* x, const double* y,
+                                double radius, double omega, double* gap) {
+  return guarded([&] {
+    const LinearProgram lp = to_lp(lp_in);
+    *gap = normalized_duality_gap(lp, point(lp_in, x, y), radius, omega);
+  });
+}
+
+int folp_adaptive_step(const folp_lp_c* lp_in, const double* x, const double* y, double omega,
+                       double eta_hat, int64_t k, double* x_next, double* y_next,
+                       double* eta_used, double* eta_hat_next, int64_t* trials,
+                       double* movement_sq, double* cross_term) {
+  return guarded([&] {
+    const LinearProgram lp = to_lp(lp_in);
+    const AdaptiveStepResult r = adaptive_step(lp, point(lp_in, x, y), omega, eta_hat, k);
+    put(r.next.primal, x_next);
+    put(r.next.dual, y_next);
+    *eta_used = r.eta_used;
+    *eta_hat_next = r.eta_hat_next;
+    *trials = r.trials;
+    *movement_sq = r.movement_sq;
+    *cross_term = r.cross_term;
+  });
+}
+
+const char* folp_last_error(void) { return g_err.c_str(); }
+
+const char* folp_engine_info(void) {
+  return "folp B200 engine: sm_100a (compute_100a), fp64 segmented-dot kernels, "
+         "conditional-graph PDHG chunks";
+}
+
+}  // extern "C"
