@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- PDHG iterations/s of the B200 PDLP loop (BASELINE.json metric).
+
+Workload: BASELINE.json configs[1] (config 2): seeded synthetic LP, m=200,000
+(half >= rows), n=400,000, power-law column degrees (~3.5M nonzeros), fp64.
+A step = one evaluation period of the reference's loop
+(SolverParams::evaluation_cadence = 40 accepted PDHG iterations, then the
+evaluation / restart check), run on device through the resumable folp solve
+session (include/folp_c.h folp_session_*).
+
+  value      : PDHG iterations/s over K timed steps (CUDA events on the engine
+               stream, LP resident in HBM), summed over ranks / max time
+  e2e        : the same metric through folp_solve() on host arrays (C ABI):
+               upload, rescaling, loop, download inside the timed region
+  roofline   : fused step kernels (K'y+primal step, Kx'+dual step) --
+               algorithmic bytes per trial slot 24*nnz + 68*(m+n)
+                over their CUDA-event time, vs measured HBM peak
+  cpu_baseline: the compiled reference (oracle/_ref) on 1 host core
+
+``--impl reference`` times the reference CPU solver (oracle/_ref, compiled
+from the reference sources) on all host cores: one independent solve per core,
+aggregate iterations/s.  Multi-GPU (torchrun): independent replicas of the
+config per rank ("replicas only" for config 2).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "PDHG iters/s"
+UNIT = "iter/s"
+CADENCE = 40
+
+
+def bytes_per_trial(m: int, n: int, nnz: int) -> int:
+    """Algorithmic HBM bytes of one trial slot (kernel A + kernel B), fp64 values,
+    int32 indices/pointers, every vector touched once."""
+    return 24 * nnz + 68 * (m + n)
+
+
+def measured_peak() -> tuple[float, str]:
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[2:]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    os.environ["FOLP_DEVICE"] = str(local)
+    return world, rank, local
+
+
+def allreduce_max(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reference_loop_rate(lp, iters_small: int, iters_big: int, threads: int = 1):
+    """Reference CPU solver iterations/s from two runs with different iteration
+    limits (setup cancels out).  `threads` independent solves run concurrently
+    (ctypes releases the GIL); returns aggregate iterations/s."""
+    from oracle import ref
+    from paper_2106_04756_b200 import cabi
+
+    b = ref.binding()
+
+    def run(limit: int, out: list, i: int):
+        t = time.perf_counter()
+        r = b.solve_lp(lp, cabi.params(iteration_limit=limit), trace_capacity=1)
+        out[i] = (time.perf_counter() - t, r.iterations)
+
+    def batch(limit: int):
+        out = [None] * threads
+        ts = [threading.Thread(target=run, args=(limit, out, i)) for i in range(threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return out
+
+    small = batch(iters_small)
+    big = batch(iters_big)
+    rates = []
+    for (ts_, is_), (tb, ib) in zip(small, big):
+        rates.append((ib - is_) / max(1e-9, tb - ts_))
+    return float(sum(rates)), small, big
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_2106_04756_b200 import instances
+
+    lp = instances.generate(args.config, args.seed, 1.0)
+    threads = args.ref_threads or (os.cpu_count() or 1)
+    w_iters = CADENCE * max(1, args.warmup)
+    k_iters = CADENCE * args.steps
+    rate, small, big = reference_loop_rate(lp, w_iters, w_iters + k_iters, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * CADENCE * threads / rate if rate > 0 else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE.json configs[1])",
+        "config": config_block(lp, args),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{threads} independent reference solves of the workload, "
+                                   f"{k_iters} PDHG iterations each, timed as the difference "
+                                   f"of {w_iters + k_iters}- and {w_iters}-iteration runs"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(lp, args) -> dict:
+    from paper_2106_04756_b200 import instances
+
+    working_mb = (24 * lp.nnz * 2 + 8 * 16 * (lp.num_rows + lp.num_cols)) / 1e6
+    return {"workload": instances.CONFIG_NAMES[args.config], "config_index": args.config - 1,
+            "m": lp.num_rows, "m_inequality": lp.num_inequality_rows, "n": lp.num_cols,
+            "nnz": lp.nnz, "seed": args.seed, "evaluation_cadence": CADENCE,
+            "step": f"{CADENCE} accepted PDHG iterations + evaluation/restart check",
+            "l2": f"resident working set ~{working_mb:.0f} MB (K~ CSR+CSC, original values, "
+                  f"iterate vectors) > 126 MB L2; no flush",
+            "parallelism": "replicas" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single"}
+
+
+def run_b200(args, world, rank, local):
+    from paper_2106_04756_b200 import cabi, engine, instances
+
+    eng = engine()
+    lp = instances.generate(args.config, args.seed, 1.0)
+    m, n, nnz = lp.num_rows, lp.num_cols, lp.nnz
+    p = cabi.params(eps_optimal=args.eps)
+
+    # ---- device-resident loop: W untimed + K timed evaluation periods ----
+    sess = eng.session(lp, p)
+    if args.warmup:
+        sess.advance(args.warmup)
+    s0 = sess.stats()
+    barrier(world)
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            step_ms.append(sess.advance(1))
+            if sess.finished:
+                break
+    s1 = sess.stats()
+    finished_early = sess.finished
+    sess.close()
+    total_ms = float(sum(step_ms))
+    iters = s1["iterations"] - s0["iterations"]
+    max_ms = allreduce_max(total_ms, world)
+    value = iters * world / (max_ms / 1000.0)
+    slots = s1["loop_slots"] - s0["loop_slots"]
+    loop_ms = s1["loop_ms"] - s0["loop_ms"]
+    launches = s1["launches"] - s0["launches"]
+    b_trial = bytes_per_trial(m, n, nnz)
+    achieved = b_trial * slots / (loop_ms / 1000.0) / 1e9 if loop_ms > 0 else 0.0
+    peak, peak_src = measured_peak()
+
+    # ---- end to end: folp_solve() on host arrays, transfers inside --------
+    e2e_iters = CADENCE * args.steps
+    t = time.perf_counter()
+    r = eng.solve_lp(lp, cabi.params(eps_optimal=args.eps, iteration_limit=e2e_iters),
+                     trace_capacity=1)
+    e2e_s = time.perf_counter() - t
+    e2e_s = allreduce_max(e2e_s, world)
+    # CSR+CSC pointers and int64 indices + values, c/l/u/q, start point
+    h2d = 8 * (m + n + 2) + 32 * nnz + 8 * (3 * n + m) + 8 * (n + m)
+    d2h = 8 * (n + m) + 8 * n
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": len(step_ms), "warmup": args.warmup,
+        "ms_per_step": max_ms / max(1, len(step_ms)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE.json configs[1])",
+        "config": config_block(lp, args),
+        "iterations_timed": iters, "trial_slots_timed": slots,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "segdot_kernel<EpiPrimal> + segdot_kernel<EpiDual> (one trial)",
+                     "bytes_per_launch_pair": b_trial,
+                     "kernel_ms_per_trial": loop_ms / max(1, slots), "peak_source": peak_src},
+        "e2e": {"value": e2e_iters * world / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
+                "seconds": e2e_s, "iterations": r.iterations,
+                "termination": r.termination_reason},
+        "clocks": clocks.summary(),
+    }
+    if finished_early:
+        line["note"] = "solve converged inside the timed region; fewer steps timed"
+
+    if rank == 0 and world == 1 and not args.skip_cpu_baseline:
+        rate, small, big = reference_loop_rate(lp, CADENCE, 3 * CADENCE, 1)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"oracle/_ref (reference compiled from its sources), 1 thread, same LP: "
+                      f"{2 * CADENCE} PDHG iterations timed as the difference of "
+                      f"{3 * CADENCE}- and {CADENCE}-iteration solves "
+                      f"({big[0][0]:.1f}s - {small[0][0]:.1f}s)"}
+    if args.time_to_tol and rank == 0:
+        t = time.perf_counter()
+        r = eng.solve_lp(lp, cabi.params(eps_optimal=1e-8, time_limit_seconds=args.time_to_tol),
+                         trace_capacity=1)
+        line["time_to_1e-8"] = {"seconds": time.perf_counter() - t,
+                                "termination": r.termination_reason,
+                                "iterations": r.iterations, "kkt_passes": r.kkt_passes,
+                                "restarts": r.restarts}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--eps", type=float, default=1e-8)
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--time-to-tol", type=float, default=120.0,
+                    help="also solve to 1e-8 with this time limit (s); 0 disables")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_b200(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -190,6 +190,26 @@ int folp_adaptive_step(const folp_lp_c* lp, const double* x, const double* y,
                        double* eta_hat_next, int64_t* trials,
                        double* movement_sq, double* cross_term);
 
+/* ---- resumable solve session (B200 engine only) ----------------------
+ * folp_solve split into evaluation periods: create runs validate, presolve,
+ * rescaling and the start evaluation; each advance runs `evaluations`
+ * periods of evaluation_cadence PDHG iterations plus the evaluation /
+ * restart step.  Running it to the end gives exactly folp_solve's result.
+ * The timed variant brackets the work with CUDA events on the engine
+ * stream and returns the device time. */
+typedef struct folp_session folp_session;
+int folp_session_create(const folp_lp_c* lp, const folp_params_c* params,
+                        const double* x0, const double* y0,
+                        folp_session** out);
+int folp_session_advance(folp_session* s, int64_t evaluations,
+                         int32_t* finished, double* device_ms);
+/* iterations so far; summed device time and trial slots of the fused step
+ * kernels (profiling is on for sessions); kernel launches so far. */
+int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms,
+                       int64_t* loop_slots, int64_t* launches);
+int folp_session_result(folp_session* s, folp_result_c* out);
+void folp_session_destroy(folp_session* s);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* folp_last_error(void);
 

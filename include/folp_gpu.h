@@ -204,11 +204,17 @@ int folp_gpu_multiply_transpose(folp_gpu_ctx* ctx, int32_t working,
 /* Kernel launches issued by this context so far (for bench accounting). */
 int64_t folp_gpu_launch_count(const folp_gpu_ctx* ctx);
 
-/* Timing of the two fused step kernels inside the last chunk (ms),
- * measured with CUDA events on the context stream when enabled. */
+/* Device time of the fused step kernels (kernel A + kernel B of every trial
+ * slot) summed over all chunks since profiling was (re)enabled, measured
+ * with CUDA events on the context stream around each chunk graph. */
 int folp_gpu_set_profiling(folp_gpu_ctx* ctx, int32_t enabled);
 int folp_gpu_chunk_timing(folp_gpu_ctx* ctx, double* chunk_ms,
                           int64_t* slots);
+
+/* Wall time of a stretch of stream work, measured with CUDA events on the
+ * context stream (start records, stop records + synchronizes). */
+int folp_gpu_timer_start(folp_gpu_ctx* ctx);
+int folp_gpu_timer_stop(folp_gpu_ctx* ctx, double* ms);
 
 const char* folp_gpu_last_error(void);
 

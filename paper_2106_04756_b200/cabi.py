@@ -220,6 +220,14 @@ class Binding:
                                       C.c_int64, _f64p, _f64p, _f64p, _f64p, _i64p, _f64p,
                                       _f64p])
         f("last_error", C.c_char_p, [])
+        if hasattr(lib, prefix + "session_create"):
+            f("session_create", C.c_int, [C.POINTER(LpC), C.POINTER(ParamsC), _f64p, _f64p,
+                                           C.POINTER(C.c_void_p)])
+            f("session_advance", C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
+                                            _f64p])
+            f("session_stats", C.c_int, [C.c_void_p, _i64p, _f64p, _i64p, _i64p])
+            f("session_result", C.c_int, [C.c_void_p, C.POINTER(ResultC)])
+            f("session_destroy", None, [C.c_void_p])
 
     def _fn(self, name, restype, argtypes):
         fn = getattr(self.lib, self.prefix + name)
@@ -289,6 +297,9 @@ class Binding:
                                                         trace_capacity)]],
             trace=trace, iterate_trace=iters)
 
+    def session(self, lp: LP, p: Optional[dict] = None) -> "Session":
+        return Session(self, lp, p or params())
+
     def kx(self, lp: LP, x) -> np.ndarray:
         lpc = lp.to_c()
         x = np.ascontiguousarray(x, dtype=np.float64)
@@ -345,3 +356,51 @@ class Binding:
                                       C.byref(tr), C.byref(mv), C.byref(cr)))
         return dict(x=xn, y=yn, eta_used=eu.value, eta_hat_next=en.value, trials=tr.value,
                     movement_sq=mv.value, cross_term=cr.value)
+
+
+class Session:
+    """A resumable folp::solve (folp_session_*): advance() runs whole
+    evaluation periods and returns their device time (CUDA events on the
+    engine stream)."""
+
+    def __init__(self, b: Binding, lp: LP, p: dict):
+        self.b = b
+        self._lpc = lp.to_c()  # keeps the arrays alive
+        self._pc = params_to_c(p)
+        h = C.c_void_p()
+        b.check(b.session_create(C.byref(self._lpc), C.byref(self._pc), None, None,
+                                 C.byref(h)))
+        self.h = h
+        self.finished = False
+
+    def advance(self, evaluations: int = 1) -> float:
+        fin = C.c_int32()
+        ms = C.c_double()
+        self.b.check(self.b.session_advance(self.h, evaluations, C.byref(fin), C.byref(ms)))
+        self.finished = bool(fin.value)
+        return ms.value
+
+    def stats(self) -> dict:
+        it, slots, launches = C.c_int64(), C.c_int64(), C.c_int64()
+        ms = C.c_double()
+        self.b.check(self.b.session_stats(self.h, C.byref(it), C.byref(ms), C.byref(slots),
+                                          C.byref(launches)))
+        return dict(iterations=it.value, loop_ms=ms.value, loop_slots=slots.value,
+                    launches=launches.value)
+
+    def close(self) -> None:
+        if self.h:
+            self.b.session_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

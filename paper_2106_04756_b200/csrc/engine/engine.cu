@@ -334,9 +334,9 @@ struct folp_gpu_ctx {
   bool graph_ok = false;
   int64_t launches = 0;
   bool profiling = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  double last_chunk_ms = 0.0;
-  int64_t last_chunk_slots = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
+  double chunk_ms_total = 0.0;
+  int64_t chunk_slots_total = 0;
 
   std::vector<void*> owned;
 
@@ -458,6 +458,8 @@ struct folp_gpu_ctx {
     if (grow_h) cudaFreeHost(grow_h);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (tev0) cudaEventDestroy(tev0);
+    if (tev1) cudaEventDestroy(tev1);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -684,6 +686,8 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
+    CK(cudaEventCreate(&c->tev0));
+    CK(cudaEventCreate(&c->tev1));
     const int64_t m = p->num_rows, n = p->num_cols, nnz = p->nnz;
     c->m = m;
     c->n = n;
@@ -1190,8 +1194,8 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     if (c->profiling) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-      c->last_chunk_ms = ms;
-      c->last_chunk_slots = st->slots;
+      c->chunk_ms_total += ms;
+      c->chunk_slots_total += st->slots;
     }
     loop->status = st->status;
     loop->accepted = st->accepted;
@@ -1307,13 +1311,33 @@ int64_t folp_gpu_launch_count(const folp_gpu_ctx* c) { return c->launches; }
 
 int folp_gpu_set_profiling(folp_gpu_ctx* c, int32_t enabled) {
   c->profiling = enabled != 0;
+  c->chunk_ms_total = 0.0;
+  c->chunk_slots_total = 0;
   return FOLP_OK;
 }
 
 int folp_gpu_chunk_timing(folp_gpu_ctx* c, double* chunk_ms, int64_t* slots) {
-  if (chunk_ms) *chunk_ms = c->last_chunk_ms;
-  if (slots) *slots = c->last_chunk_slots;
+  if (chunk_ms) *chunk_ms = c->chunk_ms_total;
+  if (slots) *slots = c->chunk_slots_total;
   return FOLP_OK;
+}
+
+int folp_gpu_timer_start(folp_gpu_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    CK(cudaEventRecord(c->tev0, c->stream));
+  });
+}
+
+int folp_gpu_timer_stop(folp_gpu_ctx* c, double* ms) {
+  return guarded([&] {
+    set_device(c);
+    CK(cudaEventRecord(c->tev1, c->stream));
+    CK(cudaEventSynchronize(c->tev1));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+    *ms = f;
+  });
 }
 
 }  // extern "C"

@@ -3,6 +3,7 @@
 // Exceptions never cross this boundary: each entry maps the folp exception
 // type to its FOLP_E_* code and keeps the message for folp_last_error().
 #include <cmath>
+#include <memory>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -13,6 +14,7 @@
 #include "folp/solver.hpp"
 #include "folp/termination.hpp"
 #include "folp_c.h"
+#include "session.hpp"
 #include "sparse_access.hpp"
 
 namespace {
@@ -163,7 +165,51 @@ PrimalDualPoint point(const folp_lp_c* lp, const double* x, const double* y) {
   return z;
 }
 
+void export_result(const SolveResult& r, folp_result_c* out) {
+  put(r.primal_solution, out->primal_solution);
+  put(r.dual_solution, out->dual_solution);
+  put(r.reduced_costs, out->reduced_costs);
+  out->termination_reason = static_cast<int32_t>(r.termination_reason);
+  out->final_info = to_info(r.final_info);
+  out->iterations = r.iterations;
+  out->kkt_passes = r.kkt_passes;
+  out->wall_seconds = r.wall_seconds;
+  out->restarts = r.restarts;
+  out->step_trials = r.step_trials;
+  out->step_condition_violations = r.step_condition_violations;
+  out->num_restart_iterations = static_cast<int64_t>(r.restart_iterations.size());
+  for (int64_t i = 0; i < out->num_restart_iterations && i < out->restart_capacity; ++i) {
+    out->restart_iterations[i] = r.restart_iterations[i];
+  }
+  out->num_trace = static_cast<int64_t>(r.trace.size());
+  for (int64_t i = 0; i < out->num_trace && i < out->trace_capacity; ++i) {
+    const TraceEntry& e = r.trace[static_cast<std::size_t>(i)];
+    if (out->trace_iteration) out->trace_iteration[i] = e.iteration;
+    if (out->trace_kkt_passes) out->trace_kkt_passes[i] = e.kkt_passes;
+    if (out->trace_current) out->trace_current[i] = to_info(e.current);
+    if (out->trace_average) out->trace_average[i] = to_info(e.average);
+  }
+  out->num_iterates = static_cast<int64_t>(r.iterate_trace.size());
+  out->iterate_n = r.iterate_trace.empty()
+                       ? 0
+                       : static_cast<int64_t>(r.iterate_trace[0].point.primal.size());
+  out->iterate_m = r.iterate_trace.empty()
+                       ? 0
+                       : static_cast<int64_t>(r.iterate_trace[0].point.dual.size());
+  for (int64_t i = 0; i < out->num_iterates && i < out->iterate_capacity; ++i) {
+    const IterateRecord& rec = r.iterate_trace[static_cast<std::size_t>(i)];
+    if (out->iterate_iteration) out->iterate_iteration[i] = rec.iteration;
+    if (out->iterate_eta) out->iterate_eta[i] = rec.eta_used;
+    if (out->iterate_primal) put(rec.point.primal, out->iterate_primal + i * out->iterate_n);
+    if (out->iterate_dual) put(rec.point.dual, out->iterate_dual + i * out->iterate_m);
+  }
+}
+
 }  // namespace
+
+struct folp_session {
+  std::unique_ptr<folp::SolveSession> s;
+};
 
 extern "C" {
 
@@ -202,44 +248,7 @@ int folp_solve(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
     z0.dual.assign(static_cast<std::size_t>(lp_in->num_rows), 0.0);
     if (x0 != nullptr) z0.primal.assign(x0, x0 + lp_in->num_cols);
     if (y0 != nullptr) z0.dual.assign(y0, y0 + lp_in->num_rows);
-    const SolveResult r = solve(lp, params, z0);
-    put(r.primal_solution, out->primal_solution);
-    put(r.dual_solution, out->dual_solution);
-    put(r.reduced_costs, out->reduced_costs);
-    out->termination_reason = static_cast<int32_t>(r.termination_reason);
-    out->final_info = to_info(r.final_info);
-    out->iterations = r.iterations;
-    out->kkt_passes = r.kkt_passes;
-    out->wall_seconds = r.wall_seconds;
-    out->restarts = r.restarts;
-    out->step_trials = r.step_trials;
-    out->step_condition_violations = r.step_condition_violations;
-    out->num_restart_iterations = static_cast<int64_t>(r.restart_iterations.size());
-    for (int64_t i = 0; i < out->num_restart_iterations && i < out->restart_capacity; ++i) {
-      out->restart_iterations[i] = r.restart_iterations[i];
-    }
-    out->num_trace = static_cast<int64_t>(r.trace.size());
-    for (int64_t i = 0; i < out->num_trace && i < out->trace_capacity; ++i) {
-      const TraceEntry& e = r.trace[static_cast<std::size_t>(i)];
-      if (out->trace_iteration) out->trace_iteration[i] = e.iteration;
-      if (out->trace_kkt_passes) out->trace_kkt_passes[i] = e.kkt_passes;
-      if (out->trace_current) out->trace_current[i] = to_info(e.current);
-      if (out->trace_average) out->trace_average[i] = to_info(e.average);
-    }
-    out->num_iterates = static_cast<int64_t>(r.iterate_trace.size());
-    out->iterate_n = r.iterate_trace.empty()
-                         ? 0
-                         : static_cast<int64_t>(r.iterate_trace[0].point.primal.size());
-    out->iterate_m = r.iterate_trace.empty()
-                         ? 0
-                         : static_cast<int64_t>(r.iterate_trace[0].point.dual.size());
-    for (int64_t i = 0; i < out->num_iterates && i < out->iterate_capacity; ++i) {
-      const IterateRecord& rec = r.iterate_trace[static_cast<std::size_t>(i)];
-      if (out->iterate_iteration) out->iterate_iteration[i] = rec.iteration;
-      if (out->iterate_eta) out->iterate_eta[i] = rec.eta_used;
-      if (out->iterate_primal) put(rec.point.primal, out->iterate_primal + i * out->iterate_n);
-      if (out->iterate_dual) put(rec.point.dual, out->iterate_dual + i * out->iterate_m);
-    }
+    export_result(solve(lp, params, z0), out);
   });
 }
 
@@ -313,6 +322,57 @@ int folp_adaptive_step(const folp_lp_c* lp_in, const double* x, const double* y,
     *cross_term = r.cross_term;
   });
 }
+
+int folp_session_create(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
+                        const double* y0, folp_session** out) {
+  *out = nullptr;
+  return guarded([&] {
+    PrimalDualPoint z0;
+    z0.primal.assign(static_cast<std::size_t>(lp_in->num_cols), 0.0);
+    z0.dual.assign(static_cast<std::size_t>(lp_in->num_rows), 0.0);
+    if (x0 != nullptr) z0.primal.assign(x0, x0 + lp_in->num_cols);
+    if (y0 != nullptr) z0.dual.assign(y0, y0 + lp_in->num_rows);
+    auto sess = std::make_unique<folp_session>();
+    sess->s = std::make_unique<SolveSession>(to_lp(lp_in), to_params(p), std::move(z0));
+    if (folp_gpu_ctx* c = sess->s->context()) folp_gpu_set_profiling(c, 1);
+    *out = sess.release();
+  });
+}
+
+int folp_session_advance(folp_session* s, int64_t evaluations, int32_t* finished,
+                         double* device_ms) {
+  return guarded([&] {
+    folp_gpu_ctx* c = s->s->context();
+    if (c != nullptr && device_ms != nullptr) device::check(folp_gpu_timer_start(c), "timer");
+    const bool done = s->s->advance(evaluations);
+    if (c != nullptr && device_ms != nullptr) device::check(folp_gpu_timer_stop(c, device_ms), "timer");
+    if (finished) *finished = done ? 1 : 0;
+  });
+}
+
+int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms, int64_t* loop_slots,
+                       int64_t* launches) {
+  return guarded([&] {
+    if (iterations) *iterations = s->s->iterations();
+    folp_gpu_ctx* c = s->s->context();
+    double ms = 0.0;
+    int64_t slots = 0;
+    if (c != nullptr) folp_gpu_chunk_timing(c, &ms, &slots);
+    if (loop_ms) *loop_ms = ms;
+    if (loop_slots) *loop_slots = slots;
+    if (launches) *launches = c ? folp_gpu_launch_count(c) : 0;
+  });
+}
+
+int folp_session_result(folp_session* s, folp_result_c* out) {
+  return guarded([&] {
+    const SolveResult* r = s->s->result();
+    if (r == nullptr) throw std::invalid_argument("folp_session_result: session not finished");
+    export_result(*r, out);
+  });
+}
+
+void folp_session_destroy(folp_session* s) { delete s; }
 
 const char* folp_last_error(void) { return g_err.c_str(); }
 

@@ -1,0 +1,31 @@
+// session.hpp -- a folp::solve that can be advanced one evaluation period
+// at a time (used by the C ABI folp_session_* and by bench.py to time the
+// loop with CUDA events on the engine stream).  run-to-completion equals
+// folp::solve exactly.
+#pragma once
+
+#include <memory>
+
+#include "folp/solver.hpp"
+#include "folp_gpu.h"
+
+namespace folp {
+
+class SolveSession {
+ public:
+  SolveSession(LinearProgram lp, const SolverParams& params, PrimalDualPoint z0);
+  ~SolveSession();
+  // Advances by up to `evaluations` evaluation periods (evaluation_cadence
+  // iterations + the evaluation/restart step each); true once finished.
+  bool advance(Index evaluations);
+  bool finished() const;
+  Index iterations() const;
+  folp_gpu_ctx* context() const;       // nullptr when no device loop ran
+  const SolveResult* result() const;   // set once finished
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace folp

@@ -19,6 +19,7 @@
 #include <random>
 
 #include "device.hpp"
+#include "session.hpp"
 #include "folp/linalg.hpp"
 #include "folp/presolve.hpp"
 #include "folp/scaling.hpp"
@@ -91,6 +92,13 @@ class Driver {
       : raw_(raw), p_(params), z0_(z0), start_(Clock::now()) {}
 
   SolveResult run();
+  // Everything before the loop (solver.cpp:818-907); a value when the solve
+  // already ended (detected, trivial, optimal start).
+  std::optional<SolveResult> start();
+  // Runs the loop for at most `evaluations` evaluation periods.
+  std::optional<SolveResult> advance(Index evaluations);
+  folp_gpu_ctx* context() const { return dev_ ? dev_->get() : nullptr; }
+  Index iterations() const { return k_total_; }
 
  private:
   using Clock = std::chrono::steady_clock;
@@ -346,6 +354,11 @@ bool Driver::evaluate_and_maybe_restart(SolveResult& out) {
 }
 
 SolveResult Driver::run() {  // solver.cpp:818-946
+  if (auto done = start()) return std::move(*done);
+  return std::move(*advance(std::numeric_limits<Index>::max()));
+}
+
+std::optional<SolveResult> Driver::start() {
   check_params(p_);
   if (p_.restart_scheme == RestartSchemeKind::kTheory) {
     p_.beta_sufficient = 0.37;
@@ -432,9 +445,13 @@ SolveResult Driver::run() {  // solver.cpp:818-946
       return finish(TerminationReason::kOptimal, FOLP_PT_CURRENT, info0);
     }
   }
+  return std::nullopt;
+}
 
+std::optional<SolveResult> Driver::advance(Index evaluations) {
   const Index cadence = p_.evaluation_cadence;
-  for (;;) {
+  for (Index evals = 0;;) {
+    if (evals >= evaluations) return std::nullopt;
     if (k_total_ >= p_.iteration_limit) return finish_limit(TerminationReason::kIterationLimit);
     if (kkt_passes(ledger_) >= p_.kkt_pass_limit) {
       return finish_limit(TerminationReason::kKktPassLimit);
@@ -480,6 +497,7 @@ SolveResult Driver::run() {  // solver.cpp:818-946
     }
     if (loop.status == FOLP_CHUNK_DONE && t_inner_ % cadence == 0) {
       SolveResult out;
+      ++evals;
       try {
         if (evaluate_and_maybe_restart(out)) return out;
       } catch (const NonFiniteIterate&) {
@@ -665,6 +683,35 @@ double update_primal_weight(const PrimalDualPoint& z_new, const PrimalDualPoint&
 SolveResult solve(const LinearProgram& lp_raw, const SolverParams& params,
                   const PrimalDualPoint& z0) {
   return Driver(lp_raw, params, z0).run();
+}
+
+// ---- resumable session (include/folp_c.h folp_session_*) -------------
+struct SolveSession::Impl {
+  LinearProgram lp;
+  SolverParams params;
+  PrimalDualPoint z0;
+  std::unique_ptr<Driver> driver;
+  std::optional<SolveResult> result;
+};
+
+SolveSession::SolveSession(LinearProgram lp, const SolverParams& params, PrimalDualPoint z0)
+    : impl_(new Impl{std::move(lp), params, std::move(z0), nullptr, std::nullopt}) {
+  impl_->driver = std::make_unique<Driver>(impl_->lp, impl_->params, impl_->z0);
+  impl_->result = impl_->driver->start();
+}
+
+SolveSession::~SolveSession() = default;
+
+bool SolveSession::advance(Index evaluations) {
+  if (!impl_->result) impl_->result = impl_->driver->advance(evaluations);
+  return impl_->result.has_value();
+}
+
+bool SolveSession::finished() const { return impl_->result.has_value(); }
+Index SolveSession::iterations() const { return impl_->driver->iterations(); }
+folp_gpu_ctx* SolveSession::context() const { return impl_->driver->context(); }
+const SolveResult* SolveSession::result() const {
+  return impl_->result ? &*impl_->result : nullptr;
 }
 
 SolveResult solve(const LinearProgram& lp_raw, const SolverParams& params) {
