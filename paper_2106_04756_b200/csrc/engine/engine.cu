@@ -23,6 +23,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -269,19 +270,21 @@ struct OpNormSq {
 // ---------------------------------------------------------------------
 struct PlanDev {
   SegPlan sp{};
-  int L = 1;
   std::vector<void*> owned;
 };
 
 std::mutex g_occ_mu;
 std::unordered_map<const void*, int> g_occ;
 
-int occupancy(const void* fn) {
+int occupancy(const void* fn, int smem = 0) {
   std::lock_guard<std::mutex> lk(g_occ_mu);
   auto it = g_occ.find(fn);
   if (it != g_occ.end()) return it->second;
+  if (smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
   int b = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, smem));
   if (b < 1) b = 1;
   g_occ[fn] = b;
   return b;
@@ -379,27 +382,16 @@ struct folp_gpu_ctx {
   }
   RedBuf red(int counter) { return RedBuf{partials, counters + counter}; }
 
-  template <int L, class Epi>
-  void seg_L(const PlanDev& p, const double* val, const Epi& epi, int counter) {
-    auto fn = segdot_kernel<L, Epi>;
+  template <class Epi>
+  void seg(const PlanDev& p, const double* val, const Epi& epi, int counter) {
+    auto fn = segdot_kernel<Epi>;
     const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
-    const int grid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(p.sp.total_tiles, std::min<int64_t>(cap, kMaxGrid))));
+    const int64_t need = (static_cast<int64_t>(p.sp.n_units) + kWarps - 1) / kWarps;
+    const int grid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
     fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, red(counter));
     ++launches;
     CK(cudaGetLastError());
-  }
-
-  template <class Epi>
-  void seg(const PlanDev& p, const double* val, const Epi& epi, int counter) {
-    switch (p.L) {
-      case 1: seg_L<1>(p, val, epi, counter); break;
-      case 2: seg_L<2>(p, val, epi, counter); break;
-      case 4: seg_L<4>(p, val, epi, counter); break;
-      case 8: seg_L<8>(p, val, epi, counter); break;
-      case 16: seg_L<16>(p, val, epi, counter); break;
-      default: seg_L<32>(p, val, epi, counter); break;
-    }
   }
 
   template <class Op>
@@ -466,65 +458,65 @@ struct folp_gpu_ctx {
 
 namespace {
 
-// Work classes of one axis (see segdot.cuh).
+// Warp units of one axis (see segdot.cuh): tiles of consecutive short
+// segments (<= kWarpTile nonzeros, <= 256 segments each) and fixed parts of
+// the longer ones, in index order.
 void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
                 const int* d_ptr, const int* d_idx, PlanDev& out) {
-  const double mean = S > 0 ? static_cast<double>(nnz) / static_cast<double>(S) : 0.0;
-  int L = 1;
-  while (L < 32 && 2.0 * L <= mean / 2.0) L *= 2;
-  const int bulk_max = std::max(8 * L, 8);
-  std::vector<int> long_ids, huge_ids, giant_ids, giant_first, part_giant, part_beg, part_end;
+  (void)nnz;
+  std::vector<int4> units;
+  std::vector<int> multi_seg, multi_parts;
+  int64_t seg0 = -1, tile_nnz = 0;
+  auto close = [&](int64_t seg_end) {
+    if (seg0 >= 0 && seg_end > seg0) {
+      units.push_back(make_int4(static_cast<int>(seg0), static_cast<int>(seg_end),
+                                static_cast<int>(ptr[seg0]), static_cast<int>(ptr[seg_end])));
+    }
+    seg0 = -1;
+    tile_nnz = 0;
+  };
   for (int64_t s = 0; s < S; ++s) {
     const int64_t len = ptr[s + 1] - ptr[s];
-    if (len <= bulk_max) continue;
-    if (len <= kLongMax) {
-      long_ids.push_back(static_cast<int>(s));
-    } else if (len <= kHugeMax) {
-      huge_ids.push_back(static_cast<int>(s));
-    } else {
-      const int gi = static_cast<int>(giant_ids.size());
-      giant_ids.push_back(static_cast<int>(s));
-      giant_first.push_back(static_cast<int>(part_beg.size()));
-      for (int64_t b = ptr[s]; b < ptr[s + 1]; b += kGiantPart) {
-        part_giant.push_back(gi);
-        part_beg.push_back(static_cast<int>(b));
-        part_end.push_back(static_cast<int>(std::min<int64_t>(b + kGiantPart, ptr[s + 1])));
-      }
+    if (len <= kWarpTile) {
+      if (seg0 >= 0 && (tile_nnz + len > kWarpTile || s - seg0 >= kWarpTile)) close(s);
+      if (seg0 < 0) seg0 = s;
+      tile_nnz += len;
+      continue;
     }
+    close(s);
+    const int multi = static_cast<int>(multi_seg.size());
+    const int64_t part = len > kGiantMin ? kGiantPart : kWarpTile;
+    const int first = static_cast<int>(units.size());
+    for (int64_t b = ptr[s]; b < ptr[s + 1]; b += part) {
+      units.push_back(make_int4(-(multi + 1), first, static_cast<int>(b),
+                                static_cast<int>(std::min<int64_t>(b + part, ptr[s + 1]))));
+    }
+    multi_seg.push_back(static_cast<int>(s));
+    multi_parts.push_back(static_cast<int>(units.size()) - first);
   }
-  giant_first.push_back(static_cast<int>(part_beg.size()));
-  auto up = [&](const std::vector<int>& v) -> int* {
-    int* d = dalloc<int>(v.size());
+  close(S);
+  auto up = [&](const auto& v) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    T* d = dalloc<T>(v.size());
     out.owned.push_back(d);
-    if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
     return d;
   };
   SegPlan& p = out.sp;
   p.ptr = d_ptr;
   p.idx = d_idx;
   p.S = static_cast<int>(S);
-  p.bulk_max = bulk_max;
-  p.n_bulk_tiles = static_cast<int>((S + (kBlock / L) - 1) / (kBlock / L));
-  p.long_ids = up(long_ids);
-  p.n_long = static_cast<int>(long_ids.size());
-  p.n_long_tiles = (p.n_long + kWarps - 1) / kWarps;
-  p.huge_ids = up(huge_ids);
-  p.n_huge = static_cast<int>(huge_ids.size());
-  p.giant_ids = up(giant_ids);
-  p.giant_first = up(giant_first);
-  p.n_giant = static_cast<int>(giant_ids.size());
-  p.part_giant = up(part_giant);
-  p.part_beg = up(part_beg);
-  p.part_end = up(part_end);
-  p.n_parts = static_cast<int>(part_beg.size());
-  p.part_sums = dalloc<double>(part_beg.size());
+  p.units = up(units);
+  p.n_units = static_cast<int>(units.size());
+  p.multi_seg = up(multi_seg);
+  p.multi_parts = up(multi_parts);
+  p.n_multi = static_cast<int>(multi_seg.size());
+  p.part_sums = dalloc<double>(units.size());
   out.owned.push_back(p.part_sums);
-  p.giant_arrivals = dalloc<unsigned>(giant_ids.size());
-  out.owned.push_back(p.giant_arrivals);
-  CK(cudaMemset(p.giant_arrivals, 0, std::max<size_t>(1, giant_ids.size()) * sizeof(unsigned)));
-  p.total_tiles = p.n_parts + p.n_huge + p.n_long_tiles + p.n_bulk_tiles;
-  out.L = L;
-  c->max_giant = std::max(c->max_giant, p.n_giant);
+  p.arrivals = dalloc<unsigned>(multi_seg.size());
+  out.owned.push_back(p.arrivals);
+  CK(cudaMemset(p.arrivals, 0, std::max<size_t>(1, multi_seg.size()) * sizeof(unsigned)));
+  c->max_giant = std::max(c->max_giant, p.n_multi);
 }
 
 // Host-side CSR -> CSC (counting sort), columns in increasing row order
@@ -706,14 +698,16 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       col_values = cv.data();
     }
 
+    // value / index streams padded by 8 entries: bulk tiles are staged in
+    // 16-byte-aligned windows that may run up to 3 entries past the end
     c->csr_ptr = c->alloc<int>(m + 1);
-    c->csr_col = c->alloc<int>(nnz);
+    c->csr_col = c->alloc<int>(nnz + 8);
     c->csc_ptr = c->alloc<int>(n + 1);
-    c->csc_row = c->alloc<int>(nnz);
-    c->csr_orig = c->alloc<double>(nnz);
-    c->csc_orig = c->alloc<double>(nnz);
-    c->csr_work = c->alloc<double>(nnz);
-    c->csc_work = c->alloc<double>(nnz);
+    c->csc_row = c->alloc<int>(nnz + 8);
+    c->csr_orig = c->alloc<double>(nnz + 8);
+    c->csc_orig = c->alloc<double>(nnz + 8);
+    c->csr_work = c->alloc<double>(nnz + 8);
+    c->csc_work = c->alloc<double>(nnz + 8);
     {
       const int64_t cap = std::min<int64_t>(std::max<int64_t>({m + 1, n + 1, nnz}), int64_t(1) << 26);
       int64_t* stage = dalloc<int64_t>(cap);

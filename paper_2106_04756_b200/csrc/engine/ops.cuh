@@ -53,6 +53,13 @@ struct DevState {
   double movement;
 };
 
+// a[i] for i in {0, 1} without dynamic indexing (which would force the
+// parameter struct into local memory).
+template <class T>
+__device__ __forceinline__ T pick(const T (&a)[2], int i) {
+  return i ? a[1] : a[0];
+}
+
 // Buffers of the loop, fixed for the context lifetime.
 struct LoopBufs {
   double* x[2];
@@ -91,9 +98,9 @@ struct EpiPrimal {
     const DevState* st = b.st;
     if (!st->running) return false;
     const int cur = st->cur;
-    xc = b.x[cur];
-    xn = b.x[cur ^ 1];
-    yv = b.y[cur];
+    xc = pick(b.x, cur);
+    xn = pick(b.x, cur ^ 1);
+    yv = pick(b.y, cur);
     avg = b.avg_x;
     omega = st->omega;
     tau = st->eta / omega;  // solver.cpp:53
@@ -101,11 +108,17 @@ struct EpiPrimal {
     return true;
   }
   __device__ const double* vec() const { return yv; }
-  __device__ void apply(int j, double kty, double (&acc)[K]) const {
-    const double xj = xc[j];
-    if (pend != 0.0) avg[j] += pend * xj;
-    const double v = xj - tau * (b.c[j] - kty);
-    const double xv = ref_min(ref_max(v, b.l[j]), b.u[j]);
+  struct Pre {
+    double x, c, l, u, a;
+  };
+  __device__ Pre load(int j) const {
+    return Pre{xc[j], b.c[j], b.l[j], b.u[j], pend != 0.0 ? avg[j] : 0.0};
+  }
+  __device__ void apply(int j, double kty, const Pre& o, double (&acc)[K]) const {
+    const double xj = o.x;
+    if (pend != 0.0) avg[j] = o.a + pend * xj;
+    const double v = xj - tau * (o.c - kty);
+    const double xv = ref_min(ref_max(v, o.l), o.u);
     xn[j] = xv;
     const double dx = xv - xj;
     acc[0] += omega * dx * dx;
@@ -138,22 +151,28 @@ struct EpiDual {
     const DevState* st = b.st;
     if (!st->running) return false;
     const int cur = st->cur;
-    yc = b.y[cur];
-    yn = b.y[cur ^ 1];
-    kxc = b.kx[cur];
-    kxn = b.kx[cur ^ 1];
-    xv = b.x[cur ^ 1];
+    yc = pick(b.y, cur);
+    yn = pick(b.y, cur ^ 1);
+    kxc = pick(b.kx, cur);
+    kxn = pick(b.kx, cur ^ 1);
+    xv = pick(b.x, cur ^ 1);
     sigma = st->eta * st->omega;  // solver.cpp:54
     pend = st->pending;
     return true;
   }
   __device__ const double* vec() const { return xv; }
-  __device__ void apply(int i, double kx_next, double (&acc)[K]) const {
-    const double yi = yc[i];
-    if (pend != 0.0) b.avg_y[i] += pend * yi;
-    const double kxi = kxc[i];
+  struct Pre {
+    double y, kx, q, a;
+  };
+  __device__ Pre load(int i) const {
+    return Pre{yc[i], kxc[i], b.q[i], pend != 0.0 ? b.avg_y[i] : 0.0};
+  }
+  __device__ void apply(int i, double kx_next, const Pre& o, double (&acc)[K]) const {
+    const double yi = o.y;
+    if (pend != 0.0) b.avg_y[i] = o.a + pend * yi;
+    const double kxi = o.kx;
     const double extrapolated = 2.0 * kx_next - kxi;
-    double v = yi + sigma * (b.q[i] - extrapolated);
+    double v = yi + sigma * (o.q - extrapolated);
     if (i < b.m1) v = ref_max(v, 0.0);
     yn[i] = v;
     kxn[i] = kx_next;
@@ -240,7 +259,9 @@ struct EpiStore {
   double* out;
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return v; }
-  __device__ void apply(int s, double dot, double (&)[K]) const { out[s] = dot; }
+  struct Pre {};
+  __device__ Pre load(int) const { return Pre{}; }
+  __device__ void apply(int s, double dot, const Pre&, double (&)[K]) const { out[s] = dot; }
   __device__ void finalize(const double (&)[K]) const {}
 };
 
@@ -255,9 +276,13 @@ struct EpiStoreDotNorm {
   double* result;       // [2]
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return v; }
-  __device__ void apply(int s, double dot, double (&acc)[K]) const {
+  struct Pre {
+    double w;
+  };
+  __device__ Pre load(int s) const { return Pre{w[s]}; }
+  __device__ void apply(int s, double dot, const Pre& o, double (&acc)[K]) const {
     out[s] = dot;
-    acc[0] += w[s] * dot;
+    acc[0] += o.w * dot;
     acc[1] += dot * dot;
   }
   __device__ void finalize(const double (&tot)[K]) const {
@@ -318,8 +343,12 @@ struct EpiPrimalResidual {
   double* result;  // [1]
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return xr; }
-  __device__ void apply(int i, double kx, double (&acc)[K]) const {
-    double v = q[i] - kx;
+  struct Pre {
+    double q;
+  };
+  __device__ Pre load(int i) const { return Pre{q[i]}; }
+  __device__ void apply(int i, double kx, const Pre& o, double (&acc)[K]) const {
+    double v = o.q - kx;
     if (i < m1) v = ref_max(v, 0.0);
     acc[0] += v * v;
   }
@@ -339,9 +368,13 @@ struct EpiDualResidual {
   double* result;  // [3] dual_sq, bound terms, infinite-product count
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return yr; }
-  __device__ void apply(int j, double kty, double (&acc)[K]) const {
-    const double r = c[j] - kty;
-    const double lj = l[j], uj = u[j];
+  struct Pre {
+    double c, l, u;
+  };
+  __device__ Pre load(int j) const { return Pre{c[j], l[j], u[j]}; }
+  __device__ void apply(int j, double kty, const Pre& o, double (&acc)[K]) const {
+    const double r = o.c - kty;
+    const double lj = o.l, uj = o.u;
     const bool has_lower = lj > -INFINITY;
     const bool has_upper = uj < INFINITY;
     double lambda;
@@ -394,10 +427,14 @@ struct EpiNdgPrimal {
   double* result;
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return y; }
-  __device__ void apply(int j, double kty, double (&acc)[K]) const {
-    const double gj = kty - c[j];
-    const double loj = ref_min(0.0, l[j] - x[j]);
-    const double hij = ref_max(0.0, u[j] - x[j]);
+  struct Pre {
+    double x, c, l, u;
+  };
+  __device__ Pre load(int j) const { return Pre{x[j], c[j], l[j], u[j]}; }
+  __device__ void apply(int j, double kty, const Pre& o, double (&acc)[K]) const {
+    const double gj = kty - o.c;
+    const double loj = ref_min(0.0, o.l - o.x);
+    const double hij = ref_max(0.0, o.u - o.x);
     g[j] = gj;
     lo[j] = loj;
     hi[j] = hij;
@@ -431,10 +468,14 @@ struct EpiNdgDual {
   double* result;
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return x; }
-  __device__ void apply(int i, double kx, double (&acc)[K]) const {
+  struct Pre {
+    double y, q;
+  };
+  __device__ Pre load(int i) const { return Pre{y[i], q[i]}; }
+  __device__ void apply(int i, double kx, const Pre& o, double (&acc)[K]) const {
     if (kx_out != nullptr) kx_out[i] = kx;
-    const double gi = q[i] - kx;
-    const double loi = i < m1 ? ref_min(0.0, -y[i]) : -INFINITY;
+    const double gi = o.q - kx;
+    const double loi = i < m1 ? ref_min(0.0, -o.y) : -INFINITY;
     g[i] = gi;
     lo[i] = loi;
     const double w = winv;
@@ -462,7 +503,7 @@ struct OpNdgDualCached {
   EpiNdgDual e;
   __device__ bool prepare() { return true; }
   __device__ void apply(int64_t i, double (&acc)[K]) const {
-    e.apply(static_cast<int>(i), kx[i], acc);
+    e.apply(static_cast<int>(i), kx[i], e.load(static_cast<int>(i)), acc);
   }
   __device__ void finalize(const double (&tot)[K]) const { e.finalize(tot); }
 };

@@ -5,25 +5,34 @@
 //     dot_s = sum_{k in seg s} val[k] * vec[idx[k]]
 // followed by a per-segment *epilogue* that consumes dot_s in registers
 // (the fused primal / dual projected step, a residual, ...) and feeds
-// per-thread reduction accumulators.  The reductions are deterministic:
-// a fixed block->work mapping, fixed shuffle trees, per-block partials and a
+// per-thread reduction accumulators.  Reductions are deterministic: a fixed
+// block->work mapping, fixed shuffle trees, per-block partials and a
 // last-block-done final pass in index order -- no floating-point atomics, so
 // a rerun is bit-identical (the reference pins that in
 // proj/tests/acceptance_main.cpp:653-682).
 //
-// Load balancing for skewed segment lengths (power-law columns of config 2,
-// the 2M-entry sum row of config 3, 8000-long rows of config 5) uses four
-// work classes built once on the host (SegPlan):
-//   bulk  : segments in natural order, L lanes each (L = 1..32 from the mean
-//           length), len <= bulk_max       -> coalesced epilogue accesses
-//   long  : warp per segment, len <= kLongMax
-//   huge  : CTA per segment,  len <= kHugeMax
-//   giant : several CTAs per segment (fixed parts); the last part to arrive
-//           sums the parts in part order and runs the epilogue; its
-//           reduction contribution goes to a per-segment slot so the final
-//           order does not depend on arrival order.
-// Tiles of all classes are distributed round-robin over a persistent grid
-// (a few CTAs per SM), so the partial count stays ~1e3 at every size.
+// Work units (built once on the host, SegPlan) -- all warp-sized, one
+// balanced stream distributed round-robin over the warps of a grid of a few
+// CTAs per SM:
+//   tile : consecutive segments with len <= kWarpTile packed into <=
+//          kWarpTile nonzeros (CSR-stream per warp).  Lane l loads entries
+//          l, l+32, ... of the tile's contiguous value/index range
+//          (coalesced), issues its 8 gathers back to back and parks the
+//          products in a per-warp shared-memory buffer; one lane per segment
+//          then sums its products sequentially in index order -- the
+//          reference's own order (sparse_matrix.cpp:112-118), so these dots
+//          are bit-identical -- and runs the epilogue with operands it loaded
+//          before the gathers.
+//   part : a fixed chunk (kWarpTile entries; kGiantPart for giant segments)
+//          of a longer segment, reduced by the warp.  The last part of a
+//          segment to arrive sums the part sums in part order and runs the
+//          epilogue; its reduction contribution goes to a per-segment slot so
+//          the final order never depends on arrival order.
+// No CTA barrier outside the reduction tail: warps overlap gathering and
+// reducing, which keeps the L1 gather pipe busy (random 8-byte gathers
+// saturate at ~240 G/s on B200, one L1tex wavefront per lane --
+// tools/microbench/spmv_ceiling.cu -- which bounds a random-pattern SpMV
+// before HBM does).
 #pragma once
 
 #include <cstdint>
@@ -33,47 +42,35 @@ namespace folpgpu {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kLongMax = 2048;     // warp-per-segment up to this length
-constexpr int kHugeMax = 65536;    // CTA-per-segment up to this length
-constexpr int kGiantPart = 16384;  // nnz per part of a giant segment
-constexpr int kMaxAcc = 30;        // widest reduction (bisection pass)
+constexpr int kWarpTile = 256;        // nonzeros per tile / part (8 per lane)
+constexpr int kGiantMin = 65536;      // segments above this use kGiantPart parts
+constexpr int kGiantPart = 2048;      // nnz per part of a giant segment
+constexpr int kMaxAcc = 30;           // widest reduction (bisection pass)
 
 // std::max / std::min semantics (NaN in `a` propagates), which the
 // reference's projections rely on for its NonFiniteIterate detection.
-__device__ __forceinline__ double ref_max(double a, double b) {
-  return (a < b) ? b : a;
-}
-__device__ __forceinline__ double ref_min(double a, double b) {
-  return (b < a) ? b : a;
-}
+__device__ __forceinline__ double ref_max(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double ref_min(double a, double b) { return (b < a) ? b : a; }
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+// One warp unit: a tile {seg0, seg1, k0, k1} (seg0 >= 0) or a part
+// {-(multi+1), first_unit_of_segment, k0, k1} of multi-part segment `multi`.
 struct SegPlan {
-  const int* ptr;   // [S+1]
-  const int* idx;   // [nnz] gather index of each entry
+  const int* ptr;         // [S+1]
+  const int* idx;         // [nnz] gather index of each entry
   int S;
-  int bulk_max;     // bulk class handles len <= bulk_max
-  int n_bulk_tiles; // ceil(S / (kBlock / L))
-  const int* long_ids;
-  int n_long;
-  int n_long_tiles;  // ceil(n_long / kWarps)
-  const int* huge_ids;
-  int n_huge;
-  const int* giant_ids;   // [n_giant]
-  const int* giant_first; // [n_giant + 1] first part of each giant segment
-  int n_giant;
-  const int* part_giant;  // [n_parts] owning giant index
-  const int* part_beg;    // [n_parts]
-  const int* part_end;    // [n_parts]
-  int n_parts;
-  double* part_sums;        // [n_parts]
-  unsigned* giant_arrivals; // [n_giant]
-  int total_tiles;
+  const int4* units;      // [n_units]
+  int n_units;
+  const int* multi_seg;   // [n_multi] segment id of each multi-part segment
+  const int* multi_parts; // [n_multi] number of parts
+  int n_multi;
+  double* part_sums;      // [n_units] (only part slots used)
+  unsigned* arrivals;     // [n_multi], zero between launches
 };
 
 struct RedBuf {
-  double* partials;   // [(gridDim.x + n_giant) * K]
+  double* partials;   // [(gridDim.x + n_multi) * K]
   unsigned* counter;  // zero between launches (reset by the last block)
 };
 
@@ -95,8 +92,7 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 }
 
 template <int K>
-__device__ __forceinline__ void block_sum_vec(double (&acc)[K],
-                                              double (*scratch)[K],
+__device__ __forceinline__ void block_sum_vec(double (&acc)[K], double (*scratch)[K],
                                               double (&out)[K]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -121,8 +117,8 @@ __device__ __forceinline__ void block_sum_vec(double (&acc)[K],
 
 // Per-block partial + last-block-done final reduction, then epi.finalize().
 template <class Epi>
-__device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K],
-                                            RedBuf rb, int n_extra) {
+__device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K], RedBuf rb,
+                                            int n_extra) {
   constexpr int K = Epi::K;
   __shared__ double s_vec[kWarps][K];
   __shared__ int s_last;
@@ -153,103 +149,103 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   }
 }
 
-// The segmented-dot kernel.  L = lanes per bulk segment.
+// The segmented-dot kernel.
 // Epi must provide:  static constexpr int K (>= 1); static constexpr bool
 //   kReduce (run the reduction tail); __device__ bool prepare();
 //   __device__ const double* vec() const;
-//   __device__ void apply(int seg, double dot, double (&acc)[K]) const;
+//   struct Pre (epilogue operands of one segment, independent of the dot);
+//   __device__ Pre load(int seg) const;
+//   __device__ void apply(int seg, double dot, const Pre&, double (&acc)[K]) const;
 //   __device__ void finalize(const double (&tot)[K]) const;
-template <int L, class Epi>
+template <class Epi>
 __global__ void __launch_bounds__(kBlock)
 segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   constexpr int K = Epi::K;
   if (!epi.prepare()) return;  // loop slot disabled: every CTA agrees
   const double* __restrict__ vec = epi.vec();
   const int* __restrict__ idx = p.idx;
-  __shared__ double s_cta[kWarps];
+  const int* __restrict__ ptr = p.ptr;
+  __shared__ double s_prod[kWarps][kWarpTile];
+
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* wbuf = s_prod[warp];
+  const int nw = static_cast<int>(gridDim.x) * kWarps;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int t_huge0 = p.n_parts;
-  const int t_long0 = t_huge0 + p.n_huge;
-  const int t_bulk0 = t_long0 + p.n_long_tiles;
-
-  for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-    if (t >= t_bulk0) {
-      // ---- bulk: kBlock/L consecutive segments, L lanes each ----
-      const int seg = (t - t_bulk0) * (kBlock / L) + tid / L;
-      const int sub = tid % L;
-      double s = 0.0;
-      bool mine = false;
-      if (seg < p.S) {
-        const int beg = p.ptr[seg], end = p.ptr[seg + 1];
-        mine = (end - beg) <= p.bulk_max;
-        if (mine) {
-#pragma unroll 4
-          for (int k = beg + sub; k < end; k += L) s += val[k] * __ldg(&vec[idx[k]]);
+  for (int u = blockIdx.x * kWarps + warp; u < p.n_units; u += nw) {
+    const int4 d = p.units[u];
+    const int k0 = d.z, k1 = d.w;
+    if (d.x >= 0) {
+      // ---------------- tile of short segments ----------------
+      const int seg0 = d.x, seg1 = d.y;
+      const int s_first = seg0 + lane;
+      int b_first = 0, e_first = 0;
+      typename Epi::Pre pre_first{};
+      if (s_first < seg1) {
+        b_first = ptr[s_first];
+        e_first = ptr[s_first + 1];
+        pre_first = epi.load(s_first);  // in flight with the tile's loads
+      }
+      double prod[kWarpTile / 32];
+#pragma unroll
+      for (int j = 0; j < kWarpTile / 32; ++j) {
+        const int k = k0 + lane + 32 * j;
+        prod[j] = k < k1 ? val[k] * __ldg(&vec[idx[k]]) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kWarpTile / 32; ++j) {
+        const int k = k0 + lane + 32 * j;
+        if (k < k1) wbuf[k - k0] = prod[j];
+      }
+      __syncwarp();
+      for (int s = s_first; s < seg1; s += 32) {
+        int b = b_first, e = e_first;
+        typename Epi::Pre pre = pre_first;
+        if (s != s_first) {
+          b = ptr[s];
+          e = ptr[s + 1];
+          pre = epi.load(s);
         }
+        double sum = 0.0;
+        for (int k = b; k < e; ++k) sum += wbuf[k - k0];
+        epi.apply(s, sum, pre, acc);
       }
-      if (L > 1) {
-#pragma unroll
-        for (int off = L / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, L);
-      }
-      if (mine && sub == 0) epi.apply(seg, s, acc);
-    } else if (t >= t_long0) {
-      // ---- long: one warp per segment ----
-      const int i = (t - t_long0) * kWarps + warp;
-      if (i < p.n_long) {
-        const int seg = p.long_ids[i];
-        const int beg = p.ptr[seg], end = p.ptr[seg + 1];
-        double s = 0.0;
-#pragma unroll 4
-        for (int k = beg + lane; k < end; k += 32) s += val[k] * __ldg(&vec[idx[k]]);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-        if (lane == 0) epi.apply(seg, s, acc);
-      }
-    } else if (t >= t_huge0) {
-      // ---- huge: one CTA per segment ----
-      const int seg = p.huge_ids[t - t_huge0];
-      const int beg = p.ptr[seg], end = p.ptr[seg + 1];
-      double s = 0.0;
-#pragma unroll 4
-      for (int k = beg + tid; k < end; k += kBlock) s += val[k] * __ldg(&vec[idx[k]]);
-      s = block_sum(s, s_cta);
-      if (tid == 0) epi.apply(seg, s, acc);
+      __syncwarp();
     } else {
-      // ---- giant: one fixed part of a segment ----
-      const int beg = p.part_beg[t], end = p.part_end[t];
-      double s = 0.0;
-#pragma unroll 4
-      for (int k = beg + tid; k < end; k += kBlock) s += val[k] * __ldg(&vec[idx[k]]);
-      s = block_sum(s, s_cta);
-      if (tid == 0) {
-        p.part_sums[t] = s;
+      // ---------------- part of a long segment ----------------
+      const int multi = -d.x - 1;
+      double sum = 0.0;
+#pragma unroll 8
+      for (int k = k0 + lane; k < k1; k += 32) sum += val[k] * __ldg(&vec[idx[k]]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
+      if (lane == 0) {
+        p.part_sums[u] = sum;
         __threadfence();
-        const int g = p.part_giant[t];
-        const int first = p.giant_first[g];
-        const int np = p.giant_first[g + 1] - first;
-        const unsigned arrived = atomicAdd(&p.giant_arrivals[g], 1u);
+        const int np = p.multi_parts[multi];
+        const unsigned arrived = atomicAdd(&p.arrivals[multi], 1u);
         if (arrived == static_cast<unsigned>(np - 1)) {
           __threadfence();
+          const int first = d.y;
           double total = 0.0;
           for (int q = 0; q < np; ++q) total += ld_cg(&p.part_sums[first + q]);
-          double gacc[K];
+          const int seg = p.multi_seg[multi];
+          double macc[K];
 #pragma unroll
-          for (int k = 0; k < K; ++k) gacc[k] = 0.0;
-          epi.apply(p.giant_ids[g], total, gacc);
+          for (int k = 0; k < K; ++k) macc[k] = 0.0;
+          epi.apply(seg, total, epi.load(seg), macc);
           if constexpr (Epi::kReduce) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) rb.partials[(gridDim.x + g) * K + k] = gacc[k];
+            for (int k = 0; k < K; ++k) rb.partials[(gridDim.x + multi) * K + k] = macc[k];
           }
-          p.giant_arrivals[g] = 0u;
+          p.arrivals[multi] = 0u;
         }
       }
     }
   }
-  if constexpr (Epi::kReduce) reduce_tail(epi, acc, rb, p.n_giant);
+  if constexpr (Epi::kReduce) reduce_tail(epi, acc, rb, p.n_multi);
 }
 
 // Elementwise kernel with the same deterministic reduction tail.
