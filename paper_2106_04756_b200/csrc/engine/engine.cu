@@ -227,6 +227,25 @@ __global__ void k_div_scalar(double* __restrict__ dst, const double* __restrict_
     dst[i] = src[i] / snorm;  // sparse_matrix.cpp:213
 }
 
+// max |v|: grid-stride partial maxima into out_blocks, then one block folds
+// them (max is order-independent, so exact).
+__global__ void k_absmax_blocks(const double* __restrict__ v, int64_t n, double* out_blocks) {
+  __shared__ double s[kWarps];
+  double a = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a = fmax(a, fabs(v[i]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) a = fmax(a, __shfl_down_sync(0xffffffffu, a, off));
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < kWarps; ++w) r = fmax(r, s[w]);
+    out_blocks[blockIdx.x] = r;
+  }
+}
+
 __global__ void k_absmax_all(const double* __restrict__ v, int64_t n, double* out) {
   __shared__ double s[kWarps];
   double a = 0.0;
@@ -858,8 +877,10 @@ int folp_gpu_working_stats(folp_gpu_ctx* c, double* max_abs_entry, double* norm_
                            double* norm_q) {
   return guarded([&] {
     set_device(c);
-    k_absmax_all<<<1, kBlock, 0, c->stream>>>(c->csr_work, c->nnz, c->res + 0);
-    ++c->launches;
+    const int nb = std::min<int64_t>(c->sms * 4, std::max<int64_t>(1, (c->nnz + kBlock - 1) / kBlock));
+    k_absmax_blocks<<<nb, kBlock, 0, c->stream>>>(c->csr_work, c->nnz, c->partials);
+    k_absmax_all<<<1, kBlock, 0, c->stream>>>(c->partials, nb, c->res + 0);
+    c->launches += 2;
     c->ew(c->n, OpNormSq{c->cw, c->res + 1}, 4);
     c->ew(c->m, OpNormSq{c->qw, c->res + 2}, 5);
     c->fetch_res(3);
@@ -1067,6 +1088,7 @@ int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, do
     h->nu_lo = 0.0;
     h->nu_hi = std::sqrt(gsq) / radius;
     h->radius = radius;
+    ndg_candidates(h->nu_lo, h->nu_hi, h->nu);
     CK(cudaMemcpyAsync(c->ndg_d, h, sizeof(NdgState), cudaMemcpyHostToDevice, c->stream));
     OpNdgPass pass{};
     pass.n = n;
@@ -1077,13 +1099,13 @@ int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, do
     pass.omega = omega;
     pass.winv = 1.0 / omega;
     pass.ns = c->ndg_d;
-    int batch = 12;  // 48 levels before the first look
+    int batch = 14;  // 42 levels before the first look
     for (int round = 0; round < 64; ++round) {
       for (int i = 0; i < batch; ++i) c->ew(n + m, pass, 15);
       CK(cudaMemcpyAsync(h, c->ndg_d, sizeof(NdgState), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       if (h->done) break;
-      batch = 4;
+      batch = 5;
     }
     if (!h->done) throw EngineError(FOLP_E_RUNTIME, "normalized_duality_gap: bisection stalled");
     *gap = h->result;
@@ -1293,15 +1315,18 @@ int folp_gpu_axis_norms(folp_gpu_ctx* c, int32_t axis, double p, int32_t working
 int folp_gpu_max_abs_entry(folp_gpu_ctx* c, int32_t working, double* out) {
   return guarded([&] {
     set_device(c);
-    k_absmax_all<<<1, kBlock, 0, c->stream>>>(working ? c->csr_work : c->csr_orig, c->nnz,
-                                              c->res + 46);
-    ++c->launches;
+    const int nb = std::min<int64_t>(c->sms * 4, std::max<int64_t>(1, (c->nnz + kBlock - 1) / kBlock));
+    k_absmax_blocks<<<nb, kBlock, 0, c->stream>>>(working ? c->csr_work : c->csr_orig, c->nnz,
+                                                  c->partials);
+    k_absmax_all<<<1, kBlock, 0, c->stream>>>(c->partials, nb, c->res + 46);
+    c->launches += 2;
     c->fetch_res(47);
     *out = c->res_h[46];
   });
 }
 
 int64_t folp_gpu_launch_count(const folp_gpu_ctx* c) { return c->launches; }
+
 
 int folp_gpu_set_profiling(folp_gpu_ctx* c, int32_t enabled) {
   c->profiling = enabled != 0;

@@ -509,29 +509,30 @@ struct OpNdgDualCached {
 };
 
 // Bisection state of one normalized_duality_gap evaluation.
-constexpr int kNuLevels = 4;                     // bisection levels per pass
-constexpr int kNuCands = (1 << kNuLevels) - 1;   // 15 candidate multipliers
+constexpr int kNuLevels = 3;                     // bisection levels per pass
+constexpr int kNuCands = (1 << kNuLevels) - 1;   // 7 candidate multipliers
 struct NdgState {
   double nu_lo;
   double nu_hi;
   double radius;
   double result;   // g'd / r once done
+  double nu[kNuCands];  // candidates of the next pass (heap order)
   int32_t it;      // bisection iterations consumed (<= 200)
   int32_t done;
   int32_t passes;
   int32_t pad;
 };
 
-__device__ __forceinline__ void ndg_candidates(double lo, double hi,
-                                               double (&nu)[kNuCands]) {
-  // Heap-ordered tree of midpoints: node i covers [a_i, b_i] with
-  // nu_i = 0.5 * (a_i + b_i); children 2i+1 = [a_i, nu_i], 2i+2 = [nu_i, b_i].
+// Heap-ordered tree of the next kNuLevels bisection midpoints below
+// [lo, hi]: node i covers [a_i, b_i] with nu_i = 0.5 * (a_i + b_i)
+// (solver.cpp:360); children 2i+1 = [a_i, nu_i], 2i+2 = [nu_i, b_i].
+// Same IEEE operations on host and device.
+__host__ __device__ inline void ndg_candidates(double lo, double hi, double* nu) {
   double a[kNuCands], b[kNuCands];
   a[0] = lo;
   b[0] = hi;
-#pragma unroll
   for (int i = 0; i < kNuCands; ++i) {
-    nu[i] = 0.5 * (a[i] + b[i]);  // solver.cpp:360
+    nu[i] = 0.5 * (a[i] + b[i]);
     if (2 * i + 2 < kNuCands) {
       a[2 * i + 1] = a[i];
       b[2 * i + 1] = nu[i];
@@ -541,9 +542,10 @@ __device__ __forceinline__ void ndg_candidates(double lo, double hi,
   }
 }
 
-// One bisection pass: evaluates ||d(nu)||_w^2 and g'd(nu) for the 15 nodes of
-// the next 4 bisection levels (one read of g, lo, hi), then the last CTA
-// replays the reference's sequential bisection (solver.cpp:356-368) on them.
+// One bisection pass: evaluates ||d(nu)||_w^2 and g'd(nu) for the 7 nodes of
+// the next 3 bisection levels (one read of g, lo, hi), then the last CTA
+// replays the reference's sequential bisection (solver.cpp:356-368) on them
+// and leaves the next candidates in the state.
 struct OpNdgPass {
   static constexpr int K = 2 * kNuCands;
   static constexpr bool kReduce = true;
@@ -553,21 +555,18 @@ struct OpNdgPass {
   const double* hi;  // primal part only; dual hi = +inf
   double omega, winv;
   NdgState* ns;
-  double nu[kNuCands];
 
-  __device__ bool prepare() {
-    if (ns->done) return false;
-    ndg_candidates(ns->nu_lo, ns->nu_hi, nu);
-    return true;
-  }
+  __device__ bool prepare() { return ns->done == 0; }
   __device__ void apply(int64_t s, double (&acc)[K]) const {
     const double gs = g[s];
-    const double w = s < n ? omega : winv;
+    const bool primal = s < n;
+    const double w = primal ? omega : winv;
     const double los = lo[s];
-    const double his = s < n ? hi[s] : INFINITY;
+    const double his = primal ? hi[s] : INFINITY;
+    const double* nu = ns->nu;
 #pragma unroll
     for (int p = 0; p < kNuCands; ++p) {
-      const double unclamped = gs / (nu[p] * w);
+      const double unclamped = gs / (__ldg(&nu[p]) * w);  // solver.cpp:349
       const double d = ref_min(ref_max(unclamped, los), his);
       acc[2 * p] += w * d * d;
       acc[2 * p + 1] += gs * d;
@@ -582,29 +581,29 @@ struct OpNdgPass {
     st->passes += 1;
     for (int level = 0; level < kNuLevels; ++level) {
       const double norm_sq = tot[2 * node];
+      const int evaluated = node;
       st->it += 1;
       if (fabs(sqrt(norm_sq) - r) <= 1e-10 * r) {
-        st->result = tot[2 * node + 1] / r;
+        st->result = tot[2 * evaluated + 1] / r;
         st->done = 1;
         return;
       }
       if (norm_sq > r2) {
-        lo_ = nu[node];
+        lo_ = st->nu[node];
         node = 2 * node + 2;
       } else {
-        hi_ = nu[node];
+        hi_ = st->nu[node];
         node = 2 * node + 1;
       }
-      if (st->it >= 200) {
-        // loop exhausted: d holds the last evaluation
-        const int last = (node - 1) / 2;
-        st->result = tot[2 * last + 1] / r;
+      if (st->it >= 200) {  // loop exhausted: d holds the last evaluation
+        st->result = tot[2 * evaluated + 1] / r;
         st->done = 1;
         return;
       }
     }
     st->nu_lo = lo_;
     st->nu_hi = hi_;
+    ndg_candidates(lo_, hi_, st->nu);
   }
 };
 

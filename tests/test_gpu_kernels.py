@@ -88,3 +88,4 @@ def test_adaptive_step_matches(eng, ref, cfg, scale):
     assert a["eta_hat_next"] == pytest.approx(b["eta_hat_next"], rel=1e-10)
     np.testing.assert_allclose(a["x"], b["x"], rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(a["y"], b["y"], rtol=1e-12, atol=1e-12)
+
