@@ -102,6 +102,7 @@ typedef struct folp_gpu_eval {
   double dual_sq;            /* ||c - K'y - lambda||^2                    */
   double norm_q;             /* ||q||_2                                   */
   double norm_c;             /* ||c||_2                                   */
+  double dual_objective;     /* q'y + const + bound terms (lp_model.cpp:150-165) */
   int32_t nonfinite;         /* point had NaN/inf (NonFiniteIterate)      */
   int32_t infinite_product;  /* lambda outside its cone (InfiniteProduct) */
 } folp_gpu_eval;
@@ -200,6 +201,13 @@ int folp_gpu_multiply(folp_gpu_ctx* ctx, int32_t working, const double* x,
                       double* out);
 int folp_gpu_multiply_transpose(folp_gpu_ctx* ctx, int32_t working,
                                 const double* y, double* out);
+
+/* Reduction order of new contexts: 0 = tree (default: fast, deterministic,
+ * differs from the reference's sums in the last bits), 1 = ordered (every
+ * sum folded in the reference's sequential order: results bit-identical to
+ * the CPU reference; parity runs).  $FOLP_REDUCTION=ordered|tree overrides. */
+void folp_gpu_set_default_reduction(int32_t ordered);
+int32_t folp_gpu_reduction_ordered(const folp_gpu_ctx* ctx);
 
 /* Kernel launches issued by this context so far (for bench accounting). */
 int64_t folp_gpu_launch_count(const folp_gpu_ctx* ctx);

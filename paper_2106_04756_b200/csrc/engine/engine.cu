@@ -269,11 +269,15 @@ struct OpCountNonFinite {
   const double* y;
   double* result;
   __device__ bool prepare() { return true; }
-  __device__ void apply(int64_t i, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc& acc) const {
     const double v = i < n ? x[i] : y[i - n];
-    if (!isfinite(v)) acc[0] += 1.0;
+    acc.add(0, i, isfinite(v) ? 0.0 : 1.0);
   }
   __device__ void finalize(const double (&tot)[K]) const { result[0] = tot[0]; }
+  __device__ void finalize_ordered(const double* t, int64_t cnt) const {
+    result[0] = any_nonzero(t, cnt) ? 1.0 : 0.0;
+  }
 };
 
 struct OpNormSq {
@@ -282,8 +286,15 @@ struct OpNormSq {
   const double* v;
   double* result;
   __device__ bool prepare() { return true; }
-  __device__ void apply(int64_t i, double (&acc)[K]) const { acc[0] += v[i] * v[i]; }
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc& acc) const {
+    acc.add(0, i, v[i] * v[i]);
+  }
   __device__ void finalize(const double (&tot)[K]) const { result[0] = tot[0]; }
+  // linalg::norm2_squared order (linalg.hpp:31-35)
+  __device__ void finalize_ordered(const double* t, int64_t cnt) const {
+    result[0] = fold(0.0, t, cnt);
+  }
 };
 
 // ---------------------------------------------------------------------
@@ -292,6 +303,7 @@ struct PlanDev {
   std::vector<void*> owned;
 };
 
+bool g_default_ordered = false;
 std::mutex g_occ_mu;
 std::unordered_map<const void*, int> g_occ;
 
@@ -347,6 +359,8 @@ struct folp_gpu_ctx {
   double *red_h, *grow_h;  // pinned
   int64_t table_cap = 0;
   bool kx_valid = false;
+  bool ordered = false;     // bit-exact reference summation order (parity runs)
+  double* terms[2] = {nullptr, nullptr};  // ordered mode term regions
   bool norms_ready = false;
   double norm_q_sq = 0.0, norm_c_sq = 0.0;
   int max_giant = 0;
@@ -399,25 +413,43 @@ struct folp_gpu_ctx {
     const int64_t need = (count + kBlock - 1) / kBlock;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, sms * 8)));
   }
-  RedBuf red(int counter) { return RedBuf{partials, counters + counter}; }
+  RedBuf red(int counter) { return RedBuf{partials, counters + counter, nullptr, 0}; }
 
   template <class Epi>
-  void seg(const PlanDev& p, const double* val, const Epi& epi, int counter) {
-    auto fn = segdot_kernel<Epi>;
-    const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
+  void seg(const PlanDev& p, const double* val, const Epi& epi, int counter, int region = 1) {
+    RedBuf rb = red(counter);
     const int64_t need = (static_cast<int64_t>(p.sp.n_units) + kWarps - 1) / kWarps;
-    const int grid = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
-    fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, red(counter));
+    if (ordered) {
+      rb.terms = terms[region];
+      rb.nterm = p.sp.S;
+      auto fn = segdot_kernel<Epi, true>;
+      const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
+      fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, rb);
+    } else {
+      auto fn = segdot_kernel<Epi, false>;
+      const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
+      fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, rb);
+    }
     ++launches;
     CK(cudaGetLastError());
   }
 
   template <class Op>
-  void ew(int64_t count, const Op& op, int counter) {
-    auto fn = elementwise_kernel<Op>;
-    const int grid = ew_grid(count, reinterpret_cast<const void*>(fn));
-    fn<<<grid, kBlock, 0, stream>>>(count, op, red(counter));
+  void ew(int64_t count, const Op& op, int counter, int region = 1) {
+    RedBuf rb = red(counter);
+    if (ordered) {
+      rb.terms = terms[region];
+      rb.nterm = count;
+      auto fn = elementwise_kernel<Op, true>;
+      const int grid = ew_grid(count, reinterpret_cast<const void*>(fn));
+      fn<<<grid, kBlock, 0, stream>>>(count, op, rb);
+    } else {
+      auto fn = elementwise_kernel<Op, false>;
+      const int grid = ew_grid(count, reinterpret_cast<const void*>(fn));
+      fn<<<grid, kBlock, 0, stream>>>(count, op, rb);
+    }
     ++launches;
     CK(cudaGetLastError());
   }
@@ -448,6 +480,8 @@ struct folp_gpu_ctx {
     b.u = uw;
     b.q = qw;
     b.m1 = m1;
+    b.n = n;
+    b.a_terms = terms[0];
     b.st = st_d;
     b.red = red_d;
     b.grow = grow_d;
@@ -483,6 +517,7 @@ namespace {
 void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
                 const int* d_ptr, const int* d_idx, PlanDev& out) {
   (void)nnz;
+  const bool ordered = c->ordered;
   std::vector<int4> units;
   std::vector<int> multi_seg, multi_parts;
   int64_t seg0 = -1, tile_nnz = 0;
@@ -503,6 +538,11 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
       continue;
     }
     close(s);
+    if (ordered) {  // one lane sums the whole segment in index order
+      units.push_back(make_int4(static_cast<int>(s), static_cast<int>(s + 1),
+                                static_cast<int>(ptr[s]), static_cast<int>(ptr[s + 1])));
+      continue;
+    }
     const int multi = static_cast<int>(multi_seg.size());
     const int64_t part = len > kGiantMin ? kGiantPart : kWarpTile;
     const int first = static_cast<int>(units.size());
@@ -645,8 +685,8 @@ void build_chunk_graph(folp_gpu_ctx* c) {
     if (ok) {
       const LoopBufs b = c->loop_bufs(handle, 1);
       try {
-        c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2);
-        c->seg(c->rows, c->csr_work, EpiDual{b}, 3);
+        c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2, 0);
+        c->seg(c->rows, c->csr_work, EpiDual{b}, 3, 1);
         c->launches -= 2;
       } catch (...) {
         ok = false;
@@ -690,6 +730,10 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     }
     std::unique_ptr<folp_gpu_ctx> c(new folp_gpu_ctx());
     c->device = pick_device(device);
+    c->ordered = g_default_ordered;
+    if (const char* env = std::getenv("FOLP_REDUCTION")) {
+      c->ordered = std::strcmp(env, "ordered") == 0;
+    }
     set_device(c.get());
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, c->device));
@@ -768,6 +812,10 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     c->lo = c->alloc<double>(n + m);
     c->hi = vn();
     c->partials = c->alloc<double>(static_cast<size_t>(kMaxGrid + c->max_giant + 8) * kMaxAcc);
+    if (c->ordered) {
+      c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);
+      c->terms[1] = c->alloc<double>(5 * (n + m) + 8);
+    }
     c->counters = c->alloc<unsigned>(kCounters);
     CK(cudaMemsetAsync(c->counters, 0, kCounters * sizeof(unsigned), c->stream));
     c->res = c->alloc<double>(kResSlots);
@@ -999,12 +1047,16 @@ int folp_gpu_evaluate(folp_gpu_ctx* c, int32_t which, int32_t raw, folp_gpu_eval
     op.result = c->res + 8;
     c->ew(c->n + c->m, op, 7);
     c->seg(c->rows, c->csr_orig, EpiPrimalResidual{c->xr, c->q0, c->m1, c->res + 11}, 8);
-    c->seg(c->cols, c->csc_orig, EpiDualResidual{c->yr, c->c0, c->l0, c->u0, c->res + 12}, 9);
+    EpiDualResidual dres{c->yr, c->c0, c->l0, c->u0, c->res + 12};
+    dres.q_dot_y = c->res + 9;
+    dres.constant = c->objective_constant;
+    dres.dual_objective = c->res + 18;
+    c->seg(c->cols, c->csc_orig, dres, 9);
     if (!c->norms_ready) {
       c->ew(c->m, OpNormSq{c->q0, c->res + 15}, 10);
       c->ew(c->n, OpNormSq{c->c0, c->res + 16}, 11);
     }
-    c->fetch_res(c->norms_ready ? 15 : 17);
+    c->fetch_res(19);
     if (!c->norms_ready) {
       c->norm_q_sq = c->res_h[15];
       c->norm_c_sq = c->res_h[16];
@@ -1020,6 +1072,9 @@ int folp_gpu_evaluate(folp_gpu_ctx* c, int32_t which, int32_t raw, folp_gpu_eval
     out->infinite_product = r[14] != 0.0 ? 1 : 0;
     out->norm_q = std::sqrt(c->norm_q_sq);
     out->norm_c = std::sqrt(c->norm_c_sq);
+    // lp_model.cpp:154-163; ordered mode folded it term by term on device
+    out->dual_objective =
+        c->ordered ? r[18] : (out->q_dot_y + c->objective_constant) + out->bound_terms;
   });
 }
 
@@ -1048,7 +1103,7 @@ int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, do
     double* py = c->slot_y(which);
     // g, lo, hi over the primal coordinates (K~'y)
     EpiNdgPrimal ep{py, px, c->cw, c->lw, c->uw, omega, c->g, c->lo, c->hi, c->res + 24};
-    c->seg(c->cols, c->csc_work, ep, 13);
+    c->seg(c->cols, c->csc_work, ep, 13, 0);
     // ... and the dual ones (K~x; cached for CURRENT)
     EpiNdgDual ed{};
     ed.x = px;
@@ -1058,13 +1113,15 @@ int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, do
     ed.winv = 1.0 / omega;
     ed.g = c->g + n;
     ed.lo = c->lo + n;
-    ed.result = c->res + 29;
+    ed.result = c->res + 24;
+    ed.primal_terms = c->terms[0];
+    ed.n = n;
     if (which == FOLP_PT_CURRENT && c->kx_valid) {
       ed.kx_out = nullptr;
-      c->ew(m, OpNdgDualCached{c->kx[c->st_h->cur], ed}, 14);
+      c->ew(m, OpNdgDualCached{c->kx[c->st_h->cur], ed}, 14, 1);
     } else {
       ed.kx_out = which == FOLP_PT_AVERAGE ? c->kx_avg : c->kx_aux;
-      c->seg(c->rows, c->csr_work, ed, 14);
+      c->seg(c->rows, c->csr_work, ed, 14, 1);
     }
     c->fetch_res(34);
     const double* r = c->res_h;
@@ -1099,13 +1156,13 @@ int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, do
     pass.omega = omega;
     pass.winv = 1.0 / omega;
     pass.ns = c->ndg_d;
-    int batch = 14;  // 42 levels before the first look
-    for (int round = 0; round < 64; ++round) {
+    int batch = c->ordered ? 48 : 14;  // levels before the first look: 48 / 42
+    for (int round = 0; round < 256; ++round) {
       for (int i = 0; i < batch; ++i) c->ew(n + m, pass, 15);
       CK(cudaMemcpyAsync(h, c->ndg_d, sizeof(NdgState), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       if (h->done) break;
-      batch = 5;
+      batch = c->ordered ? 16 : 5;
     }
     if (!h->done) throw EngineError(FOLP_E_RUNTIME, "normalized_duality_gap: bisection stalled");
     *gap = h->result;
@@ -1195,8 +1252,8 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
       int64_t remaining = loop->target;
       for (;;) {
         for (int64_t s = 0; s < remaining + 2; ++s) {
-          c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2);
-          c->seg(c->rows, c->csr_work, EpiDual{b}, 3);
+          c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2, 0);
+          c->seg(c->rows, c->csr_work, EpiDual{b}, 3, 1);
         }
         CK(cudaMemcpyAsync(st, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1326,6 +1383,10 @@ int folp_gpu_max_abs_entry(folp_gpu_ctx* c, int32_t working, double* out) {
 }
 
 int64_t folp_gpu_launch_count(const folp_gpu_ctx* c) { return c->launches; }
+
+void folp_gpu_set_default_reduction(int32_t ordered) { g_default_ordered = ordered != 0; }
+
+int32_t folp_gpu_reduction_ordered(const folp_gpu_ctx* c) { return c->ordered ? 1 : 0; }
 
 
 int folp_gpu_set_profiling(folp_gpu_ctx* c, int32_t enabled) {

@@ -5,6 +5,14 @@
 // state.  Arithmetic follows the reference expression by expression (the
 // file is compiled with -fmad=false, so a*b+c is two roundings exactly like
 // the reference's x86-64 -O2 build, which emits no FMA).
+//
+// Reductions go through a sink `acc.add(k, index, term)`: tree mode sums in
+// registers (then per-CTA partials, see segdot.cuh); ordered mode stores the
+// term per index and finalize_ordered() folds the terms with one thread in
+// exactly the reference's sequential order, including the orders that span
+// two kernels (movement = sum dy^2 / omega + sum omega dx^2, solver.cpp:76-88;
+// dual objective = q'y + const + sum bound*lambda, lp_model.cpp:154-163;
+// the duality-gap sums over (x; y), solver.cpp:318-369).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -72,9 +80,11 @@ struct LoopBufs {
   const double* u;
   const double* q;
   int64_t m1;
+  int64_t n;
   DevState* st;
   const double* red;   // per-iteration factor tables of the chunk
   const double* grow;
+  const double* a_terms;  // ordered mode: kernel A's omega*dx*dx terms
   cudaGraphConditionalHandle cond;
   int use_cond;
 };
@@ -82,7 +92,7 @@ struct LoopBufs {
 // ---------------------------------------------------------------------
 // Kernel A: K'y of the current dual, fused primal projected step
 // (pdhg_trial, solver.cpp:58-63) + lazy averaging of the previous accepted
-// primal (accumulate_average, solver.cpp:530-538) + sum omega*dx*dx
+// primal (accumulate_average, solver.cpp:530-538) + omega*dx*dx
 // (solver.cpp:84-88) and the finiteness flag (solver.cpp:91-93).
 struct EpiPrimal {
   static constexpr int K = 2;
@@ -114,28 +124,95 @@ struct EpiPrimal {
   __device__ Pre load(int j) const {
     return Pre{xc[j], b.c[j], b.l[j], b.u[j], pend != 0.0 ? avg[j] : 0.0};
   }
-  __device__ void apply(int j, double kty, const Pre& o, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int j, double kty, const Pre& o, Acc& acc) const {
     const double xj = o.x;
     if (pend != 0.0) avg[j] = o.a + pend * xj;
     const double v = xj - tau * (o.c - kty);
     const double xv = ref_min(ref_max(v, o.l), o.u);
     xn[j] = xv;
     const double dx = xv - xj;
-    acc[0] += omega * dx * dx;
-    if (!isfinite(xv)) acc[1] += 1.0;
+    acc.add(0, j, omega * dx * dx);
+    acc.add(1, j, isfinite(xv) ? 0.0 : 1.0);
   }
   __device__ void finalize(const double (&tot)[K]) const {
     b.st->sx = tot[0];
     b.st->bad_a = tot[1];
   }
+  // kernel B folds the omega*dx*dx terms after its own (solver.cpp:83-88)
+  __device__ void finalize_ordered(const double* t, int64_t n) const {
+    b.st->bad_a = any_nonzero(t + n, n) ? 1.0 : 0.0;
+  }
 };
+
+// The adaptive step-size rule (adaptive_step, solver.cpp:173-199) and the
+// loop bookkeeping, run by one thread once a trial's sums are known.
+__device__ __forceinline__ void decide_trial(const LoopBufs& b, double cross, double movement,
+                                             bool bad) {
+  DevState* st = b.st;
+  st->slots += 1;
+  st->pending = 0.0;  // consumed by kernels A and B of this slot
+  const double eta = st->eta;
+  st->cross = cross;
+  st->movement = movement;
+  st->trials_iter += 1;
+  if (bad) {
+    st->status = kNonFinite;
+    st->running = 0;
+  } else {
+    bool accept = true;
+    double eta_next = eta;
+    if (st->policy == 0) {
+      const int64_t ki = st->k_total - st->k_chunk0;
+      const double eta_bar = cross > 0.0 ? movement / (2.0 * cross) : INFINITY;
+      const double a = b.red[ki] * eta_bar;
+      const double g = b.grow[ki] * eta;
+      eta_next = (g < a) ? g : a;  // std::min(a, g)
+      accept = eta <= eta_bar;
+    }
+    if (accept) {
+      st->k_total += 1;
+      st->t_inner += 1;
+      st->accepted += 1;
+      st->step_trials += st->trials_iter;
+      st->ledger_kt += 1;                   // K'y of the current point
+      st->ledger_k += 1 + st->trials_iter;  // Kx + one Kx' per trial
+      if (st->policy == 0 && cross > 0.0 && 2.0 * eta * cross > movement * (1.0 + 1e-9)) {
+        st->violations += 1;  // solver.cpp:618-621
+      }
+      st->trials_iter = 0;
+      st->last_eta_used = eta;
+      st->avg_weight += eta;
+      st->pending = eta;
+      if (st->policy == 0) {
+        st->eta_hat = eta_next;
+        st->eta = eta_next;
+      }
+      st->cur ^= 1;
+      if (st->accepted >= st->target) {
+        st->status = kDone;
+        st->running = 0;
+      } else if (st->k_total >= st->iteration_limit ||
+                 0.5 * static_cast<double>(st->ledger_k + st->ledger_kt) >= st->kkt_pass_limit) {
+        st->status = kLimit;
+        st->running = 0;
+      }
+    } else {
+      st->eta = eta_next;
+      if (eta_next < kStepSizeFloor) {
+        st->status = kUnderflow;
+        st->running = 0;
+      }
+    }
+  }
+  if (b.use_cond) cudaGraphSetConditional(b.cond, st->running ? 1u : 0u);
+}
 
 // Kernel B: K x' of the trial primal, fused dual projected step with the
 // extrapolation 2Kx'-Kx (solver.cpp:70-75), cross term and movement
 // (solver.cpp:76-83), lazy averaging of the previous accepted dual, and the
-// adaptive step-size decision (adaptive_step, solver.cpp:173-199) in the
-// last CTA.  Kx' is kept as the next Kx (bit-identical to recomputing it,
-// because the product is deterministic).
+// step-size decision in the last CTA.  Kx' is kept as the next Kx
+// (bit-identical to recomputing it: the product is deterministic).
 struct EpiDual {
   static constexpr int K = 3;
   static constexpr bool kReduce = true;
@@ -167,7 +244,8 @@ struct EpiDual {
   __device__ Pre load(int i) const {
     return Pre{yc[i], kxc[i], b.q[i], pend != 0.0 ? b.avg_y[i] : 0.0};
   }
-  __device__ void apply(int i, double kx_next, const Pre& o, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int i, double kx_next, const Pre& o, Acc& acc) const {
     const double yi = o.y;
     if (pend != 0.0) b.avg_y[i] = o.a + pend * yi;
     const double kxi = o.kx;
@@ -177,76 +255,24 @@ struct EpiDual {
     yn[i] = v;
     kxn[i] = kx_next;
     const double dy = v - yi;
-    acc[0] += dy * (kxi - kx_next);
-    acc[1] += dy * dy;
-    if (!isfinite(v)) acc[2] += 1.0;
+    acc.add(0, i, dy * (kxi - kx_next));
+    acc.add(1, i, dy * dy);
+    acc.add(2, i, isfinite(v) ? 0.0 : 1.0);
   }
   __device__ void finalize(const double (&tot)[K]) const {
-    DevState* st = b.st;
-    st->slots += 1;
-    st->pending = 0.0;  // consumed by kernels A and B of this slot
-    const double cross = tot[0];
-    const double omega = st->omega;
-    const double eta = st->eta;
-    double movement = tot[1];
-    movement = movement / omega;  // solver.cpp:83
+    const DevState* st = b.st;
+    double movement = tot[1] / st->omega;  // solver.cpp:83
     movement = movement + st->sx;
-    st->cross = cross;
-    st->movement = movement;
-    st->trials_iter += 1;
-    if (st->bad_a != 0.0 || tot[2] != 0.0) {
-      st->status = kNonFinite;
-      st->running = 0;
-    } else {
-      bool accept = true;
-      double eta_next = eta;
-      if (st->policy == 0) {
-        const int64_t ki = st->k_total - st->k_chunk0;
-        const double eta_bar =
-            cross > 0.0 ? movement / (2.0 * cross) : __longlong_as_double(0x7ff0000000000000LL);
-        const double a = b.red[ki] * eta_bar;
-        const double g = b.grow[ki] * eta;
-        eta_next = (g < a) ? g : a;  // std::min(a, g)
-        accept = eta <= eta_bar;
-      }
-      if (accept) {
-        st->k_total += 1;
-        st->t_inner += 1;
-        st->accepted += 1;
-        st->step_trials += st->trials_iter;
-        st->ledger_kt += 1;                    // K'y of the current point
-        st->ledger_k += 1 + st->trials_iter;   // Kx + one Kx' per trial
-        if (st->policy == 0 && cross > 0.0 &&
-            2.0 * eta * cross > movement * (1.0 + 1e-9)) {
-          st->violations += 1;  // solver.cpp:618-621
-        }
-        st->trials_iter = 0;
-        st->last_eta_used = eta;
-        st->avg_weight += eta;
-        st->pending = eta;
-        if (st->policy == 0) {
-          st->eta_hat = eta_next;
-          st->eta = eta_next;
-        }
-        st->cur ^= 1;
-        if (st->accepted >= st->target) {
-          st->status = kDone;
-          st->running = 0;
-        } else if (st->k_total >= st->iteration_limit ||
-                   0.5 * static_cast<double>(st->ledger_k + st->ledger_kt) >=
-                       st->kkt_pass_limit) {
-          st->status = kLimit;
-          st->running = 0;
-        }
-      } else {
-        st->eta = eta_next;
-        if (eta_next < kStepSizeFloor) {
-          st->status = kUnderflow;
-          st->running = 0;
-        }
-      }
-    }
-    if (b.use_cond) cudaGraphSetConditional(b.cond, st->running ? 1u : 0u);
+    decide_trial(b, tot[0], movement, st->bad_a != 0.0 || tot[2] != 0.0);
+  }
+  __device__ void finalize_ordered(const double* t, int64_t m) const {
+    const DevState* st = b.st;
+    const double cross = fold(0.0, t, m);       // solver.cpp:80
+    double movement = fold(0.0, t + m, m);      // solver.cpp:81
+    movement /= st->omega;                      // solver.cpp:83
+    movement = fold(movement, b.a_terms, b.n);  // solver.cpp:84-88
+    const bool bad = st->bad_a != 0.0 || any_nonzero(t + 2 * m, m);
+    decide_trial(b, cross, movement, bad);
   }
 };
 
@@ -261,8 +287,12 @@ struct EpiStore {
   __device__ const double* vec() const { return v; }
   struct Pre {};
   __device__ Pre load(int) const { return Pre{}; }
-  __device__ void apply(int s, double dot, const Pre&, double (&)[K]) const { out[s] = dot; }
+  template <class Acc>
+  __device__ void apply(int s, double dot, const Pre&, Acc&) const {
+    out[s] = dot;
+  }
   __device__ void finalize(const double (&)[K]) const {}
+  __device__ void finalize_ordered(const double*, int64_t) const {}
 };
 
 // out = K v plus the power-iteration reductions v'out and ||out||^2
@@ -280,14 +310,19 @@ struct EpiStoreDotNorm {
     double w;
   };
   __device__ Pre load(int s) const { return Pre{w[s]}; }
-  __device__ void apply(int s, double dot, const Pre& o, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int s, double dot, const Pre& o, Acc& acc) const {
     out[s] = dot;
-    acc[0] += o.w * dot;
-    acc[1] += dot * dot;
+    acc.add(0, s, o.w * dot);
+    acc.add(1, s, dot * dot);
   }
   __device__ void finalize(const double (&tot)[K]) const {
     result[0] = tot[0];
     result[1] = tot[1];
+  }
+  __device__ void finalize_ordered(const double* t, int64_t n) const {
+    result[0] = fold(0.0, t, n);
+    result[1] = fold(0.0, t + n, n);
   }
 };
 
@@ -312,24 +347,32 @@ struct OpEvalPoint {
   double* yr;
   double* result;    // [3] c'x, q'y, nonfinite count
   __device__ bool prepare() { return true; }
-  __device__ void apply(int64_t i, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc& acc) const {
     if (i < n) {
       const double v = raw ? xs[i] : ref_min(ref_max(xs[i] * d2[i], l[i]), u[i]);
       xr[i] = v;
-      acc[0] += c[i] * v;
-      if (!isfinite(v)) acc[2] += 1.0;
+      acc.add(0, i, c[i] * v);
+      acc.add(1, i, 0.0);
+      acc.add(2, i, isfinite(v) ? 0.0 : 1.0);
     } else {
       const int64_t j = i - n;
       const double v = raw ? ys[j] : ys[j] * d1[j];
       yr[j] = v;
-      acc[1] += q[j] * v;
-      if (!isfinite(v)) acc[2] += 1.0;
+      acc.add(0, i, 0.0);
+      acc.add(1, i, q[j] * v);
+      acc.add(2, i, isfinite(v) ? 0.0 : 1.0);
     }
   }
   __device__ void finalize(const double (&tot)[K]) const {
     result[0] = tot[0];
     result[1] = tot[1];
     result[2] = tot[2];
+  }
+  __device__ void finalize_ordered(const double* t, int64_t tot) const {
+    result[0] = fold(0.0, t, n);            // linalg::dot(c, x)
+    result[1] = fold(0.0, t + tot + n, m);  // linalg::dot(q, y)
+    result[2] = any_nonzero(t + 2 * tot, tot) ? 1.0 : 0.0;
   }
 };
 
@@ -347,12 +390,16 @@ struct EpiPrimalResidual {
     double q;
   };
   __device__ Pre load(int i) const { return Pre{q[i]}; }
-  __device__ void apply(int i, double kx, const Pre& o, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int i, double kx, const Pre& o, Acc& acc) const {
     double v = o.q - kx;
     if (i < m1) v = ref_max(v, 0.0);
-    acc[0] += v * v;
+    acc.add(0, i, v * v);
   }
   __device__ void finalize(const double (&tot)[K]) const { result[0] = tot[0]; }
+  __device__ void finalize_ordered(const double* t, int64_t m) const {
+    result[0] = fold(0.0, t, m);
+  }
 };
 
 // Step 3 (columns, original values): reduced costs, dual residual and the
@@ -365,14 +412,18 @@ struct EpiDualResidual {
   const double* c;
   const double* l;
   const double* u;
-  double* result;  // [3] dual_sq, bound terms, infinite-product count
+  double* result;          // [3] dual_sq, bound terms, infinite-product count
+  const double* q_dot_y;   // ordered mode: q'y from step 1
+  double constant;         // ordered mode: objective constant
+  double* dual_objective;  // ordered mode: q'y + const + sum bound*lambda
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return yr; }
   struct Pre {
     double c, l, u;
   };
   __device__ Pre load(int j) const { return Pre{c[j], l[j], u[j]}; }
-  __device__ void apply(int j, double kty, const Pre& o, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int j, double kty, const Pre& o, Acc& acc) const {
     const double r = o.c - kty;
     const double lj = o.l, uj = o.u;
     const bool has_lower = lj > -INFINITY;
@@ -388,20 +439,35 @@ struct EpiDualResidual {
       lambda = r;
     }
     const double d = r - lambda;
-    acc[0] += d * d;
+    acc.add(0, j, d * d);
+    double bt = 0.0, inf = 0.0;
     if (lambda != 0.0) {
       const double bound = lambda > 0.0 ? lj : uj;
       if (!isfinite(bound)) {
-        acc[2] += 1.0;
+        inf = 1.0;
       } else {
-        acc[1] += bound * lambda;
+        bt = bound * lambda;
       }
     }
+    acc.add(1, j, bt);
+    acc.add(2, j, inf);
   }
   __device__ void finalize(const double (&tot)[K]) const {
     result[0] = tot[0];
     result[1] = tot[1];
     result[2] = tot[2];
+  }
+  __device__ void finalize_ordered(const double* t, int64_t n) const {
+    result[0] = fold(0.0, t, n);
+    result[1] = 0.0;
+    result[2] = any_nonzero(t + 2 * n, n) ? 1.0 : 0.0;
+    // lp_model.cpp:154-163: value = q'y + const, then += bound*lambda in order
+    double v = *q_dot_y + constant;
+    for (int64_t j = 0; j < n; ++j) {
+      const double bt = ld_cg(&t[n + j]);
+      if (bt != 0.0) v += bt;
+    }
+    *dual_objective = v;
   }
 };
 
@@ -410,8 +476,21 @@ struct EpiDualResidual {
 // n primal coordinates (columns: K'y) and the m dual ones (rows: Kx), with
 // the reductions of the any-gradient test, sum g^2/w and the nu -> 0
 // "bounded" corner (solver.cpp:318-342).
-// acc: [0] #g!=0, [1] sum g*g/w, [2] #non-finite corner, [3] sum w*d*d,
-//      [4] sum g*d
+// terms: [0] g!=0, [1] g*g/w, [2] non-finite corner, [3] w*d*d, [4] g*d
+__device__ __forceinline__ void ndg_terms(double gj, double w, double d, double (&t)[5]) {
+  t[0] = gj != 0.0 ? 1.0 : 0.0;
+  t[1] = gj * gj / w;
+  if (!isfinite(d)) {
+    t[2] = 1.0;
+    t[3] = 0.0;
+    t[4] = 0.0;
+  } else {
+    t[2] = 0.0;
+    t[3] = w * d * d;
+    t[4] = gj * d;
+  }
+}
+
 struct EpiNdgPrimal {
   static constexpr int K = 5;
   static constexpr bool kReduce = true;
@@ -431,27 +510,26 @@ struct EpiNdgPrimal {
     double x, c, l, u;
   };
   __device__ Pre load(int j) const { return Pre{x[j], c[j], l[j], u[j]}; }
-  __device__ void apply(int j, double kty, const Pre& o, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int j, double kty, const Pre& o, Acc& acc) const {
     const double gj = kty - o.c;
     const double loj = ref_min(0.0, o.l - o.x);
     const double hij = ref_max(0.0, o.u - o.x);
     g[j] = gj;
     lo[j] = loj;
     hi[j] = hij;
-    const double w = omega;
-    if (gj != 0.0) acc[0] += 1.0;
-    acc[1] += gj * gj / w;
     const double d = gj > 0.0 ? hij : (gj < 0.0 ? loj : 0.0);
-    if (!isfinite(d)) {
-      acc[2] += 1.0;
-    } else {
-      acc[3] += w * d * d;
-      acc[4] += gj * d;
-    }
+    double t[5];
+    ndg_terms(gj, omega, d, t);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc.add(k, j, t[k]);
   }
   __device__ void finalize(const double (&tot)[K]) const {
+#pragma unroll
     for (int k = 0; k < K; ++k) result[k] = tot[k];
   }
+  // the dual half folds both halves in (x; y) order
+  __device__ void finalize_ordered(const double*, int64_t) const {}
 };
 
 struct EpiNdgDual {
@@ -465,32 +543,41 @@ struct EpiNdgDual {
   double* g;         // dual part (already offset by n)
   double* lo;
   double* kx_out;    // Kx of the point (kept for a restart to it)
-  double* result;
+  double* result;    // [10]: primal half [0..5), dual half [5..10)
+  const double* primal_terms;  // ordered mode: EpiNdgPrimal's terms [5 n]
+  int64_t n;
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return x; }
   struct Pre {
     double y, q;
   };
   __device__ Pre load(int i) const { return Pre{y[i], q[i]}; }
-  __device__ void apply(int i, double kx, const Pre& o, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int i, double kx, const Pre& o, Acc& acc) const {
     if (kx_out != nullptr) kx_out[i] = kx;
     const double gi = o.q - kx;
     const double loi = i < m1 ? ref_min(0.0, -o.y) : -INFINITY;
     g[i] = gi;
     lo[i] = loi;
-    const double w = winv;
-    if (gi != 0.0) acc[0] += 1.0;
-    acc[1] += gi * gi / w;
     const double d = gi > 0.0 ? INFINITY : (gi < 0.0 ? loi : 0.0);
-    if (!isfinite(d)) {
-      acc[2] += 1.0;
-    } else {
-      acc[3] += w * d * d;
-      acc[4] += gi * d;
-    }
+    double t[5];
+    ndg_terms(gi, winv, d, t);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc.add(k, i, t[k]);
   }
   __device__ void finalize(const double (&tot)[K]) const {
-    for (int k = 0; k < K; ++k) result[k] = tot[k];
+#pragma unroll
+    for (int k = 0; k < K; ++k) result[k + 5] = tot[k];
+  }
+  // both halves, (x; y) order; the primal slots [0..5) carry the totals
+  __device__ void finalize_ordered(const double* t, int64_t m) const {
+    const double* p = primal_terms;
+    result[0] = (any_nonzero(p, n) || any_nonzero(t, m)) ? 1.0 : 0.0;
+    result[1] = fold(fold(0.0, p + n, n), t + m, m);          // solver.cpp:322
+    result[2] = (any_nonzero(p + 2 * n, n) || any_nonzero(t + 2 * m, m)) ? 1.0 : 0.0;
+    result[3] = fold(fold(0.0, p + 3 * n, n), t + 3 * m, m);  // solver.cpp:338
+    result[4] = fold(fold(0.0, p + 4 * n, n), t + 4 * m, m);  // linalg::dot(g, d)
+    for (int k = 5; k < 10; ++k) result[k] = 0.0;
   }
 };
 
@@ -502,10 +589,14 @@ struct OpNdgDualCached {
   const double* kx;
   EpiNdgDual e;
   __device__ bool prepare() { return true; }
-  __device__ void apply(int64_t i, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc& acc) const {
     e.apply(static_cast<int>(i), kx[i], e.load(static_cast<int>(i)), acc);
   }
   __device__ void finalize(const double (&tot)[K]) const { e.finalize(tot); }
+  __device__ void finalize_ordered(const double* t, int64_t m) const {
+    e.finalize_ordered(t, m);
+  }
 };
 
 // Bisection state of one normalized_duality_gap evaluation.
@@ -542,10 +633,44 @@ __host__ __device__ inline void ndg_candidates(double lo, double hi, double* nu)
   }
 }
 
-// One bisection pass: evaluates ||d(nu)||_w^2 and g'd(nu) for the 7 nodes of
-// the next 3 bisection levels (one read of g, lo, hi), then the last CTA
-// replays the reference's sequential bisection (solver.cpp:356-368) on them
-// and leaves the next candidates in the state.
+// Replays `levels` levels of the reference bisection (solver.cpp:356-368)
+// from per-node sums (heap order) and leaves the next bracket.
+__device__ inline void ndg_replay(NdgState* st, const double* norm_sq, const double* gd,
+                                  int levels) {
+  const double r = st->radius;
+  const double r2 = r * r;
+  double lo_ = st->nu_lo, hi_ = st->nu_hi;
+  int node = 0;
+  st->passes += 1;
+  for (int level = 0; level < levels; ++level) {
+    const int evaluated = node;
+    st->it += 1;
+    if (fabs(sqrt(norm_sq[evaluated]) - r) <= 1e-10 * r) {
+      st->result = gd[evaluated] / r;
+      st->done = 1;
+      return;
+    }
+    if (norm_sq[evaluated] > r2) {
+      lo_ = st->nu[evaluated];
+      node = 2 * node + 2;
+    } else {
+      hi_ = st->nu[evaluated];
+      node = 2 * node + 1;
+    }
+    if (st->it >= 200) {  // loop exhausted: d holds the last evaluation
+      st->result = gd[evaluated] / r;
+      st->done = 1;
+      return;
+    }
+  }
+  st->nu_lo = lo_;
+  st->nu_hi = hi_;
+  ndg_candidates(lo_, hi_, st->nu);
+}
+
+// One bisection pass.  Tree mode: ||d(nu)||_w^2 and g'd(nu) for the 7 nodes
+// of the next 3 levels (one read of g, lo, hi).  Ordered mode: the first
+// node only, folded in (x; y) order -- one reference iteration per pass.
 struct OpNdgPass {
   static constexpr int K = 2 * kNuCands;
   static constexpr bool kReduce = true;
@@ -557,53 +682,35 @@ struct OpNdgPass {
   NdgState* ns;
 
   __device__ bool prepare() { return ns->done == 0; }
-  __device__ void apply(int64_t s, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int64_t s, Acc& acc) const {
     const double gs = g[s];
     const bool primal = s < n;
     const double w = primal ? omega : winv;
     const double los = lo[s];
     const double his = primal ? hi[s] : INFINITY;
     const double* nu = ns->nu;
+    constexpr int P = Acc::kOrdered ? 1 : kNuCands;
 #pragma unroll
-    for (int p = 0; p < kNuCands; ++p) {
+    for (int p = 0; p < P; ++p) {
       const double unclamped = gs / (__ldg(&nu[p]) * w);  // solver.cpp:349
       const double d = ref_min(ref_max(unclamped, los), his);
-      acc[2 * p] += w * d * d;
-      acc[2 * p + 1] += gs * d;
+      acc.add(2 * p, s, w * d * d);
+      acc.add(2 * p + 1, s, gs * d);
     }
   }
   __device__ void finalize(const double (&tot)[K]) const {
-    NdgState* st = ns;
-    const double r = st->radius;
-    const double r2 = r * r;
-    double lo_ = st->nu_lo, hi_ = st->nu_hi;
-    int node = 0;
-    st->passes += 1;
-    for (int level = 0; level < kNuLevels; ++level) {
-      const double norm_sq = tot[2 * node];
-      const int evaluated = node;
-      st->it += 1;
-      if (fabs(sqrt(norm_sq) - r) <= 1e-10 * r) {
-        st->result = tot[2 * evaluated + 1] / r;
-        st->done = 1;
-        return;
-      }
-      if (norm_sq > r2) {
-        lo_ = st->nu[node];
-        node = 2 * node + 2;
-      } else {
-        hi_ = st->nu[node];
-        node = 2 * node + 1;
-      }
-      if (st->it >= 200) {  // loop exhausted: d holds the last evaluation
-        st->result = tot[2 * evaluated + 1] / r;
-        st->done = 1;
-        return;
-      }
+    double nsq[kNuCands], gd[kNuCands];
+    for (int p = 0; p < kNuCands; ++p) {
+      nsq[p] = tot[2 * p];
+      gd[p] = tot[2 * p + 1];
     }
-    st->nu_lo = lo_;
-    st->nu_hi = hi_;
-    ndg_candidates(lo_, hi_, st->nu);
+    ndg_replay(ns, nsq, gd, kNuLevels);
+  }
+  __device__ void finalize_ordered(const double* t, int64_t tot_n) const {
+    const double norm_sq = fold(0.0, t, tot_n);
+    const double gd = fold(0.0, t + tot_n, tot_n);
+    ndg_replay(ns, &norm_sq, &gd, 1);
   }
 };
 
@@ -619,18 +726,25 @@ struct OpDistance {
   const double* yb;
   double* result;
   __device__ bool prepare() { return true; }
-  __device__ void apply(int64_t i, double (&acc)[K]) const {
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc& acc) const {
     if (i < n) {
       const double d = xa[i] - xb[i];
-      acc[0] += d * d;
+      acc.add(0, i, d * d);
+      acc.add(1, i, 0.0);
     } else {
       const double d = ya[i - n] - yb[i - n];
-      acc[1] += d * d;
+      acc.add(0, i, 0.0);
+      acc.add(1, i, d * d);
     }
   }
   __device__ void finalize(const double (&tot)[K]) const {
     result[0] = tot[0];
     result[1] = tot[1];
+  }
+  __device__ void finalize_ordered(const double* t, int64_t tot) const {
+    result[0] = fold(0.0, t, n);
+    result[1] = fold(0.0, t + tot + n, tot - n);
   }
 };
 
@@ -652,7 +766,8 @@ struct OpAverage {
   double* out_x;
   double* out_y;
   __device__ bool prepare() { return true; }
-  __device__ void apply(int64_t i, double (&)[K]) const {
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc&) const {
     if (i < n) {
       double s = ax[i];
       if (pending != 0.0) {
@@ -673,6 +788,7 @@ struct OpAverage {
     }
   }
   __device__ void finalize(const double (&)[K]) const {}
+  __device__ void finalize_ordered(const double*, int64_t) const {}
 };
 
 }  // namespace folpgpu

@@ -36,6 +36,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace folpgpu {
@@ -72,7 +73,47 @@ struct SegPlan {
 struct RedBuf {
   double* partials;   // [(gridDim.x + n_multi) * K]
   unsigned* counter;  // zero between launches (reset by the last block)
+  double* terms;      // ordered mode: [K * nterm] per-segment terms
+  int64_t nterm;      // ordered mode: segment (element) count
 };
+
+// Reduction sinks.  Tree mode accumulates in registers (fast, deterministic
+// but not the reference's summation order); ordered mode stores each
+// segment's term so one thread can fold them in the reference's sequential
+// order afterwards (bit-identical to the reference, used for parity runs).
+template <int K>
+struct TreeAcc {
+  static constexpr bool kOrdered = false;
+  double v[K];
+  __device__ void zero() {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = 0.0;
+  }
+  __device__ __forceinline__ void add(int k, int64_t, double x) { v[k] += x; }
+};
+
+template <int K>
+struct OrderedAcc {
+  static constexpr bool kOrdered = true;
+  double* terms;
+  int64_t nterm;
+  __device__ void zero() {}
+  __device__ __forceinline__ void add(int k, int64_t seg, double x) {
+    terms[k * nterm + seg] = x;
+  }
+};
+
+// fold(init, t[0..n)) in index order, one thread
+__device__ __forceinline__ double fold(double init, const double* t, int64_t n) {
+  double s = init;
+  for (int64_t i = 0; i < n; ++i) s += ld_cg(&t[i]);
+  return s;
+}
+__device__ __forceinline__ bool any_nonzero(const double* t, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (ld_cg(&t[i]) != 0.0) return true;
+  return false;
+}
 
 // Sum over the CTA; result valid in thread 0.  Ends with a barrier so the
 // scratch can be reused immediately.
@@ -113,6 +154,26 @@ __device__ __forceinline__ void block_sum_vec(double (&acc)[K], double (*scratch
     }
   }
   __syncthreads();
+}
+
+// Ordered mode: after every CTA stored its terms, the last CTA's thread 0
+// folds them (epi.finalize_ordered).
+template <class Epi>
+__device__ __forceinline__ void ordered_tail(const Epi& epi, RedBuf rb) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned ticket = atomicAdd(rb.counter, 1u);
+    s_last = (ticket == gridDim.x - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    epi.finalize_ordered(rb.terms, rb.nterm);
+    *rb.counter = 0u;
+  }
 }
 
 // Per-block partial + last-block-done final reduction, then epi.finalize().
@@ -157,7 +218,7 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
 //   __device__ Pre load(int seg) const;
 //   __device__ void apply(int seg, double dot, const Pre&, double (&acc)[K]) const;
 //   __device__ void finalize(const double (&tot)[K]) const;
-template <class Epi>
+template <class Epi, bool ORDERED>
 __global__ void __launch_bounds__(kBlock)
 segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   constexpr int K = Epi::K;
@@ -167,9 +228,13 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   const int* __restrict__ ptr = p.ptr;
   __shared__ double s_prod[kWarps][kWarpTile];
 
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  using Acc = std::conditional_t<ORDERED, OrderedAcc<K>, TreeAcc<K>>;
+  Acc acc;
+  if constexpr (ORDERED) {
+    acc.terms = rb.terms;
+    acc.nterm = rb.nterm;
+  }
+  acc.zero();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* wbuf = s_prod[warp];
   const int nw = static_cast<int>(gridDim.x) * kWarps;
@@ -177,7 +242,14 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   for (int u = blockIdx.x * kWarps + warp; u < p.n_units; u += nw) {
     const int4 d = p.units[u];
     const int k0 = d.z, k1 = d.w;
-    if (d.x >= 0) {
+    if (d.x >= 0 && k1 - k0 > kWarpTile) {
+      // ordered plan: one long segment, summed by one lane in index order
+      if (lane == 0) {
+        double sum = 0.0;
+        for (int k = k0; k < k1; ++k) sum += val[k] * vec[idx[k]];
+        epi.apply(d.x, sum, epi.load(d.x), acc);
+      }
+    } else if (d.x >= 0) {
       // ---------------- tile of short segments ----------------
       const int seg0 = d.x, seg1 = d.y;
       const int s_first = seg0 + lane;
@@ -213,7 +285,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         epi.apply(s, sum, pre, acc);
       }
       __syncwarp();
-    } else {
+    } else if constexpr (!ORDERED) {
       // ---------------- part of a long segment ----------------
       const int multi = -d.x - 1;
       double sum = 0.0;
@@ -232,36 +304,52 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
           double total = 0.0;
           for (int q = 0; q < np; ++q) total += ld_cg(&p.part_sums[first + q]);
           const int seg = p.multi_seg[multi];
-          double macc[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) macc[k] = 0.0;
+          TreeAcc<K> macc;
+          macc.zero();
           epi.apply(seg, total, epi.load(seg), macc);
           if constexpr (Epi::kReduce) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) rb.partials[(gridDim.x + multi) * K + k] = macc[k];
+            for (int k = 0; k < K; ++k) rb.partials[(gridDim.x + multi) * K + k] = macc.v[k];
           }
           p.arrivals[multi] = 0u;
         }
       }
     }
   }
-  if constexpr (Epi::kReduce) reduce_tail(epi, acc, rb, p.n_multi);
+  if constexpr (Epi::kReduce) {
+    if constexpr (ORDERED) {
+      ordered_tail(epi, rb);
+    } else {
+      reduce_tail(epi, acc.v, rb, p.n_multi);
+    }
+  }
 }
 
 // Elementwise kernel with the same deterministic reduction tail.
-// Op must provide K (>= 1), kReduce, prepare(), apply(i, acc), finalize(tot).
-template <class Op>
+// Op must provide K (>= 1), kReduce, prepare(), apply(i, acc), finalize(tot),
+// finalize_ordered(terms, n).
+template <class Op, bool ORDERED>
 __global__ void __launch_bounds__(kBlock) elementwise_kernel(int64_t n, Op op, RedBuf rb) {
   constexpr int K = Op::K;
   if (!op.prepare()) return;
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  using Acc = std::conditional_t<ORDERED, OrderedAcc<K>, TreeAcc<K>>;
+  Acc acc;
+  if constexpr (ORDERED) {
+    acc.terms = rb.terms;
+    acc.nterm = rb.nterm;
+  }
+  acc.zero();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kBlock;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x; i < n; i += stride) {
     op.apply(i, acc);
   }
-  if constexpr (Op::kReduce) reduce_tail(op, acc, rb, 0);
+  if constexpr (Op::kReduce) {
+    if constexpr (ORDERED) {
+      ordered_tail(op, rb);
+    } else {
+      reduce_tail(op, acc.v, rb, 0);
+    }
+  }
 }
 
 }  // namespace folpgpu

@@ -94,7 +94,7 @@ ConvergenceInfo Context::evaluate(int which, bool raw, double objective_constant
   // termination.cpp:43-71 final arithmetic
   ConvergenceInfo info;
   info.primal_objective = e.c_dot_x + objective_constant;
-  info.dual_objective = (e.q_dot_y + objective_constant) + e.bound_terms;
+  info.dual_objective = e.dual_objective;
   info.gap_abs = std::fabs(info.dual_objective - info.primal_objective);
   info.primal_residual_norm = std::sqrt(e.primal_sq);
   info.dual_residual_norm = std::sqrt(e.dual_sq);
