@@ -210,6 +210,14 @@ int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms,
 int folp_session_result(folp_session* s, folp_result_c* out);
 void folp_session_destroy(folp_session* s);
 
+/* malitsky_pock_step (solver.hpp:160-164): next point to x_next/y_next;
+ * params supplies the mp_* factors. */
+int folp_malitsky_pock_step(const folp_lp_c* lp, const double* x,
+                            const double* y, double omega, double eta_prev,
+                            double theta_prev, const folp_params_c* params,
+                            double* x_next, double* y_next, double* eta_next,
+                            double* theta_next, int64_t* trials);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* folp_last_error(void);
 

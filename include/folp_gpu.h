@@ -69,7 +69,7 @@ typedef struct folp_gpu_problem {
 
 /* Loop state mirrored between host and device at chunk boundaries. */
 typedef struct folp_gpu_loop {
-  int32_t policy;            /* FOLP_STEP_ADAPTIVE or FOLP_STEP_CONSTANT  */
+  int32_t policy;            /* FOLP_STEP_* (adaptive, constant, Malitsky-Pock) */
   int32_t status;            /* out: FOLP_CHUNK_*                         */
   int64_t target;            /* in: accepted iterations wanted            */
   int64_t accepted;          /* out                                        */
@@ -82,7 +82,12 @@ typedef struct folp_gpu_loop {
   int64_t iteration_limit;   /* in                                         */
   double kkt_pass_limit;     /* in                                         */
   double omega;              /* in: primal weight                          */
-  double eta;                /* in/out: eta_hat (adaptive) or eta (const)  */
+  double eta;                /* in/out: eta_hat (adaptive), eta (constant),
+                                the last accepted step (Malitsky-Pock)    */
+  double theta;              /* in/out: Malitsky-Pock step ratio           */
+  double mp_breaking_factor; /* in: SolverParams mp_* (solver.hpp:41-43)   */
+  double mp_downscaling_factor;
+  double mp_interpolation_coefficient;
   double last_eta_used;      /* out                                        */
   double avg_weight;         /* out: sum of eta over the running average   */
   double last_movement;      /* out: ||z'-z||_omega^2 of the last trial    */
@@ -182,6 +187,32 @@ int folp_gpu_restart_to(folp_gpu_ctx* ctx, int32_t which,
 /* Sets LAST = CURRENT without touching the average (kNone schedule,
  * solver.cpp:771-781). */
 int folp_gpu_mark_last(folp_gpu_ctx* ctx);
+
+/* One evaluation period of the restarted loop (solver.cpp:751-798) in a
+ * single asynchronous sequence with one host synchronisation:
+ * materialize_average, convergence_info of CURRENT and AVERAGE and, when
+ * want_gaps, restart_candidate's distances to LAST and both normalized
+ * duality gaps (solver.cpp:372-393; the radius is computed on device from
+ * the distances, a zero radius gives a zero gap).  gaps_valid is 0 when a
+ * point is non-finite or out of its sign cone (the caller raises then). */
+typedef struct folp_gpu_period {
+  folp_gpu_eval current;
+  folp_gpu_eval average;
+  double avg_weight;
+  double dist_x[2]; /* sum (x - x_last)^2 of CURRENT, AVERAGE */
+  double dist_y[2]; /* sum (y - y_last)^2 of CURRENT, AVERAGE */
+  double gap[2];    /* restart-candidate duality gaps of CURRENT, AVERAGE */
+  int32_t gaps_valid;
+  int32_t pad;
+} folp_gpu_period;
+int folp_gpu_evaluation_period(folp_gpu_ctx* ctx, double omega,
+                               int32_t want_gaps, folp_gpu_period* out);
+
+/* Restart commit (solver.cpp:800-815): the new reference gap
+ * normalized_duality_gap(slot, radius, omega) when radius > 0 (else 0),
+ * then LAST = CURRENT = slot and the average cleared; one synchronisation. */
+int folp_gpu_restart_commit(folp_gpu_ctx* ctx, int32_t which, double radius,
+                            double omega, double* reference_gap);
 
 /* Runs PDHG iterations on device until loop->target steps were accepted
  * or the loop stopped (limit, non-finite, underflow).  Trials, step-size

@@ -1116,4 +1116,30 @@ int folp_port_adaptive_step(const folp_lp_c* lp, const double* x, const double* 
   return rc;
 }
 
+int folp_port_malitsky_pock_step(const folp_lp_c* lp, const double* x, const double* y,
+                                 double omega, double eta_prev, double theta_prev,
+                                 const folp_params_c* p, double* x_next, double* y_next,
+                                 double* eta_next, double* theta_next, int64_t* trials) {
+  if (!(eta_prev > 0.0) || !(theta_prev > 0.0))
+    return fail(FOLP_E_INVALID_ARGUMENT,
+                "malitsky_pock_step: needs positive previous step size and ratio");
+  Lp w;
+  TRY(lp_load(lp, &w));
+  double* xs = dcopy(x, w.n);
+  double* ys = dcopy(y, w.m);
+  int64_t lk = 0, lkt = 0;
+  double eta = eta_prev, theta = theta_prev;
+  int rc = mp_step(&w, xs, ys, omega, &eta, &theta, p, &lk, &lkt, trials);
+  if (rc == FOLP_OK) {
+    memcpy(x_next, xs, (size_t)w.n * sizeof(double));
+    memcpy(y_next, ys, (size_t)w.m * sizeof(double));
+    *eta_next = eta;
+    *theta_next = theta;
+  }
+  free(xs);
+  free(ys);
+  lp_free(&w);
+  return rc;
+}
+
 const char* folp_port_last_error(void) { return g_err; }

@@ -46,6 +46,11 @@ int folp_port_adaptive_step(const folp_lp_c* lp, const double* x,
                             double* eta_used, double* eta_hat_next,
                             int64_t* trials, double* movement_sq,
                             double* cross_term);
+int folp_port_malitsky_pock_step(const folp_lp_c* lp, const double* x,
+                                 const double* y, double omega, double eta_prev,
+                                 double theta_prev, const folp_params_c* params,
+                                 double* x_next, double* y_next, double* eta_next,
+                                 double* theta_next, int64_t* trials);
 const char* folp_port_last_error(void);
 
 #ifdef __cplusplus

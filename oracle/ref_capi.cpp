@@ -304,6 +304,25 @@ int folp_ref_adaptive_step(const folp_lp_c* lp_in, const double* x,
   });
 }
 
+int folp_ref_malitsky_pock_step(const folp_lp_c* lp_in, const double* x, const double* y,
+                                double omega, double eta_prev, double theta_prev,
+                                const folp_params_c* p, double* x_next, double* y_next,
+                                double* eta_next, double* theta_next, int64_t* trials) {
+  return guarded([&] {
+    const LinearProgram lp = to_lp(lp_in);
+    PrimalDualPoint z;
+    z.primal.assign(x, x + lp_in->num_cols);
+    z.dual.assign(y, y + lp_in->num_rows);
+    const MalitskyPockResult r =
+        malitsky_pock_step(lp, z, omega, eta_prev, theta_prev, to_params(p));
+    copy_vec(r.next.primal, x_next);
+    copy_vec(r.next.dual, y_next);
+    *eta_next = r.eta_next;
+    *theta_next = r.theta_next;
+    *trials = r.trials;
+  });
+}
+
 const char* folp_ref_last_error(void) { return g_err.c_str(); }
 
 // ---- reference instance generators (instance_gen.hpp) ---------------------

@@ -220,6 +220,9 @@ class Binding:
                                       C.c_int64, _f64p, _f64p, _f64p, _f64p, _i64p, _f64p,
                                       _f64p])
         f("last_error", C.c_char_p, [])
+        f("malitsky_pock_step", C.c_int, [C.POINTER(LpC), _f64p, _f64p, C.c_double, C.c_double,
+                                           C.c_double, C.POINTER(ParamsC), _f64p, _f64p, _f64p,
+                                           _f64p, _i64p])
         if hasattr(lib, prefix + "session_create"):
             f("session_create", C.c_int, [C.POINTER(LpC), C.POINTER(ParamsC), _f64p, _f64p,
                                            C.POINTER(C.c_void_p)])
@@ -299,6 +302,21 @@ class Binding:
 
     def session(self, lp: LP, p: Optional[dict] = None) -> "Session":
         return Session(self, lp, p or params())
+
+    def mp_step(self, lp: LP, x, y, omega: float, eta_prev: float, theta_prev: float,
+                p: Optional[dict] = None) -> dict:
+        lpc = lp.to_c()
+        pc = params_to_c(p or params())
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        xn = np.zeros(lp.num_cols)
+        yn = np.zeros(lp.num_rows)
+        en, tn = C.c_double(), C.c_double()
+        tr = C.c_int64()
+        self.check(self.malitsky_pock_step(C.byref(lpc), _f64(x), _f64(y), omega, eta_prev,
+                                           theta_prev, C.byref(pc), _f64(xn), _f64(yn),
+                                           C.byref(en), C.byref(tn), C.byref(tr)))
+        return dict(x=xn, y=yn, eta_next=en.value, theta_next=tn.value, trials=tr.value)
 
     def kx(self, lp: LP, x) -> np.ndarray:
         lpc = lp.to_c()

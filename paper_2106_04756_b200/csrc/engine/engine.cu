@@ -30,6 +30,8 @@
 #include "folp_gpu.h"
 #include "ops.cuh"
 
+#include <cooperative_groups.h>
+
 using namespace folpgpu;
 
 namespace {
@@ -321,7 +323,7 @@ int occupancy(const void* fn, int smem = 0) {
   return b;
 }
 
-constexpr int kResSlots = 64;
+constexpr int kResSlots = 96;
 constexpr int kCounters = 16;
 constexpr int kMaxGrid = 148 * 8;
 
@@ -343,18 +345,19 @@ struct folp_gpu_ctx {
   double *x[2], *y[2], *kx[2];
   double *avg_x, *avg_y;
   double *avgp_x, *avgp_y, *last_x, *last_y, *aux_x, *aux_y;
+  double *mp_ext, *mp_dy;  // Malitsky-Pock scratch
   double *kx_avg;   // K~ x of AVERAGE (filled by the duality gap)
   double *kx_aux;
   double *xr, *yr;  // reduced point scratch
-  double *g, *lo, *hi;
+  double *g[2], *lo[2], *hi[2];  // duality-gap scratch per candidate (CURRENT, AVERAGE)
   double *partials;
   unsigned* counters;
   double* res;      // small result slots
   double* res_h;    // pinned mirror
   DevState* st_d;
   DevState* st_h;   // pinned
-  NdgState* ndg_d;
-  NdgState* ndg_h;  // pinned
+  NdgState* ndg_d;  // [2]
+  NdgState* ndg_h;  // [2], pinned
   double *red_d, *grow_d;
   double *red_h, *grow_h;  // pinned
   int64_t table_cap = 0;
@@ -364,10 +367,11 @@ struct folp_gpu_ctx {
   bool norms_ready = false;
   double norm_q_sq = 0.0, norm_c_sq = 0.0;
   int max_giant = 0;
+  int bisect_grid = 0;
 
-  cudaGraphExec_t chunk_exec = nullptr;
-  bool graph_tried = false;
-  bool graph_ok = false;
+  cudaGraphExec_t chunk_exec[3] = {nullptr, nullptr, nullptr};  // per step policy
+  bool graph_tried[3] = {false, false, false};
+  bool graph_ok[3] = {false, false, false};
   int64_t launches = 0;
   bool profiling = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
@@ -482,6 +486,8 @@ struct folp_gpu_ctx {
     b.m1 = m1;
     b.n = n;
     b.a_terms = terms[0];
+    b.mp_ext = mp_ext;
+    b.mp_dy = mp_dy;
     b.st = st_d;
     b.red = red_d;
     b.grow = grow_d;
@@ -492,7 +498,8 @@ struct folp_gpu_ctx {
 
   ~folp_gpu_ctx() {
     if (device >= 0) cudaSetDevice(device);
-    if (chunk_exec) cudaGraphExecDestroy(chunk_exec);
+    for (auto& e : chunk_exec)
+      if (e) cudaGraphExecDestroy(e);
     for (void* p : owned) cudaFree(p);
     for (void* p : rows.owned) cudaFree(p);
     for (void* p : cols.owned) cudaFree(p);
@@ -660,9 +667,396 @@ void zero_average(folp_gpu_ctx* c) {
   c->st_h->pending = 0.0;
 }
 
-// Builds the chunk graph: WHILE(running) { kernel A ; kernel B }.
-void build_chunk_graph(folp_gpu_ctx* c) {
-  c->graph_tried = true;
+// ---------------------------------------------------------------------
+// Evaluation period (solver.cpp:751-816) as one asynchronous sequence.
+// Result-slot blocks of the period's reductions:
+constexpr int kResEval[2] = {32, 44};  // [0] c'x [1] q'y [2] non-finite [3] primal^2
+                                        // [4] dual^2 [5] bound terms [6] inf product
+                                        // [10] dual objective (ordered)
+constexpr int kResNorms = 56;           // ||q||^2, ||c||^2
+constexpr int kResDist[2] = {60, 62};   // sum dx^2, sum dy^2 to LAST
+constexpr int kResNdg[2] = {64, 74};    // duality-gap setup sums (10 each)
+constexpr int kResUsed = 84;
+static_assert(kResUsed <= kResSlots, "result slots");
+
+// Bracket of one normalized_duality_gap evaluation from its setup sums
+// (solver.cpp:318-355).  The radius is either given or the weighted
+// distance to LAST of restart_candidate (solver.cpp:378-386; a zero radius
+// gives a zero gap there without evaluating).
+__global__ void k_ndg_init(NdgState* st, const double* sums, const double* dist, double radius,
+                           double omega) {
+  NdgState s{};
+  s.omega = omega;
+  s.winv = 1.0 / omega;
+  const double r = dist != nullptr ? sqrt(omega * dist[0] + dist[1] / omega) : radius;
+  s.radius = r;
+  if (r == 0.0 || sums[0] + sums[5] == 0.0) {  // solver.cpp:324
+    s.done = 1;
+    s.result = 0.0;
+    *st = s;
+    return;
+  }
+  if (sums[2] + sums[7] == 0.0) {  // bounded corner, solver.cpp:339-341
+    const double norm_sq = sums[3] + sums[8];
+    if (sqrt(norm_sq) <= r * (1.0 + 1e-12)) {
+      s.done = 1;
+      s.result = (sums[4] + sums[9]) / r;
+      *st = s;
+      return;
+    }
+  }
+  s.nu_lo = 0.0;
+  s.nu_hi = sqrt(sums[1] + sums[6]) / r;
+  ndg_candidates(s.nu_lo, s.nu_hi, s.nu);
+  ndg_reciprocals(&s);
+  *st = s;
+}
+
+// Tree-mode bisection of up to two duality gaps in ONE cooperative launch
+// (solver.cpp:356-368).  Every pass evaluates the 7 midpoints of the next
+// 3 levels per scratch set; the block partials are published, the grid
+// synchronizes once, and every block sums the partials in the same order
+// and replays the same decisions, so the bisection state never leaves
+// shared memory until the end.  Replaces up to ~70 launches per period.
+constexpr int kBisectThreads = 512;
+constexpr int kBisectVals = 2 * kNuCands;  // ||d||_w^2 and g'd per midpoint
+
+struct BisectArgs {
+  int64_t n, total;
+  const double* g[2];
+  const double* lo[2];
+  const double* hi[2];
+  NdgState* ns[2];
+  int active[2];
+  double* partials;  // [2 parity][2 sets][kBisectVals][grid]
+};
+
+__global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ NdgState st[2];
+  __shared__ double wsum[kBisectThreads / 32][2][kBisectVals];
+  __shared__ double tot[2][kBisectVals];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = gridDim.x;
+  if (tid < 2) {
+    st[tid] = *a.ns[tid];
+    if (!a.active[tid]) st[tid].done = 1;
+  }
+  __syncthreads();
+  for (int parity = 0;; parity ^= 1) {
+    const bool run[2] = {st[0].done == 0, st[1].done == 0};
+    if (!run[0] && !run[1]) break;  // same state in every block
+    double acc[2][kBisectVals];
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int k = 0; k < kBisectVals; ++k) acc[s][k] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!run[s]) continue;
+      const double* g = a.g[s];
+      const double* lo = a.lo[s];
+      const double* hi = a.hi[s];
+      const double omega = st[s].omega, winv = st[s].winv;
+      for (int64_t i = static_cast<int64_t>(blockIdx.x) * kBisectThreads + tid; i < a.total;
+           i += static_cast<int64_t>(nb) * kBisectThreads) {
+        const double gs = g[i];
+        const bool primal = i < a.n;
+        const double w = primal ? omega : winv;
+        const double los = lo[i];
+        const double his = primal ? hi[i] : INFINITY;
+        const double* rcp = primal ? st[s].rcp_primal : st[s].rcp_dual;
+#pragma unroll
+        for (int p = 0; p < kNuCands; ++p) {
+          const double d = ref_min(ref_max(gs * rcp[p], los), his);
+          acc[s][2 * p] += w * d * d;
+          acc[s][2 * p + 1] += gs * d;
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int k = 0; k < kBisectVals; ++k) {
+        double v = acc[s][k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) wsum[warp][s][k] = v;
+      }
+    __syncthreads();
+    double* part = a.partials + static_cast<size_t>(parity) * 2 * kBisectVals * nb;
+    if (tid < 2 * kBisectVals) {
+      const int s = tid / kBisectVals, k = tid % kBisectVals;
+      double v = 0.0;
+      for (int w = 0; w < kBisectThreads / 32; ++w) v += wsum[w][s][k];
+      part[static_cast<size_t>(tid) * nb + blockIdx.x] = v;
+    }
+    grid.sync();
+    // every block: totals in block order, one warp per (set, value) pair
+    for (int pair = warp; pair < 2 * kBisectVals; pair += kBisectThreads / 32) {
+      const double* src = part + static_cast<size_t>(pair) * nb;
+      double v = 0.0;
+      for (int b = lane; b < nb; b += 32) v += src[b];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) tot[pair / kBisectVals][pair % kBisectVals] = v;
+    }
+    __syncthreads();
+    if (tid < 2 && run[tid]) {
+      double nsq[kNuCands], gd[kNuCands];
+      for (int p = 0; p < kNuCands; ++p) {
+        nsq[p] = tot[tid][2 * p];
+        gd[p] = tot[tid][2 * p + 1];
+      }
+      ndg_replay(&st[tid], nsq, gd, kNuLevels);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid < 2 && a.active[tid]) *a.ns[tid] = st[tid];
+}
+
+void enqueue_average(folp_gpu_ctx* c) {
+  DevState* st = c->st_h;
+  OpAverage op{};
+  op.n = c->n;
+  op.m1 = c->m1;
+  op.x = c->cur_x();
+  op.y = c->cur_y();
+  op.ax = c->avg_x;
+  op.ay = c->avg_y;
+  op.l = c->lw;
+  op.u = c->uw;
+  op.pending = st->pending;
+  op.copy_current = st->avg_weight <= 0.0 ? 1 : 0;
+  op.inv = st->avg_weight > 0.0 ? 1.0 / st->avg_weight : 0.0;
+  op.out_x = c->avgp_x;
+  op.out_y = c->avgp_y;
+  c->ew(c->n + c->m, op, 6);
+  st->pending = 0.0;
+  c->push_state();
+}
+
+// convergence_info reductions of a slot into the block at res[base].
+void enqueue_evaluate(folp_gpu_ctx* c, int which, int raw, int base) {
+  OpEvalPoint op{};
+  op.raw = raw != 0 ? 1 : 0;
+  op.n = c->n;
+  op.m = c->m;
+  op.xs = c->slot_x(which);
+  op.ys = c->slot_y(which);
+  op.d1 = c->d1;
+  op.d2 = c->d2;
+  op.l = c->l0;
+  op.u = c->u0;
+  op.c = c->c0;
+  op.q = c->q0;
+  op.xr = c->xr;
+  op.yr = c->yr;
+  op.result = c->res + base;
+  c->ew(c->n + c->m, op, 7);
+  c->seg(c->rows, c->csr_orig, EpiPrimalResidual{c->xr, c->q0, c->m1, c->res + base + 3}, 8);
+  EpiDualResidual dres{c->yr, c->c0, c->l0, c->u0, c->res + base + 4};
+  dres.q_dot_y = c->res + base + 1;
+  dres.constant = c->objective_constant;
+  dres.dual_objective = c->res + base + 10;
+  c->seg(c->cols, c->csc_orig, dres, 9);
+  if (!c->norms_ready) {
+    c->ew(c->m, OpNormSq{c->q0, c->res + kResNorms}, 10);
+    c->ew(c->n, OpNormSq{c->c0, c->res + kResNorms + 1}, 11);
+  }
+}
+
+// Reads a block written by enqueue_evaluate (after the sync).
+void read_evaluate(folp_gpu_ctx* c, int base, folp_gpu_eval* out) {
+  if (!c->norms_ready) {
+    c->norm_q_sq = c->res_h[kResNorms];
+    c->norm_c_sq = c->res_h[kResNorms + 1];
+    c->norms_ready = true;
+  }
+  const double* r = c->res_h + base;
+  out->c_dot_x = r[0];
+  out->q_dot_y = r[1];
+  out->nonfinite = r[2] != 0.0 ? 1 : 0;
+  out->primal_sq = r[3];
+  out->dual_sq = r[4];
+  out->bound_terms = r[5];
+  out->infinite_product = r[6] != 0.0 ? 1 : 0;
+  out->norm_q = std::sqrt(c->norm_q_sq);
+  out->norm_c = std::sqrt(c->norm_c_sq);
+  // lp_model.cpp:154-163; ordered mode folded it term by term on device
+  out->dual_objective =
+      c->ordered ? r[10] : (out->q_dot_y + c->objective_constant) + out->bound_terms;
+}
+
+void enqueue_distance(folp_gpu_ctx* c, int a, int b, int base) {
+  OpDistance op{c->n, c->slot_x(a), c->slot_x(b), c->slot_y(a), c->slot_y(b), c->res + base};
+  c->ew(c->n + c->m, op, 12);
+}
+
+// g, lo, hi of a slot into scratch set s with the setup sums
+// (solver.cpp:300-342); Kx of the point is cached for CURRENT and kept for
+// AVERAGE (a restart to it reuses it).
+void enqueue_ndg_setup(folp_gpu_ctx* c, int which, int s, double omega) {
+  const int64_t n = c->n, m = c->m;
+  double* px = c->slot_x(which);
+  double* py = c->slot_y(which);
+  double* sums = c->res + kResNdg[s];
+  EpiNdgPrimal ep{py, px, c->cw, c->lw, c->uw, omega, c->g[s], c->lo[s], c->hi[s], sums};
+  c->seg(c->cols, c->csc_work, ep, 13, 0);
+  EpiNdgDual ed{};
+  ed.x = px;
+  ed.y = py;
+  ed.q = c->qw;
+  ed.m1 = c->m1;
+  ed.winv = 1.0 / omega;
+  ed.g = c->g[s] + n;
+  ed.lo = c->lo[s] + n;
+  ed.result = sums;
+  ed.primal_terms = c->terms[0];
+  ed.n = n;
+  if (which == FOLP_PT_CURRENT && c->kx_valid) {
+    ed.kx_out = nullptr;
+    c->ew(m, OpNdgDualCached{c->kx[c->st_h->cur], ed}, 14, 1);
+  } else {
+    ed.kx_out = which == FOLP_PT_AVERAGE ? c->kx_avg : c->kx_aux;
+    c->seg(c->rows, c->csr_work, ed, 14, 1);
+  }
+}
+
+void enqueue_ndg_init(folp_gpu_ctx* c, int s, int dist_base, double radius, double omega) {
+  const double* dist = dist_base >= 0 ? c->res + dist_base : nullptr;
+  k_ndg_init<<<1, 1, 0, c->stream>>>(c->ndg_d + s, c->res + kResNdg[s], dist, radius, omega);
+  ++c->launches;
+  CK(cudaGetLastError());
+}
+
+// One bisection pass (3 levels in tree mode, 1 in ordered mode); a no-op
+// once the bisection of that scratch set is done.
+void enqueue_ndg_pass(folp_gpu_ctx* c, int s, double omega) {
+  OpNdgPass pass{};
+  pass.n = c->n;
+  pass.total = c->n + c->m;
+  pass.g = c->g[s];
+  pass.lo = c->lo[s];
+  pass.hi = c->hi[s];
+  pass.omega = omega;
+  pass.winv = 1.0 / omega;
+  pass.ns = c->ndg_d + s;
+  c->ew(c->n + c->m, pass, 15);
+}
+
+// Passes before the first look: 42 tree levels / 48 ordered levels cover
+// a typical evaluation (the bracket starts at ||g|| / r, the stop is 1e-10 r).
+int ndg_first_batch(const folp_gpu_ctx* c) { return c->ordered ? 48 : 14; }
+int ndg_next_batch(const folp_gpu_ctx* c) { return c->ordered ? 16 : 5; }
+
+// Starts the bisections of the wanted scratch sets and queues the readback
+// of their states: tree mode runs them to the end in one cooperative
+// launch, ordered mode (one reference level per pass) queues a first batch.
+void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]);
+
+void fetch_ndg(folp_gpu_ctx* c) {
+  CK(cudaMemcpyAsync(c->ndg_h, c->ndg_d, 2 * sizeof(NdgState), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// After a synchronized fetch: runs more passes on the scratch sets still
+// bisecting until all wanted ones are done.
+void finish_ndg(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]) {
+  for (int round = 0; round < 256; ++round) {
+    bool pending = false;
+    for (int s = 0; s < 2; ++s) pending = pending || (want[s] && !c->ndg_h[s].done);
+    if (!pending) return;
+    const int batch = ndg_next_batch(c);
+    for (int i = 0; i < batch; ++i) {
+      for (int s = 0; s < 2; ++s) {
+        if (want[s] && !c->ndg_h[s].done) enqueue_ndg_pass(c, s, omega[s]);
+      }
+    }
+    fetch_ndg(c);
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  throw EngineError(FOLP_E_RUNTIME, "normalized_duality_gap: bisection stalled");
+}
+
+void check_ndg_args(double radius, double omega) {
+  if (!(radius > 0.0)) {
+    throw EngineError(FOLP_E_NONPOSITIVE_RADIUS, "normalized_duality_gap: radius must be > 0");
+  }
+  if (!(omega > 0.0)) {
+    throw EngineError(FOLP_E_NONPOSITIVE_WEIGHT, "normalized_duality_gap: omega must be > 0");
+  }
+}
+
+void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]) {
+  if (c->ordered) {
+    for (int i = 0, e = ndg_first_batch(c); i < e; ++i) {
+      for (int s = 0; s < 2; ++s) {
+        if (want[s]) enqueue_ndg_pass(c, s, omega[s]);
+      }
+    }
+  } else {
+    BisectArgs a{};
+    a.n = c->n;
+    a.total = c->n + c->m;
+    for (int s = 0; s < 2; ++s) {
+      a.g[s] = c->g[s];
+      a.lo[s] = c->lo[s];
+      a.hi[s] = c->hi[s];
+      a.ns[s] = c->ndg_d + s;
+      a.active[s] = want[s] ? 1 : 0;
+    }
+    a.partials = c->partials;
+    int& grid = c->bisect_grid;
+    if (grid == 0) {  // co-resident by construction (cooperative launch)
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ndg_bisect, kBisectThreads, 0));
+      grid = std::max(1, std::min(c->sms * std::max(occ, 1), std::min(c->sms * 2, kMaxGrid / 2)));
+    }
+    void* args[] = {&a};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ndg_bisect), dim3(grid),
+                                   dim3(kBisectThreads), args, 0, c->stream));
+    ++c->launches;
+  }
+  fetch_ndg(c);
+}
+
+// restart_to without the sync: copies of the restart point (solver.cpp:805-813).
+void enqueue_restart(folp_gpu_ctx* c, int which, int reset_average) {
+  DevState* st = c->st_h;
+  if (which != FOLP_PT_CURRENT) {
+    copy_d2d(c, c->cur_x(), c->slot_x(which), c->n);
+    copy_d2d(c, c->cur_y(), c->slot_y(which), c->m);
+    if (which == FOLP_PT_AVERAGE) {
+      copy_d2d(c, c->kx[st->cur], c->kx_avg, c->m);
+      c->kx_valid = true;
+    } else {
+      refresh_kx(c);
+    }
+  }
+  copy_d2d(c, c->last_x, c->cur_x(), c->n);
+  copy_d2d(c, c->last_y, c->cur_y(), c->m);
+  if (reset_average) zero_average(c);
+  c->push_state();
+}
+
+// One trial slot of a step policy: adaptive / constant = {A; B},
+// Malitsky-Pock = {MP-A (first trial only); MP-E; MP-B; MP-C}.
+void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
+  if (policy == FOLP_STEP_MALITSKY_POCK) {
+    c->seg(c->cols, c->csc_work, EpiMpPrimal{b}, 2, 0);
+    c->ew(c->n, OpMpExtrapolate{b}, 5, 1);
+    c->seg(c->rows, c->csr_work, EpiMpDual{b}, 3, 1);
+    c->seg(c->cols, c->csc_work, EpiMpCheck{b}, 6, 0);
+  } else {
+    c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2, 0);
+    c->seg(c->rows, c->csr_work, EpiDual{b}, 3, 1);
+  }
+}
+
+// Builds the chunk graph of a policy: WHILE(running) { trial slot }.
+void build_chunk_graph(folp_gpu_ctx* c, int policy) {
+  c->graph_tried[policy] = true;
   if (std::getenv("FOLP_NO_GRAPH") != nullptr) return;
   cudaGraph_t graph = nullptr;
   if (cudaGraphCreate(&graph, 0) != cudaSuccess) return;
@@ -684,24 +1078,24 @@ void build_chunk_graph(folp_gpu_ctx* c) {
                                        cudaStreamCaptureModeRelaxed) == cudaSuccess;
     if (ok) {
       const LoopBufs b = c->loop_bufs(handle, 1);
+      const int64_t before = c->launches;
       try {
-        c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2, 0);
-        c->seg(c->rows, c->csr_work, EpiDual{b}, 3, 1);
-        c->launches -= 2;
+        launch_slot(c, policy, b);
       } catch (...) {
         ok = false;
       }
+      c->launches = before;
       cudaGraph_t captured = nullptr;
       ok = (cudaStreamEndCapture(c->stream, &captured) == cudaSuccess) && ok;
     }
   }
-  if (ok) ok = cudaGraphInstantiate(&c->chunk_exec, graph, 0) == cudaSuccess;
+  if (ok) ok = cudaGraphInstantiate(&c->chunk_exec[policy], graph, 0) == cudaSuccess;
   cudaGetLastError();  // clear a failed optional path
   if (graph) cudaGraphDestroy(graph);
-  c->graph_ok = ok;
-  if (!ok && c->chunk_exec) {
-    cudaGraphExecDestroy(c->chunk_exec);
-    c->chunk_exec = nullptr;
+  c->graph_ok[policy] = ok;
+  if (!ok && c->chunk_exec[policy]) {
+    cudaGraphExecDestroy(c->chunk_exec[policy]);
+    c->chunk_exec[policy] = nullptr;
   }
 }
 
@@ -807,10 +1201,13 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     c->last_x = vn(); c->last_y = vm();
     c->aux_x = vn(); c->aux_y = vm();
     c->kx_avg = vm(); c->kx_aux = vm();
+    c->mp_ext = vn(); c->mp_dy = vm();
     c->xr = vn(); c->yr = vm();
-    c->g = c->alloc<double>(n + m);
-    c->lo = c->alloc<double>(n + m);
-    c->hi = vn();
+    for (int s = 0; s < 2; ++s) {
+      c->g[s] = c->alloc<double>(n + m);
+      c->lo[s] = c->alloc<double>(n + m);
+      c->hi[s] = vn();
+    }
     c->partials = c->alloc<double>(static_cast<size_t>(kMaxGrid + c->max_giant + 8) * kMaxAcc);
     if (c->ordered) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);
@@ -823,8 +1220,8 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     c->st_d = c->alloc<DevState>(1);
     CK(cudaMallocHost(&c->st_h, sizeof(DevState)));
     std::memset(c->st_h, 0, sizeof(DevState));
-    c->ndg_d = c->alloc<NdgState>(1);
-    CK(cudaMallocHost(&c->ndg_h, sizeof(NdgState)));
+    c->ndg_d = c->alloc<NdgState>(2);
+    CK(cudaMallocHost(&c->ndg_h, 2 * sizeof(NdgState)));
     c->table_cap = 4096;
     c->red_d = c->alloc<double>(c->table_cap);
     c->grow_d = c->alloc<double>(c->table_cap);
@@ -1004,189 +1401,105 @@ int folp_gpu_get_reduced_point(folp_gpu_ctx* c, int32_t which, double* x, double
 int folp_gpu_materialize_average(folp_gpu_ctx* c, double* weight) {
   return guarded([&] {
     set_device(c);
-    DevState* st = c->st_h;
-    OpAverage op{};
-    op.n = c->n;
-    op.m1 = c->m1;
-    op.x = c->cur_x();
-    op.y = c->cur_y();
-    op.ax = c->avg_x;
-    op.ay = c->avg_y;
-    op.l = c->lw;
-    op.u = c->uw;
-    op.pending = st->pending;
-    op.copy_current = st->avg_weight <= 0.0 ? 1 : 0;
-    op.inv = st->avg_weight > 0.0 ? 1.0 / st->avg_weight : 0.0;
-    op.out_x = c->avgp_x;
-    op.out_y = c->avgp_y;
-    c->ew(c->n + c->m, op, 6);
-    st->pending = 0.0;
-    c->push_state();
+    enqueue_average(c);
     CK(cudaStreamSynchronize(c->stream));
-    if (weight) *weight = st->avg_weight;
+    if (weight) *weight = c->st_h->avg_weight;
   });
 }
 
 int folp_gpu_evaluate(folp_gpu_ctx* c, int32_t which, int32_t raw, folp_gpu_eval* out) {
   return guarded([&] {
     set_device(c);
-    OpEvalPoint op{};
-    op.raw = raw != 0 ? 1 : 0;
-    op.n = c->n;
-    op.m = c->m;
-    op.xs = c->slot_x(which);
-    op.ys = c->slot_y(which);
-    op.d1 = c->d1;
-    op.d2 = c->d2;
-    op.l = c->l0;
-    op.u = c->u0;
-    op.c = c->c0;
-    op.q = c->q0;
-    op.xr = c->xr;
-    op.yr = c->yr;
-    op.result = c->res + 8;
-    c->ew(c->n + c->m, op, 7);
-    c->seg(c->rows, c->csr_orig, EpiPrimalResidual{c->xr, c->q0, c->m1, c->res + 11}, 8);
-    EpiDualResidual dres{c->yr, c->c0, c->l0, c->u0, c->res + 12};
-    dres.q_dot_y = c->res + 9;
-    dres.constant = c->objective_constant;
-    dres.dual_objective = c->res + 18;
-    c->seg(c->cols, c->csc_orig, dres, 9);
-    if (!c->norms_ready) {
-      c->ew(c->m, OpNormSq{c->q0, c->res + 15}, 10);
-      c->ew(c->n, OpNormSq{c->c0, c->res + 16}, 11);
-    }
-    c->fetch_res(19);
-    if (!c->norms_ready) {
-      c->norm_q_sq = c->res_h[15];
-      c->norm_c_sq = c->res_h[16];
-      c->norms_ready = true;
-    }
-    const double* r = c->res_h;
-    out->c_dot_x = r[8];
-    out->q_dot_y = r[9];
-    out->nonfinite = r[10] != 0.0 ? 1 : 0;
-    out->primal_sq = r[11];
-    out->dual_sq = r[12];
-    out->bound_terms = r[13];
-    out->infinite_product = r[14] != 0.0 ? 1 : 0;
-    out->norm_q = std::sqrt(c->norm_q_sq);
-    out->norm_c = std::sqrt(c->norm_c_sq);
-    // lp_model.cpp:154-163; ordered mode folded it term by term on device
-    out->dual_objective =
-        c->ordered ? r[18] : (out->q_dot_y + c->objective_constant) + out->bound_terms;
+    enqueue_evaluate(c, which, raw, kResEval[0]);
+    c->fetch_res(kResUsed);
+    read_evaluate(c, kResEval[0], out);
   });
 }
 
 int folp_gpu_distance(folp_gpu_ctx* c, int32_t a, int32_t b, double* sx, double* sy) {
   return guarded([&] {
     set_device(c);
-    OpDistance op{c->n, c->slot_x(a), c->slot_x(b), c->slot_y(a), c->slot_y(b), c->res + 20};
-    c->ew(c->n + c->m, op, 12);
-    c->fetch_res(22);
-    *sx = c->res_h[20];
-    *sy = c->res_h[21];
+    enqueue_distance(c, a, b, kResDist[0]);
+    c->fetch_res(kResUsed);
+    *sx = c->res_h[kResDist[0]];
+    *sy = c->res_h[kResDist[0] + 1];
   });
 }
 
 int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, double* gap) {
   return guarded([&] {
     set_device(c);
-    if (!(radius > 0.0)) {
-      throw EngineError(FOLP_E_NONPOSITIVE_RADIUS, "normalized_duality_gap: radius must be > 0");
-    }
-    if (!(omega > 0.0)) {
+    check_ndg_args(radius, omega);
+    enqueue_ndg_setup(c, which, 0, omega);
+    enqueue_ndg_init(c, 0, -1, radius, omega);
+    enqueue_ndg_solve(c, {true, false}, {omega, omega});
+    CK(cudaStreamSynchronize(c->stream));
+    finish_ndg(c, {true, false}, {omega, omega});
+    *gap = c->ndg_h[0].result;
+  });
+}
+
+int folp_gpu_evaluation_period(folp_gpu_ctx* c, double omega, int32_t want_gaps,
+                               folp_gpu_period* out) {
+  return guarded([&] {
+    set_device(c);
+    if (want_gaps && !(omega > 0.0)) {
       throw EngineError(FOLP_E_NONPOSITIVE_WEIGHT, "normalized_duality_gap: omega must be > 0");
     }
-    const int64_t n = c->n, m = c->m;
-    double* px = c->slot_x(which);
-    double* py = c->slot_y(which);
-    // g, lo, hi over the primal coordinates (K~'y)
-    EpiNdgPrimal ep{py, px, c->cw, c->lw, c->uw, omega, c->g, c->lo, c->hi, c->res + 24};
-    c->seg(c->cols, c->csc_work, ep, 13, 0);
-    // ... and the dual ones (K~x; cached for CURRENT)
-    EpiNdgDual ed{};
-    ed.x = px;
-    ed.y = py;
-    ed.q = c->qw;
-    ed.m1 = c->m1;
-    ed.winv = 1.0 / omega;
-    ed.g = c->g + n;
-    ed.lo = c->lo + n;
-    ed.result = c->res + 24;
-    ed.primal_terms = c->terms[0];
-    ed.n = n;
-    if (which == FOLP_PT_CURRENT && c->kx_valid) {
-      ed.kx_out = nullptr;
-      c->ew(m, OpNdgDualCached{c->kx[c->st_h->cur], ed}, 14, 1);
-    } else {
-      ed.kx_out = which == FOLP_PT_AVERAGE ? c->kx_avg : c->kx_aux;
-      c->seg(c->rows, c->csr_work, ed, 14, 1);
-    }
-    c->fetch_res(34);
-    const double* r = c->res_h;
-    const double any = r[24] + r[29];
-    if (any == 0.0) {
-      *gap = 0.0;  // solver.cpp:324
-      return;
-    }
-    const double gsq = r[25] + r[30];
-    const bool bounded = (r[26] + r[31]) == 0.0;
-    if (bounded) {
-      const double norm_sq = r[27] + r[32];
-      if (std::sqrt(norm_sq) <= radius * (1.0 + 1e-12)) {
-        *gap = (r[28] + r[33]) / radius;  // solver.cpp:339-341
-        return;
+    const int slots[2] = {FOLP_PT_CURRENT, FOLP_PT_AVERAGE};
+    enqueue_average(c);
+    for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s]);
+    if (want_gaps) {
+      for (int s = 0; s < 2; ++s) {
+        enqueue_distance(c, slots[s], FOLP_PT_LAST, kResDist[s]);
+        enqueue_ndg_setup(c, slots[s], s, omega);
+        enqueue_ndg_init(c, s, kResDist[s], 0.0, omega);
       }
+      enqueue_ndg_solve(c, {true, true}, {omega, omega});
     }
-    // bisection on nu (solver.cpp:356-368), 4 levels per pass
-    NdgState* h = c->ndg_h;
-    std::memset(h, 0, sizeof(NdgState));
-    h->nu_lo = 0.0;
-    h->nu_hi = std::sqrt(gsq) / radius;
-    h->radius = radius;
-    ndg_candidates(h->nu_lo, h->nu_hi, h->nu);
-    CK(cudaMemcpyAsync(c->ndg_d, h, sizeof(NdgState), cudaMemcpyHostToDevice, c->stream));
-    OpNdgPass pass{};
-    pass.n = n;
-    pass.total = n + m;
-    pass.g = c->g;
-    pass.lo = c->lo;
-    pass.hi = c->hi;
-    pass.omega = omega;
-    pass.winv = 1.0 / omega;
-    pass.ns = c->ndg_d;
-    int batch = c->ordered ? 48 : 14;  // levels before the first look: 48 / 42
-    for (int round = 0; round < 256; ++round) {
-      for (int i = 0; i < batch; ++i) c->ew(n + m, pass, 15);
-      CK(cudaMemcpyAsync(h, c->ndg_d, sizeof(NdgState), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      if (h->done) break;
-      batch = c->ordered ? 16 : 5;
+    c->fetch_res(kResUsed);
+    read_evaluate(c, kResEval[0], &out->current);
+    read_evaluate(c, kResEval[1], &out->average);
+    out->avg_weight = c->st_h->avg_weight;
+    out->gaps_valid = 0;
+    for (int s = 0; s < 2; ++s) {
+      out->dist_x[s] = want_gaps ? c->res_h[kResDist[s]] : 0.0;
+      out->dist_y[s] = want_gaps ? c->res_h[kResDist[s] + 1] : 0.0;
+      out->gap[s] = 0.0;
     }
-    if (!h->done) throw EngineError(FOLP_E_RUNTIME, "normalized_duality_gap: bisection stalled");
-    *gap = h->result;
+    // a non-finite or out-of-cone point ends the solve before any gap is used
+    const bool bad = out->current.nonfinite || out->current.infinite_product ||
+                     out->average.nonfinite || out->average.infinite_product;
+    if (!want_gaps || bad) return;
+    finish_ndg(c, {true, true}, {omega, omega});
+    for (int s = 0; s < 2; ++s) out->gap[s] = c->ndg_h[s].result;
+    out->gaps_valid = 1;
+  });
+}
+
+int folp_gpu_restart_commit(folp_gpu_ctx* c, int32_t which, double radius, double omega,
+                            double* reference_gap) {
+  return guarded([&] {
+    set_device(c);
+    const bool gap = radius > 0.0;
+    if (gap) {
+      check_ndg_args(radius, omega);
+      enqueue_ndg_setup(c, which, 0, omega);
+      enqueue_ndg_init(c, 0, -1, radius, omega);
+      enqueue_ndg_solve(c, {true, false}, {omega, omega});
+    }
+    // the passes read only the scratch set, so the restart copies go behind them
+    enqueue_restart(c, which, 1);
+    CK(cudaStreamSynchronize(c->stream));
+    if (gap) finish_ndg(c, {true, false}, {omega, omega});
+    if (reference_gap) *reference_gap = gap ? c->ndg_h[0].result : 0.0;
   });
 }
 
 int folp_gpu_restart_to(folp_gpu_ctx* c, int32_t which, int32_t reset_average) {
   return guarded([&] {
     set_device(c);
-    DevState* st = c->st_h;
-    if (which != FOLP_PT_CURRENT) {
-      copy_d2d(c, c->cur_x(), c->slot_x(which), c->n);
-      copy_d2d(c, c->cur_y(), c->slot_y(which), c->m);
-      if (which == FOLP_PT_AVERAGE) {
-        copy_d2d(c, c->kx[st->cur], c->kx_avg, c->m);
-        c->kx_valid = true;
-      } else {
-        refresh_kx(c);
-      }
-    }
-    copy_d2d(c, c->last_x, c->cur_x(), c->n);
-    copy_d2d(c, c->last_y, c->cur_y(), c->m);
-    if (reset_average) zero_average(c);
-    c->push_state();
+    enqueue_restart(c, which, reset_average);
     CK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1204,10 +1517,12 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
   return guarded([&] {
     set_device(c);
     if (loop->target < 1) throw std::invalid_argument("run_chunk: target must be >= 1");
-    if (loop->policy != FOLP_STEP_ADAPTIVE && loop->policy != FOLP_STEP_CONSTANT) {
-      throw std::invalid_argument("run_chunk: policy not handled by the fused loop");
+    const int policy = loop->policy;
+    if (policy != FOLP_STEP_ADAPTIVE && policy != FOLP_STEP_CONSTANT &&
+        policy != FOLP_STEP_MALITSKY_POCK) {
+      throw std::invalid_argument("run_chunk: unknown step policy");
     }
-    if (!c->kx_valid) refresh_kx(c);
+    if (policy != FOLP_STEP_MALITSKY_POCK && !c->kx_valid) refresh_kx(c);
     if (loop->target > c->table_cap) {
       throw std::invalid_argument("run_chunk: target above the factor-table capacity");
     }
@@ -1239,22 +1554,24 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     st->eta = loop->eta;
     st->eta_hat = loop->eta;
     st->slots = 0;
+    st->mp_theta = loop->theta;
+    st->mp_break = loop->mp_breaking_factor;
+    st->mp_down = loop->mp_downscaling_factor;
+    st->mp_interp = loop->mp_interpolation_coefficient;
     c->push_state();
-    if (!c->graph_tried) build_chunk_graph(c);
+    if (!c->graph_tried[policy]) build_chunk_graph(c, policy);
+    const int per_slot = policy == FOLP_STEP_MALITSKY_POCK ? 4 : 2;
     if (c->profiling) CK(cudaEventRecord(c->ev0, c->stream));
-    if (c->graph_ok) {
-      CK(cudaGraphLaunch(c->chunk_exec, c->stream));
-      c->launches += 2 * 1;  // refined below from the slot count
+    if (c->graph_ok[policy]) {
+      CK(cudaGraphLaunch(c->chunk_exec[policy], c->stream));
     } else {
       // Plain stream launches: enough slots for the target plus a few
       // retries, then look at the state and continue if needed.
       const LoopBufs b = c->loop_bufs(cudaGraphConditionalHandle{}, 0);
       int64_t remaining = loop->target;
       for (;;) {
-        for (int64_t s = 0; s < remaining + 2; ++s) {
-          c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2, 0);
-          c->seg(c->rows, c->csr_work, EpiDual{b}, 3, 1);
-        }
+        for (int64_t s = 0; s < remaining + 2; ++s) launch_slot(c, policy, b);
+        c->launches -= per_slot * (remaining + 2);
         CK(cudaMemcpyAsync(st, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (!st->running) break;
@@ -1263,7 +1580,8 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     }
     if (c->profiling) CK(cudaEventRecord(c->ev1, c->stream));
     c->pull_state();
-    if (c->graph_ok) c->launches += 2 * st->slots - 2;
+    c->launches += per_slot * st->slots;
+    if (policy == FOLP_STEP_MALITSKY_POCK) c->kx_valid = false;  // Kx cache not kept
     if (c->profiling) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
@@ -1278,7 +1596,10 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     loop->violations = st->violations;
     loop->ledger_k = st->ledger_k;
     loop->ledger_kt = st->ledger_kt;
-    loop->eta = st->policy == FOLP_STEP_ADAPTIVE ? st->eta_hat : loop->eta;
+    loop->eta = st->policy == FOLP_STEP_ADAPTIVE ? st->eta_hat
+              : st->policy == FOLP_STEP_MALITSKY_POCK ? st->eta
+                                                      : loop->eta;
+    loop->theta = st->mp_theta;
     loop->last_eta_used = st->last_eta_used;
     loop->avg_weight = st->avg_weight;
     loop->last_movement = st->movement;

@@ -59,6 +59,11 @@ struct DevState {
   double bad_a;      // non-finite x' entries of the current trial
   double cross;      // last trial diagnostics
   double movement;
+  // Malitsky-Pock policy (solver.cpp:202-275)
+  double mp_theta;   // theta of the last accepted step
+  double mp_eta_hat; // candidate step of the current trial
+  double mp_dy_sq;   // ||dy||^2 of the current trial
+  double mp_break, mp_down, mp_interp;
 };
 
 // a[i] for i in {0, 1} without dynamic indexing (which would force the
@@ -85,6 +90,8 @@ struct LoopBufs {
   const double* red;   // per-iteration factor tables of the chunk
   const double* grow;
   const double* a_terms;  // ordered mode: kernel A's omega*dx*dx terms
+  double* mp_ext;         // Malitsky-Pock: extrapolated primal [n]
+  double* mp_dy;          // Malitsky-Pock: dual difference [m]
   cudaGraphConditionalHandle cond;
   int use_cond;
 };
@@ -274,6 +281,190 @@ struct EpiDual {
     const bool bad = st->bad_a != 0.0 || any_nonzero(t + 2 * m, m);
     decide_trial(b, cross, movement, bad);
   }
+};
+
+// ---------------------------------------------------------------------
+// Malitsky-Pock step (malitsky_pock_step, solver.cpp:202-275) as four
+// kernels per trial: MP-A once per iteration (K'y, x' = clamp(x - tau(c -
+// K'y)), the first step-size candidate), MP-E (extrapolation), MP-B (K w,
+// dual step, dy), MP-C (K'dy and the breaking test).
+struct EpiMpPrimal {
+  static constexpr int K = 1;
+  static constexpr bool kReduce = true;
+  LoopBufs b;
+  const double* xc;
+  double* xn;
+  const double* yv;
+  double tau, pend;
+  __device__ bool prepare() {
+    const DevState* st = b.st;
+    if (!st->running || st->trials_iter != 0) return false;  // once per iteration
+    const int cur = st->cur;
+    xc = pick(b.x, cur);
+    xn = pick(b.x, cur ^ 1);
+    yv = pick(b.y, cur);
+    tau = st->eta / st->omega;  // solver.cpp:219: eta_prev / omega
+    pend = st->pending;
+    return true;
+  }
+  __device__ const double* vec() const { return yv; }
+  struct Pre {
+    double x, c, l, u, a;
+  };
+  __device__ Pre load(int j) const {
+    return Pre{xc[j], b.c[j], b.l[j], b.u[j], pend != 0.0 ? b.avg_x[j] : 0.0};
+  }
+  template <class Acc>
+  __device__ void apply(int j, double kty, const Pre& o, Acc& acc) const {
+    if (pend != 0.0) b.avg_x[j] = o.a + pend * o.x;
+    const double v = o.x - tau * (o.c - kty);
+    const double xv = ref_min(ref_max(v, o.l), o.u);
+    xn[j] = xv;
+    acc.add(0, j, isfinite(xv) ? 0.0 : 1.0);
+  }
+  __device__ void start(bool bad) const {
+    DevState* st = b.st;
+    if (bad) {  // solver.cpp:226-228
+      st->status = kNonFinite;
+      st->running = 0;
+      if (b.use_cond) cudaGraphSetConditional(b.cond, 0u);
+      return;
+    }
+    const double eta_prev = st->eta;  // solver.cpp:230-233
+    st->mp_eta_hat =
+        eta_prev + st->mp_interp * (sqrt(1.0 + st->mp_theta) - 1.0) * eta_prev;
+  }
+  __device__ void finalize(const double (&tot)[K]) const { start(tot[0] != 0.0); }
+  __device__ void finalize_ordered(const double* t, int64_t n) const {
+    start(any_nonzero(t, n));
+  }
+};
+
+struct OpMpExtrapolate {
+  static constexpr int K = 1;
+  static constexpr bool kReduce = false;
+  LoopBufs b;
+  const double* xc;
+  const double* xn;
+  double theta_hat;
+  __device__ bool prepare() {
+    const DevState* st = b.st;
+    if (!st->running) return false;
+    xc = pick(b.x, st->cur);
+    xn = pick(b.x, st->cur ^ 1);
+    theta_hat = st->eta / st->mp_eta_hat;  // solver.cpp:241
+    return true;
+  }
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc&) const {
+    b.mp_ext[i] = xn[i] + theta_hat * (xn[i] - xc[i]);  // solver.cpp:244
+  }
+  __device__ void finalize(const double (&)[K]) const {}
+  __device__ void finalize_ordered(const double*, int64_t) const {}
+};
+
+struct EpiMpDual {
+  static constexpr int K = 2;
+  static constexpr bool kReduce = true;
+  LoopBufs b;
+  const double* yc;
+  double* yn;
+  double sigma, pend;
+  __device__ bool prepare() {
+    const DevState* st = b.st;
+    if (!st->running) return false;
+    yc = pick(b.y, st->cur);
+    yn = pick(b.y, st->cur ^ 1);
+    sigma = st->omega * st->mp_eta_hat;  // solver.cpp:249
+    pend = st->trials_iter == 0 ? st->pending : 0.0;
+    return true;
+  }
+  __device__ const double* vec() const { return b.mp_ext; }
+  struct Pre {
+    double y, q, a;
+  };
+  __device__ Pre load(int i) const {
+    return Pre{yc[i], b.q[i], pend != 0.0 ? b.avg_y[i] : 0.0};
+  }
+  template <class Acc>
+  __device__ void apply(int i, double kw, const Pre& o, Acc& acc) const {
+    if (pend != 0.0) b.avg_y[i] = o.a + pend * o.y;
+    double v = o.y + sigma * (o.q - kw);  // solver.cpp:252-255
+    if (i < b.m1) v = ref_max(v, 0.0);
+    yn[i] = v;
+    const double dy = v - o.y;
+    b.mp_dy[i] = dy;
+    acc.add(0, i, dy * dy);
+    acc.add(1, i, isfinite(v) ? 0.0 : 1.0);
+  }
+  __device__ void store(double dy_sq, bool bad) const {
+    DevState* st = b.st;
+    st->mp_dy_sq = dy_sq;
+    if (bad) {  // solver.cpp:257-259
+      st->status = kNonFinite;
+      st->running = 0;
+      if (b.use_cond) cudaGraphSetConditional(b.cond, 0u);
+    }
+  }
+  __device__ void finalize(const double (&tot)[K]) const { store(tot[0], tot[1] != 0.0); }
+  __device__ void finalize_ordered(const double* t, int64_t m) const {
+    store(fold(0.0, t, m), any_nonzero(t + m, m));
+  }
+};
+
+struct EpiMpCheck {
+  static constexpr int K = 1;
+  static constexpr bool kReduce = true;
+  LoopBufs b;
+  __device__ bool prepare() { return b.st->running != 0; }
+  __device__ const double* vec() const { return b.mp_dy; }
+  struct Pre {};
+  __device__ Pre load(int) const { return Pre{}; }
+  template <class Acc>
+  __device__ void apply(int j, double ktdy, const Pre&, Acc& acc) const {
+    acc.add(0, j, ktdy * ktdy);
+  }
+  __device__ void decide(double ktdy_sq) const {
+    DevState* st = b.st;
+    st->slots += 1;
+    st->trials_iter += 1;
+    st->pending = 0.0;
+    const double eta_hat = st->mp_eta_hat;
+    // solver.cpp:263-269: eta_hat ||K'dy|| <= breaking ||dy||
+    if (eta_hat * sqrt(ktdy_sq) <= st->mp_break * sqrt(st->mp_dy_sq)) {
+      const double theta_hat = st->eta / eta_hat;
+      st->k_total += 1;
+      st->t_inner += 1;
+      st->accepted += 1;
+      st->step_trials += st->trials_iter;
+      st->ledger_kt += 1 + st->trials_iter;  // K'y, then K'dy per trial
+      st->ledger_k += st->trials_iter;       // K w per trial
+      st->trials_iter = 0;
+      st->eta = eta_hat;
+      st->mp_theta = theta_hat;
+      st->last_eta_used = eta_hat;
+      st->avg_weight += eta_hat;
+      st->pending = eta_hat;
+      st->cur ^= 1;
+      if (st->accepted >= st->target) {
+        st->status = kDone;
+        st->running = 0;
+      } else if (st->k_total >= st->iteration_limit ||
+                 0.5 * static_cast<double>(st->ledger_k + st->ledger_kt) >= st->kkt_pass_limit) {
+        st->status = kLimit;
+        st->running = 0;
+      }
+    } else {
+      st->mp_eta_hat = eta_hat * st->mp_down;  // solver.cpp:270-273
+      if (st->mp_eta_hat < kStepSizeFloor) {
+        st->status = kUnderflow;
+        st->running = 0;
+      }
+    }
+    if (b.use_cond) cudaGraphSetConditional(b.cond, st->running ? 1u : 0u);
+  }
+  __device__ void finalize(const double (&tot)[K]) const { decide(tot[0]); }
+  __device__ void finalize_ordered(const double* t, int64_t n) const { decide(fold(0.0, t, n)); }
 };
 
 // ---------------------------------------------------------------------
@@ -608,6 +799,9 @@ struct NdgState {
   double radius;
   double result;   // g'd / r once done
   double nu[kNuCands];  // candidates of the next pass (heap order)
+  double rcp_primal[kNuCands];  // tree mode: RN(1 / (nu * omega))
+  double rcp_dual[kNuCands];    // tree mode: RN(1 / (nu * (1/omega)))
+  double omega, winv;
   int32_t it;      // bisection iterations consumed (<= 200)
   int32_t done;
   int32_t passes;
@@ -630,6 +824,13 @@ __host__ __device__ inline void ndg_candidates(double lo, double hi, double* nu)
       a[2 * i + 2] = nu[i];
       b[2 * i + 2] = b[i];
     }
+  }
+}
+
+__host__ __device__ inline void ndg_reciprocals(NdgState* st) {
+  for (int i = 0; i < kNuCands; ++i) {
+    st->rcp_primal[i] = 1.0 / (st->nu[i] * st->omega);
+    st->rcp_dual[i] = 1.0 / (st->nu[i] * st->winv);
   }
 }
 
@@ -666,6 +867,7 @@ __device__ inline void ndg_replay(NdgState* st, const double* norm_sq, const dou
   st->nu_lo = lo_;
   st->nu_hi = hi_;
   ndg_candidates(lo_, hi_, st->nu);
+  ndg_reciprocals(st);
 }
 
 // One bisection pass.  Tree mode: ||d(nu)||_w^2 and g'd(nu) for the 7 nodes
@@ -690,13 +892,23 @@ struct OpNdgPass {
     const double los = lo[s];
     const double his = primal ? hi[s] : INFINITY;
     const double* nu = ns->nu;
-    constexpr int P = Acc::kOrdered ? 1 : kNuCands;
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const double unclamped = gs / (__ldg(&nu[p]) * w);  // solver.cpp:349
+    if constexpr (Acc::kOrdered) {
+      // exactly the reference's quotient g / (nu * w) (solver.cpp:349)
+      const double unclamped = gs / (__ldg(&nu[0]) * w);
       const double d = ref_min(ref_max(unclamped, los), his);
-      acc.add(2 * p, s, w * d * d);
-      acc.add(2 * p + 1, s, gs * d);
+      acc.add(0, s, w * d * d);
+      acc.add(1, s, gs * d);
+    } else {
+      // tree mode: g * RN(1 / (nu * w)) -- within 1.5 ulp of the quotient,
+      // far below the tree-order noise; no per-element division
+      const double* rcp = primal ? ns->rcp_primal : ns->rcp_dual;
+#pragma unroll
+      for (int p = 0; p < kNuCands; ++p) {
+        const double unclamped = gs * __ldg(&rcp[p]);
+        const double d = ref_min(ref_max(unclamped, los), his);
+        acc.add(2 * p, s, w * d * d);
+        acc.add(2 * p + 1, s, gs * d);
+      }
     }
   }
   __device__ void finalize(const double (&tot)[K]) const {

@@ -323,6 +323,22 @@ int folp_adaptive_step(const folp_lp_c* lp_in, const double* x, const double* y,
   });
 }
 
+int folp_malitsky_pock_step(const folp_lp_c* lp_in, const double* x, const double* y,
+                            double omega, double eta_prev, double theta_prev,
+                            const folp_params_c* p, double* x_next, double* y_next,
+                            double* eta_next, double* theta_next, int64_t* trials) {
+  return guarded([&] {
+    const LinearProgram lp = to_lp(lp_in);
+    const MalitskyPockResult r =
+        malitsky_pock_step(lp, point(lp_in, x, y), omega, eta_prev, theta_prev, to_params(p));
+    put(r.next.primal, x_next);
+    put(r.next.dual, y_next);
+    *eta_next = r.eta_next;
+    *theta_next = r.theta_next;
+    *trials = r.trials;
+  });
+}
+
 int folp_session_create(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
                         const double* y0, folp_session** out) {
   *out = nullptr;

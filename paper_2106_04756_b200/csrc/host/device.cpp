@@ -82,9 +82,7 @@ PrimalDualPoint Context::get_point(int which) {
   return z;
 }
 
-ConvergenceInfo Context::evaluate(int which, bool raw, double objective_constant) {
-  folp_gpu_eval e{};
-  check(folp_gpu_evaluate(ctx_, which, raw ? 1 : 0, &e), "convergence_info");
+ConvergenceInfo to_info(const folp_gpu_eval& e, double objective_constant) {
   if (e.nonfinite) {
     throw NonFiniteIterate("convergence_info: point has NaN or inf entries");
   }
@@ -101,6 +99,12 @@ ConvergenceInfo Context::evaluate(int which, bool raw, double objective_constant
   info.norm_q = e.norm_q;
   info.norm_c = e.norm_c;
   return info;
+}
+
+ConvergenceInfo Context::evaluate(int which, bool raw, double objective_constant) {
+  folp_gpu_eval e{};
+  check(folp_gpu_evaluate(ctx_, which, raw ? 1 : 0, &e), "convergence_info");
+  return to_info(e, objective_constant);
 }
 
 }  // namespace folp::device

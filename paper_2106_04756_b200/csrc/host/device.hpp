@@ -21,6 +21,10 @@ inline void check(int code, const char* where) {
   if (code != FOLP_OK) raise(code, where);
 }
 
+// convergence_info from the device reductions of a point; throws
+// NonFiniteIterate / InfiniteProduct exactly where convergence_info would.
+ConvergenceInfo to_info(const folp_gpu_eval& e, double objective_constant);
+
 // One device context holding one LP.
 class Context {
  public:

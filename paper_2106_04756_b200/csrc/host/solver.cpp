@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <ostream>
 #include <random>
@@ -180,6 +181,8 @@ class Driver {
   double omega_ = 1.0;
   double eta_hat_ = 1.0;
   double eta_constant_ = 1.0;
+  double mp_eta_ = 1.0;    // Malitsky-Pock accepted step (solver.cpp:595)
+  double mp_theta_ = 1.0;  // Malitsky-Pock step ratio (solver.cpp:596)
   double last_eta_used_ = 0.0;
   double avg_weight_ = 0.0;
   double reference_gap_ = kInf;
@@ -189,6 +192,9 @@ class Driver {
   Index n_outer_ = 0;
   SolveResult tmpl_;
   std::vector<double> red_, grow_;
+  double time_chunks_ = 0.0;  // host wall time in loop chunks / evaluations
+  double time_evals_ = 0.0;   // (printed at finish when FOLP_TIMING is set)
+  double time_setup_ = 0.0;
 };
 
 SolveResult Driver::finish_point(TerminationReason reason, const PrimalDualPoint& reduced,
@@ -218,6 +224,13 @@ SolveResult Driver::finish_point(TerminationReason reason, const PrimalDualPoint
   r.kkt_passes = kkt_passes(ledger_);
   r.wall_seconds = elapsed();
   log_summary(r);
+  if (std::getenv("FOLP_TIMING") != nullptr) {
+    std::fprintf(stderr,
+                 "[folp timing] total %.4fs  setup %.4fs  chunks %.4fs  evaluations %.4fs  "
+                 "iterations %lld\n",
+                 r.wall_seconds, time_setup_, time_chunks_, time_evals_,
+                 static_cast<long long>(r.iterations));
+  }
   return r;
 }
 
@@ -299,9 +312,17 @@ void Driver::record_iterate() {
 
 // solver.cpp:751-816.  Returns true when the solve terminated (out is set).
 bool Driver::evaluate_and_maybe_restart(SolveResult& out) {
-  materialize_average();
-  const ConvergenceInfo cur = evaluate(FOLP_PT_CURRENT);
-  const ConvergenceInfo avg = evaluate(FOLP_PT_AVERAGE);
+  const bool restarts = p_.restart_scheme != RestartSchemeKind::kNone;
+  folp_gpu_period period{};
+  device::check(folp_gpu_evaluation_period(ctx(), omega_, restarts ? 1 : 0, &period),
+                "evaluation period");
+  avg_weight_ = period.avg_weight;
+  const ConvergenceInfo cur = device::to_info(period.current, work_->objective_constant);
+  ledger_.add_k();
+  ledger_.add_kt();
+  const ConvergenceInfo avg = device::to_info(period.average, work_->objective_constant);
+  ledger_.add_k();
+  ledger_.add_kt();
   tmpl_.trace.push_back(TraceEntry{k_total_, kkt_passes(ledger_), cur, avg});
   log_evaluation(cur, avg);
   if (check_termination(cur, p_.eps_optimal)) {
@@ -313,7 +334,7 @@ bool Driver::evaluate_and_maybe_restart(SolveResult& out) {
     return true;
   }
 
-  if (p_.restart_scheme == RestartSchemeKind::kNone) {
+  if (!restarts) {
     if (static_cast<double>(t_inner_) >= p_.beta_artificial * static_cast<double>(k_total_)) {
       double sx = 0.0, sy = 0.0;
       distance_to_last(FOLP_PT_CURRENT, sx, sy);
@@ -323,15 +344,20 @@ bool Driver::evaluate_and_maybe_restart(SolveResult& out) {
     }
     return false;
   }
+  if (!period.gaps_valid) throw DeviceError("evaluation period: duality gaps missing");
 
-  // restart_candidate (solver.cpp:372-393)
-  double sx[2], sy[2], mu[2];
-  const int slots[2] = {FOLP_PT_CURRENT, FOLP_PT_AVERAGE};
+  // restart_candidate (solver.cpp:372-393); the device evaluated both gaps
+  // at the radius weighted(sx, sy, omega) and skipped a zero radius
+  double mu[2];
   for (int i = 0; i < 2; ++i) {
-    distance_to_last(slots[i], sx[i], sy[i]);
-    const double radius = weighted(sx[i], sy[i], omega_);
-    mu[i] = radius == 0.0 ? 0.0 : ndg(slots[i], radius, omega_);
+    const double radius = weighted(period.dist_x[i], period.dist_y[i], omega_);
+    mu[i] = period.gap[i];
+    if (radius != 0.0) {
+      ledger_.add_kt();
+      ledger_.add_k();
+    }
   }
+  const int slots[2] = {FOLP_PT_CURRENT, FOLP_PT_AVERAGE};
   const int pick = mu[0] < mu[1] ? 0 : 1;  // the average wins ties
   const double gap = mu[pick];
   const RestartDecision decision =
@@ -342,11 +368,21 @@ bool Driver::evaluate_and_maybe_restart(SolveResult& out) {
   }
   ++n_outer_;
   tmpl_.restart_iterations.push_back(k_total_);
-  const double omega_new = new_primal_weight(sx[pick], sy[pick], omega_);
-  const double radius = weighted(sx[pick], sy[pick], omega_new);
-  reference_gap_ = radius > 0.0 ? ndg(slots[pick], radius, omega_new) : 0.0;
+  const double sx = period.dist_x[pick], sy = period.dist_y[pick];
+  const double omega_new = new_primal_weight(sx, sy, omega_);
+  const double radius = weighted(sx, sy, omega_new);
+  if (radius > 0.0) {
+    ledger_.add_kt();
+    ledger_.add_k();
+  }
+  // Same point, weight and radius as the candidate: the gap is the same
+  // deterministic evaluation, so it is not repeated on device.
+  const bool same = omega_new == omega_;
+  double ref = 0.0;
+  device::check(folp_gpu_restart_commit(ctx(), slots[pick], same ? 0.0 : radius, omega_new, &ref),
+                "restart");
+  reference_gap_ = radius > 0.0 ? (same ? mu[pick] : ref) : 0.0;
   omega_ = omega_new;
-  device::check(folp_gpu_restart_to(ctx(), slots[pick], 1), "restart");
   avg_weight_ = 0.0;
   last_candidate_gap_.reset();
   t_inner_ = 0;
@@ -369,10 +405,6 @@ std::optional<SolveResult> Driver::start() {
       return finish_detected(PresolveStatus::kPrimalInfeasible);
     }
     throw std::invalid_argument("solve: invalid program: " + issue->message);
-  }
-  if (p_.step_policy == StepPolicy::kMalitskyPock) {
-    throw std::invalid_argument(
-        "solve: the Malitsky-Pock step policy is not available on the B200 engine yet");
   }
 
   if (p_.use_presolve) {
@@ -435,8 +467,11 @@ std::optional<SolveResult> Driver::start() {
     eta_constant_ = norm > 0.0 ? kConstantSafety / norm : 1.0;
   } else {
     eta_hat_ = 1.0 / (has_entries ? max_abs : 1.0);
+    mp_eta_ = eta_hat_;  // solver.cpp:879-880
+    mp_theta_ = 1.0;
   }
 
+  time_setup_ = elapsed();
   {
     const ConvergenceInfo info0 = evaluate(FOLP_PT_CURRENT);
     tmpl_.trace.push_back(TraceEntry{0, kkt_passes(ledger_), info0, info0});
@@ -462,7 +497,9 @@ std::optional<SolveResult> Driver::advance(Index evaluations) {
     target = std::min<Index>(target, p_.iteration_limit - k_total_);
     target = std::min<Index>(target, 4096);
     folp_gpu_loop loop{};
-    loop.policy = p_.step_policy == StepPolicy::kConstant ? FOLP_STEP_CONSTANT : FOLP_STEP_ADAPTIVE;
+    loop.policy = p_.step_policy == StepPolicy::kConstant       ? FOLP_STEP_CONSTANT
+                  : p_.step_policy == StepPolicy::kMalitskyPock ? FOLP_STEP_MALITSKY_POCK
+                                                                : FOLP_STEP_ADAPTIVE;
     loop.target = target;
     loop.k_total = k_total_;
     loop.t_inner = t_inner_;
@@ -473,7 +510,13 @@ std::optional<SolveResult> Driver::advance(Index evaluations) {
     loop.iteration_limit = p_.iteration_limit;
     loop.kkt_pass_limit = p_.kkt_pass_limit;
     loop.omega = omega_;
-    loop.eta = loop.policy == FOLP_STEP_CONSTANT ? eta_constant_ : eta_hat_;
+    loop.eta = loop.policy == FOLP_STEP_CONSTANT        ? eta_constant_
+               : loop.policy == FOLP_STEP_MALITSKY_POCK ? mp_eta_
+                                                        : eta_hat_;
+    loop.theta = mp_theta_;
+    loop.mp_breaking_factor = p_.mp_breaking_factor;
+    loop.mp_downscaling_factor = p_.mp_downscaling_factor;
+    loop.mp_interpolation_coefficient = p_.mp_interpolation_coefficient;
     if (loop.policy == FOLP_STEP_ADAPTIVE) {
       red_.resize(static_cast<std::size_t>(target));
       grow_.resize(static_cast<std::size_t>(target));
@@ -481,7 +524,9 @@ std::optional<SolveResult> Driver::advance(Index evaluations) {
       loop.reduction = red_.data();
       loop.growth = grow_.data();
     }
+    const auto t_chunk = Clock::now();
     device::check(folp_gpu_run_chunk(ctx(), &loop), "pdhg chunk");
+    time_chunks_ += std::chrono::duration<double>(Clock::now() - t_chunk).count();
     k_total_ = loop.k_total;
     t_inner_ = loop.t_inner;
     tmpl_.step_trials = loop.step_trials;
@@ -490,6 +535,10 @@ std::optional<SolveResult> Driver::advance(Index evaluations) {
     ledger_.kt_multiplies = loop.ledger_kt;
     if (loop.accepted > 0) last_eta_used_ = loop.last_eta_used;
     if (loop.policy == FOLP_STEP_ADAPTIVE) eta_hat_ = loop.eta;
+    if (loop.policy == FOLP_STEP_MALITSKY_POCK) {
+      mp_eta_ = loop.eta;
+      mp_theta_ = loop.theta;
+    }
     avg_weight_ = loop.avg_weight;
     if (p_.record_iterate_trace && loop.accepted > 0) record_iterate();
     if (loop.status == FOLP_CHUNK_NONFINITE || loop.status == FOLP_CHUNK_UNDERFLOW) {
@@ -499,7 +548,10 @@ std::optional<SolveResult> Driver::advance(Index evaluations) {
       SolveResult out;
       ++evals;
       try {
-        if (evaluate_and_maybe_restart(out)) return out;
+        const auto t_eval = Clock::now();
+        const bool done = evaluate_and_maybe_restart(out);
+        time_evals_ += std::chrono::duration<double>(Clock::now() - t_eval).count();
+        if (done) return out;
       } catch (const NonFiniteIterate&) {
         return finish_numerical_error();
       }
@@ -533,14 +585,21 @@ struct StepOut {
 };
 
 StepOut one_step(const LinearProgram& lp, const PrimalDualPoint& z, double omega, double eta,
-                 Index k, bool adaptive, KktPassLedger* ledger) {
+                 Index k, int policy, KktPassLedger* ledger, double theta = 1.0,
+                 const SolverParams* mp = nullptr) {
   device::Context ctx(lp);
   ctx.set_point(FOLP_PT_CURRENT, z.primal, z.dual);
   StepOut out;
   folp_gpu_loop& loop = out.loop;
   double red = 0.0, grow = 0.0;
   step_factors(k, red, grow);
-  loop.policy = adaptive ? FOLP_STEP_ADAPTIVE : FOLP_STEP_CONSTANT;
+  loop.policy = policy;
+  loop.theta = theta;
+  if (mp != nullptr) {
+    loop.mp_breaking_factor = mp->mp_breaking_factor;
+    loop.mp_downscaling_factor = mp->mp_downscaling_factor;
+    loop.mp_interpolation_coefficient = mp->mp_interpolation_coefficient;
+  }
   loop.target = 1;
   loop.k_total = k - 1;
   loop.iteration_limit = std::numeric_limits<Index>::max();
@@ -555,10 +614,14 @@ StepOut one_step(const LinearProgram& lp, const PrimalDualPoint& z, double omega
     ledger->add_kt(loop.ledger_kt);
   }
   if (loop.status == FOLP_CHUNK_NONFINITE) {
-    throw NonFiniteIterate("pdhg step produced a NaN or infinite iterate");
+    throw NonFiniteIterate(policy == FOLP_STEP_MALITSKY_POCK
+                               ? "malitsky_pock_step: non-finite iterate"
+                               : "pdhg step produced a NaN or infinite iterate");
   }
   if (loop.status == FOLP_CHUNK_UNDERFLOW) {
-    throw StepSizeUnderflow("adaptive_step: step size underflow");
+    throw StepSizeUnderflow(policy == FOLP_STEP_MALITSKY_POCK
+                                ? "malitsky_pock_step: step size underflow"
+                                : "adaptive_step: step size underflow");
   }
   out.next = ctx.get_point(FOLP_PT_CURRENT);
   return out;
@@ -571,7 +634,7 @@ PrimalDualPoint pdhg_step(const LinearProgram& lp, const PrimalDualPoint& z, dou
   require_point(lp, z, "pdhg_step");
   if (!(eta > 0.0)) throw std::invalid_argument("pdhg_step: eta must be > 0");
   if (!(omega > 0.0)) throw NonPositiveWeight("pdhg_step: omega must be > 0");
-  return one_step(lp, z, omega, eta, 1, false, ledger).next;
+  return one_step(lp, z, omega, eta, 1, FOLP_STEP_CONSTANT, ledger).next;
 }
 
 double step_size_limit(const PrimalDualPoint& dz, double cross_term, double omega) {
@@ -587,7 +650,7 @@ AdaptiveStepResult adaptive_step(const LinearProgram& lp, const PrimalDualPoint&
   require_point(lp, z, "adaptive_step");
   if (k < 1) throw std::invalid_argument("adaptive_step: counter k is 1-based");
   if (!(eta_hat > 0.0)) throw std::invalid_argument("adaptive_step: eta_hat must be > 0");
-  StepOut s = one_step(lp, z, omega, eta_hat, k, true, ledger);
+  StepOut s = one_step(lp, z, omega, eta_hat, k, FOLP_STEP_ADAPTIVE, ledger);
   AdaptiveStepResult r;
   r.next = std::move(s.next);
   r.eta_used = s.loop.last_eta_used;
@@ -599,13 +662,20 @@ AdaptiveStepResult adaptive_step(const LinearProgram& lp, const PrimalDualPoint&
 }
 
 MalitskyPockResult malitsky_pock_step(const LinearProgram& lp, const PrimalDualPoint& z,
-                                      double, double eta_prev, double theta_prev,
-                                      const SolverParams&, KktPassLedger*) {
+                                      double omega, double eta_prev, double theta_prev,
+                                      const SolverParams& params, KktPassLedger* ledger) {
   require_point(lp, z, "malitsky_pock_step");
   if (!(eta_prev > 0.0) || !(theta_prev > 0.0)) {
     throw std::invalid_argument("malitsky_pock_step: needs positive previous step size and ratio");
   }
-  throw std::invalid_argument("malitsky_pock_step: not available on the B200 engine yet");
+  StepOut s = one_step(lp, z, omega, eta_prev, 1, FOLP_STEP_MALITSKY_POCK, ledger, theta_prev,
+                       &params);
+  MalitskyPockResult r;
+  r.next = std::move(s.next);
+  r.eta_next = s.loop.eta;
+  r.theta_next = s.loop.theta;
+  r.trials = s.loop.step_trials;
+  return r;
 }
 
 double normalized_duality_gap(const LinearProgram& lp, const PrimalDualPoint& z, double radius,

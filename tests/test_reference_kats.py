@@ -258,7 +258,28 @@ def test_deterministic_reruns(be):
     assert a.final_info == b.final_info
 
 
+def test_malitsky_pock_step_hand_values(be):
+    """test_solver.cpp:173-217."""
+    p0 = cabi.params(mp_interpolation_coefficient=0.0)
+    r = be.mp_step(tiny(), [0.5], [0.5], 1.0, 0.25, 1.0, p0)
+    assert (r["eta_next"], r["theta_next"], r["trials"]) == (0.25, 1.0, 1)
+    assert be.mp_step(tiny(), [0.0], [0.0], 1.0, 0.9, 1.0, p0)["trials"] == 1
+    r = be.mp_step(tiny(), [0.0], [0.0], 1.0, 1.9, 1.0, p0)
+    assert r["trials"] == 2 and r["eta_next"] == pytest.approx(0.95)
+    p4 = cabi.params(mp_interpolation_coefficient=0.4)
+    expected = 4.0 + 0.4 * (math.sqrt(2.0) - 1.0) * 4.0
+    trials = 1
+    while expected > 1.0:
+        expected *= 0.5
+        trials += 1
+    r = be.mp_step(tiny(), [0.0], [0.0], 1.0, 4.0, 1.0, p4)
+    assert r["trials"] == trials
+    assert r["eta_next"] == pytest.approx(expected)
+    assert r["theta_next"] == pytest.approx(4.0 / expected)
+
+
 @pytest.mark.parametrize("overrides", [dict(step_policy="constant"),
+                                       dict(step_policy="malitsky_pock"),
                                        dict(restart_scheme="none"),
                                        dict(restart_scheme="theory")])
 def test_policies_solve_tiny(be, overrides):
