@@ -210,6 +210,22 @@ int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms,
 int folp_session_result(folp_session* s, folp_result_c* out);
 void folp_session_destroy(folp_session* s);
 
+/* ---- multi-GPU row shards (include/folp_gpu.h) ----------
+ * folp_solve / folp_session_create as shard `shard->rank` of
+ * `shard->world`: every shard calls with the same LP, parameters and start
+ * point (one process per GPU over NCCL, or one host thread per shard of an
+ * in-process loopback group) and every shard receives the same result.
+ * Extension of the reference API (it has no multi-GPU solve). */
+struct folp_gpu_shard;
+int folp_solve_sharded(const folp_lp_c* lp, const folp_params_c* params,
+                       const double* x0, const double* y0,
+                       const struct folp_gpu_shard* shard, folp_result_c* out);
+int folp_session_create_sharded(const folp_lp_c* lp,
+                                const folp_params_c* params, const double* x0,
+                                const double* y0,
+                                const struct folp_gpu_shard* shard,
+                                folp_session** out);
+
 /* malitsky_pock_step (solver.hpp:160-164): next point to x_next/y_next;
  * params supplies the mp_* factors. */
 int folp_malitsky_pock_step(const folp_lp_c* lp, const double* x,

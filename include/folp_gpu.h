@@ -257,6 +257,65 @@ int folp_gpu_timer_stop(folp_gpu_ctx* ctx, double* ms);
 
 const char* folp_gpu_last_error(void);
 
+/* ------------------------------------------------------------------------
+ * Row shards (BASELINE.json north_star: "K is row-partitioned
+ * across the 8 GPUs of one box, with NCCL over NVLink doing an allgather of
+ * x before K x and a reduce-scatter/allreduce of the partial K'y and the
+ * scalar reductions").  Every shard builds the full context (same LP, same
+ * rescaling, bit-identical), then attaches: the PDHG loop of run_chunk works
+ * on rows [r0, r1) only -- partial K'_p y_p over the shard's CSC entries,
+ * all-reduce (n), replicated primal step, K_p x' + dual step on the local
+ * rows, all-reduce of the 3 trial sums, identical step decision everywhere.
+ * Every other engine call first reassembles y, Kx and the averaged y
+ * (broadcast of each shard's rows), then runs replicated.  Collectives are
+ * NCCL (one process per GPU, libnccl.so.2 loaded at run time) or an
+ * in-process loopback group (one host thread per shard on one GPU; parity
+ * tests).  Tree reductions only; the Malitsky-Pock policy stays single-GPU. */
+#define FOLP_SHARD_NCCL 1
+#define FOLP_SHARD_LOOPBACK 2
+#define FOLP_NCCL_ID_BYTES 128
+
+typedef struct folp_gpu_shard {
+  int32_t rank;
+  int32_t world;
+  int32_t backend; /* FOLP_SHARD_NCCL or FOLP_SHARD_LOOPBACK */
+  int32_t pad;
+  unsigned char nccl_id[FOLP_NCCL_ID_BYTES]; /* folp_gpu_nccl_unique_id on rank 0 */
+  void* loopback;                            /* folp_gpu_loopback_create(world) */
+} folp_gpu_shard;
+
+/* ncclGetUniqueId, to be broadcast by the caller to every rank. */
+int folp_gpu_nccl_unique_id(unsigned char* out);
+
+/* In-process group of `world` shards (one host thread each). */
+int folp_gpu_loopback_create(int32_t world, void** out);
+void folp_gpu_loopback_destroy(void* group);
+
+/* Row ranges of the shards, bounds [world+1]: contiguous, balanced on
+ * nonzeros + rows.  Host only. */
+int folp_gpu_shard_rows(int64_t m, const int64_t* row_start, int32_t world,
+                        int64_t* bounds);
+
+/* The CSC entries of rows [r0, r1): local column starts lptr [n+1] and
+ * their positions in the full CSC (pos, up to pos_capacity; may be NULL to
+ * count only).  Host only. */
+int folp_gpu_shard_local_csc(int64_t n, const int64_t* col_start,
+                             const int64_t* col_rows, int64_t r0, int64_t r1,
+                             int64_t* lptr, int64_t* pos, int64_t pos_capacity,
+                             int64_t* lnnz);
+
+/* Turns a context into shard spec->rank of spec->world (after create and
+ * rescale; the host CSR row starts and CSC of the same matrix). */
+int folp_gpu_shard_attach(folp_gpu_ctx* ctx, const folp_gpu_shard* spec,
+                          const int64_t* row_start, const int64_t* col_start,
+                          const int64_t* col_rows);
+
+/* *value = max over the shards (identity on an unsharded context). */
+int folp_gpu_shard_max(folp_gpu_ctx* ctx, double* value);
+
+int folp_gpu_shard_info(folp_gpu_ctx* ctx, int32_t* rank, int32_t* world,
+                        int64_t* r0, int64_t* r1, int64_t* local_nnz);
+
 #ifdef __cplusplus
 }
 #endif

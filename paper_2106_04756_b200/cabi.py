@@ -199,6 +199,16 @@ class SolveResult:
     iterate_trace: list  # (iteration, eta_used, x, y) in the working space
 
 
+class ShardC(C.Structure):
+    """include/folp_gpu.h folp_gpu_shard."""
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("backend", C.c_int32),
+                ("pad", C.c_int32), ("nccl_id", C.c_ubyte * 128), ("loopback", C.c_void_p)]
+
+
+SHARD_NCCL = 1
+SHARD_LOOPBACK = 2
+
+
 class Binding:
     """The folp_c.h entry points of one shared library."""
 
@@ -231,6 +241,12 @@ class Binding:
             f("session_stats", C.c_int, [C.c_void_p, _i64p, _f64p, _i64p, _i64p])
             f("session_result", C.c_int, [C.c_void_p, C.POINTER(ResultC)])
             f("session_destroy", None, [C.c_void_p])
+        if hasattr(lib, prefix + "solve_sharded"):
+            f("solve_sharded", C.c_int, [C.POINTER(LpC), C.POINTER(ParamsC), _f64p, _f64p,
+                                          C.POINTER(ShardC), C.POINTER(ResultC)])
+            f("session_create_sharded", C.c_int, [C.POINTER(LpC), C.POINTER(ParamsC), _f64p,
+                                                   _f64p, C.POINTER(ShardC),
+                                                   C.POINTER(C.c_void_p)])
 
     def _fn(self, name, restype, argtypes):
         fn = getattr(self.lib, self.prefix + name)
@@ -244,7 +260,10 @@ class Binding:
 
     # ---- high-level wrappers --------------------------------------------
     def solve_lp(self, lp: LP, p: Optional[dict] = None, x0=None, y0=None,
-                 trace_capacity: int = 100000, iterate_capacity: int = 0) -> SolveResult:
+                 trace_capacity: int = 100000, iterate_capacity: int = 0,
+                 shard: Optional[ShardC] = None) -> SolveResult:
+        """folp_solve, or folp_solve_sharded as one row shard when `shard`
+        is given (see paper_2106_04756_b200/shard.py)."""
         p = p or params()
         lpc = lp.to_c()
         pc = params_to_c(p)
@@ -280,7 +299,11 @@ class Binding:
         res.iterate_dual = _f64(i_y)
         xp = None if x0 is None else _f64(np.ascontiguousarray(x0, dtype=np.float64))
         yp = None if y0 is None else _f64(np.ascontiguousarray(y0, dtype=np.float64))
-        self.check(self.solve(C.byref(lpc), C.byref(pc), xp, yp, C.byref(res)))
+        if shard is None:
+            self.check(self.solve(C.byref(lpc), C.byref(pc), xp, yp, C.byref(res)))
+        else:
+            self.check(self.solve_sharded(C.byref(lpc), C.byref(pc), xp, yp, C.byref(shard),
+                                          C.byref(res)))
         nt = min(res.num_trace, trace_capacity)
         trace = [dict(iteration=int(t_it[i]), kkt_passes=float(t_kkt[i]),
                       current=t_cur[i].as_dict(), average=t_avg[i].as_dict())
@@ -300,8 +323,9 @@ class Binding:
                                                         trace_capacity)]],
             trace=trace, iterate_trace=iters)
 
-    def session(self, lp: LP, p: Optional[dict] = None) -> "Session":
-        return Session(self, lp, p or params())
+    def session(self, lp: LP, p: Optional[dict] = None,
+                shard: Optional[ShardC] = None) -> "Session":
+        return Session(self, lp, p or params(), shard)
 
     def mp_step(self, lp: LP, x, y, omega: float, eta_prev: float, theta_prev: float,
                 p: Optional[dict] = None) -> dict:
@@ -381,13 +405,18 @@ class Session:
     evaluation periods and returns their device time (CUDA events on the
     engine stream)."""
 
-    def __init__(self, b: Binding, lp: LP, p: dict):
+    def __init__(self, b: Binding, lp: LP, p: dict, shard: Optional[ShardC] = None):
         self.b = b
         self._lpc = lp.to_c()  # keeps the arrays alive
         self._pc = params_to_c(p)
+        self._shard = shard
         h = C.c_void_p()
-        b.check(b.session_create(C.byref(self._lpc), C.byref(self._pc), None, None,
-                                 C.byref(h)))
+        if shard is None:
+            b.check(b.session_create(C.byref(self._lpc), C.byref(self._pc), None, None,
+                                     C.byref(h)))
+        else:
+            b.check(b.session_create_sharded(C.byref(self._lpc), C.byref(self._pc), None, None,
+                                             C.byref(shard), C.byref(h)))
         self.h = h
         self.finished = False
 

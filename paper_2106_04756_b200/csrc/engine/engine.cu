@@ -13,8 +13,11 @@
 // Compiled with -fmad=false (see Makefile): every a*b+c is two IEEE
 // roundings like the reference's x86-64 build.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -73,6 +76,217 @@ int guarded(F&& f) {
     return FOLP_E_RUNTIME;
   }
 }
+
+// ---------------------------------------------------------------------
+// Collectives of the row-sharded loop.  One process (or, for
+// the loopback group, one host thread) per shard; every shard calls the same
+// collectives in the same order because every shard takes the same
+// decisions.
+struct ShardComm {
+  int rank = 0, world = 1;
+  virtual ~ShardComm() = default;
+  // in-place sum over the shards, identical result on every shard
+  virtual void allreduce_sum(double* buf, int64_t count, cudaStream_t s) = 0;
+  // in-place: every shard receives root's buf[0..count)
+  virtual void broadcast(double* buf, int64_t count, int root, cudaStream_t s) = 0;
+  // host scalar max over the shards (wall-clock limit checks)
+  virtual double max_scalar(double v, cudaStream_t s) = 0;
+  // in-place: rows [bounds[r], bounds[r+1]) of buf from shard r, for every r
+  virtual void gather_rows(double* buf, const std::vector<int64_t>& bounds, cudaStream_t s) = 0;
+};
+
+// NCCL, loaded at run time: the single-GPU path has no NCCL dependency, and
+// a process that already loaded torch's libnccl.so.2 shares it.
+struct NcclApi {
+  void* handle = nullptr;
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclBroadcast) bcast = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return;
+    api.handle = h;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    api.bcast = reinterpret_cast<decltype(api.bcast)>(dlsym(h, "ncclBroadcast"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  });
+  if (api.handle == nullptr || api.comm_init_rank == nullptr || api.all_reduce == nullptr ||
+      api.bcast == nullptr || api.get_unique_id == nullptr) {
+    throw EngineError(FOLP_E_RUNTIME, "NCCL (libnccl.so.2) is not loadable");
+  }
+  return api;
+}
+
+#define NCK(call)                                                                  \
+  do {                                                                             \
+    ncclResult_t r_ = (call);                                                      \
+    if (r_ != ncclSuccess) {                                                       \
+      throw EngineError(FOLP_E_RUNTIME, std::string(#call) + ": " +                \
+                                            nccl_api().error_string(r_));          \
+    }                                                                              \
+  } while (0)
+
+struct NcclComm final : ShardComm {
+  ncclComm_t comm = nullptr;
+  double* scratch = nullptr;
+  NcclComm(const unsigned char* id_bytes, int r, int w) {
+    rank = r;
+    world = w;
+    const NcclApi& api = nccl_api();
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, sizeof(id));
+    NCK(api.comm_init_rank(&comm, w, id, r));
+    CK(cudaMalloc(&scratch, sizeof(double)));
+  }
+  ~NcclComm() override {
+    if (scratch) cudaFree(scratch);
+    if (comm) nccl_api().comm_destroy(comm);
+  }
+  void allreduce_sum(double* buf, int64_t count, cudaStream_t s) override {
+    if (count > 0) NCK(nccl_api().all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm, s));
+  }
+  void broadcast(double* buf, int64_t count, int root, cudaStream_t s) override {
+    if (count > 0) NCK(nccl_api().bcast(buf, buf, count, ncclFloat64, root, comm, s));
+  }
+  void gather_rows(double* buf, const std::vector<int64_t>& bounds, cudaStream_t s) override {
+    const NcclApi& api = nccl_api();
+    NCK(api.group_start());
+    for (int r = 0; r < world; ++r) {
+      const int64_t count = bounds[r + 1] - bounds[r];
+      if (count > 0) {
+        NCK(api.bcast(buf + bounds[r], buf + bounds[r], count, ncclFloat64, r, comm, s));
+      }
+    }
+    NCK(api.group_end());
+  }
+  double max_scalar(double v, cudaStream_t s) override {
+    CK(cudaMemcpyAsync(scratch, &v, sizeof(double), cudaMemcpyHostToDevice, s));
+    NCK(nccl_api().all_reduce(scratch, scratch, 1, ncclFloat64, ncclMax, comm, s));
+    CK(cudaMemcpyAsync(&v, scratch, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+  }
+};
+
+// In-process group: W shards driven by W host threads of one process, all
+// on one device (parity tests of the sharded schedule on a single GPU).
+// Every collective synchronizes the caller's stream first and exchanges
+// through plain device copies, so no kernel ever waits on another shard.
+__global__ void k_sum_shards(double* const* parts, int world, int64_t count, double* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = parts[0][i];
+    for (int r = 1; r < world; ++r) s += parts[r][i];
+    out[i] = s;
+  }
+}
+
+struct LoopbackGroup {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t generation = 0;
+  std::vector<double*> ptrs;
+  std::vector<double> scalars;
+  explicit LoopbackGroup(int w) : world(w), ptrs(w, nullptr), scalars(w, 0.0) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+struct LoopbackComm final : ShardComm {
+  LoopbackGroup* g;
+  double** d_ptrs = nullptr;
+  double* d_sum = nullptr;
+  int64_t sum_cap = 0;
+  LoopbackComm(LoopbackGroup* group, int r) : g(group) {
+    rank = r;
+    world = group->world;
+  }
+  ~LoopbackComm() override {
+    if (d_ptrs) cudaFree(d_ptrs);
+    if (d_sum) cudaFree(d_sum);
+  }
+  void allreduce_sum(double* buf, int64_t count, cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));
+    g->ptrs[rank] = buf;
+    g->barrier();
+    if (rank == 0 && count > 0) {
+      if (d_ptrs == nullptr) CK(cudaMalloc(&d_ptrs, world * sizeof(double*)));
+      if (sum_cap < count) {
+        if (d_sum) cudaFree(d_sum);
+        CK(cudaMalloc(&d_sum, count * sizeof(double)));
+        sum_cap = count;
+      }
+      CK(cudaMemcpyAsync(d_ptrs, g->ptrs.data(), world * sizeof(double*), cudaMemcpyHostToDevice, s));
+      k_sum_shards<<<static_cast<int>(std::min<int64_t>((count + 255) / 256, 1184)), 256, 0, s>>>(
+          d_ptrs, world, count, d_sum);
+      CK(cudaGetLastError());
+      for (int r = 0; r < world; ++r) {
+        CK(cudaMemcpyAsync(g->ptrs[r], d_sum, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      }
+      CK(cudaStreamSynchronize(s));
+    }
+    g->barrier();
+  }
+  void broadcast(double* buf, int64_t count, int root, cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));
+    g->ptrs[rank] = buf;
+    g->barrier();
+    if (rank != root && count > 0) {
+      CK(cudaMemcpyAsync(buf, g->ptrs[root], count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    g->barrier();
+  }
+  void gather_rows(double* buf, const std::vector<int64_t>& bounds, cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));
+    g->ptrs[rank] = buf;
+    g->barrier();
+    for (int r = 0; r < world; ++r) {
+      const int64_t count = bounds[r + 1] - bounds[r];
+      if (r != rank && count > 0) {
+        CK(cudaMemcpyAsync(buf + bounds[r], g->ptrs[r] + bounds[r], count * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    CK(cudaStreamSynchronize(s));
+    g->barrier();
+  }
+  double max_scalar(double v, cudaStream_t) override {
+    g->scalars[rank] = v;
+    g->barrier();
+    double m = g->scalars[0];
+    for (int r = 1; r < world; ++r) m = std::max(m, g->scalars[r]);
+    g->barrier();
+    return m;
+  }
+};
+
 
 template <class T>
 T* dalloc(size_t count) {
@@ -369,6 +583,21 @@ struct folp_gpu_ctx {
   int max_giant = 0;
   int bisect_grid = 0;
 
+  // row shard: rows [r0, r1) of K~ are this shard's
+  std::unique_ptr<ShardComm> comm;
+  std::vector<int64_t> shard_bounds;  // [world + 1]
+  int64_t r0 = 0, r1 = 0, lnnz = 0;
+  PlanDev lrows, lcols;               // local rows of the CSR; local CSC
+  int* lcsc_ptr = nullptr;
+  int* lcsc_row = nullptr;
+  int* lcsc_pos = nullptr;            // local CSC entry -> full CSC position
+  double* lcsc_val = nullptr;
+  double* kty_part = nullptr;
+  double* shard_sums = nullptr;
+  bool shard_values_ready = false;
+  bool rows_dirty = false;            // y, Kx, avg_y outside [r0, r1) stale
+  bool sharded() const { return comm != nullptr; }
+
   cudaGraphExec_t chunk_exec[3] = {nullptr, nullptr, nullptr};  // per step policy
   bool graph_tried[3] = {false, false, false};
   bool graph_ok[3] = {false, false, false};
@@ -503,6 +732,9 @@ struct folp_gpu_ctx {
     for (void* p : owned) cudaFree(p);
     for (void* p : rows.owned) cudaFree(p);
     for (void* p : cols.owned) cudaFree(p);
+    for (void* p : lrows.owned) cudaFree(p);
+    for (void* p : lcols.owned) cudaFree(p);
+    comm.reset();
     if (res_h) cudaFreeHost(res_h);
     if (st_h) cudaFreeHost(st_h);
     if (ndg_h) cudaFreeHost(ndg_h);
@@ -522,7 +754,7 @@ namespace {
 // segments (<= kWarpTile nonzeros, <= 256 segments each) and fixed parts of
 // the longer ones, in index order.
 void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
-                const int* d_ptr, const int* d_idx, PlanDev& out) {
+                const int* d_ptr, const int* d_idx, PlanDev& out, int64_t s_begin = 0) {
   (void)nnz;
   const bool ordered = c->ordered;
   std::vector<int4> units;
@@ -536,7 +768,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
     seg0 = -1;
     tile_nnz = 0;
   };
-  for (int64_t s = 0; s < S; ++s) {
+  for (int64_t s = s_begin; s < S; ++s) {
     const int64_t len = ptr[s + 1] - ptr[s];
     if (len <= kWarpTile) {
       if (seg0 >= 0 && (tile_nnz + len > kWarpTile || s - seg0 >= kWarpTile)) close(s);
@@ -1040,6 +1272,78 @@ void enqueue_restart(folp_gpu_ctx* c, int which, int reset_average) {
   c->push_state();
 }
 
+// ---------------------------------------------------------------------
+// Row shards (north_star: K row-partitioned, all-reduce of the
+// partial K'y and of the scalar sums).
+__global__ void k_gather_values(double* out, const double* src, const int* pos, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    out[i] = src[pos[i]];
+  }
+}
+
+// Contiguous row ranges with about equal nonzeros + rows (so empty rows
+// still spread); monotone, covers [0, m).
+std::vector<int64_t> shard_rows(int64_t m, const int64_t* row_start, int world) {
+  std::vector<int64_t> b(static_cast<size_t>(world) + 1, 0);
+  const double total = static_cast<double>(row_start[m]) + static_cast<double>(m);
+  int64_t r = 0;
+  for (int p = 1; p < world; ++p) {
+    const double target = total * p / world;
+    while (r < m && static_cast<double>(row_start[r]) + static_cast<double>(r) < target) ++r;
+    b[p] = r;
+  }
+  b[world] = m;
+  return b;
+}
+
+// The entries of rows [r0, r1) in CSC order: within every column the rows
+// are increasing (sparse_matrix.cpp:82-102), so they form one sub-range.
+// lptr [n+1] local column starts; pos = full-CSC positions of the entries.
+void shard_local_csc(int64_t n, const int64_t* col_start, const int64_t* col_rows, int64_t r0,
+                     int64_t r1, std::vector<int64_t>& lptr, std::vector<int64_t>& pos) {
+  lptr.assign(static_cast<size_t>(n) + 1, 0);
+  pos.clear();
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t* b = col_rows + col_start[j];
+    const int64_t* e = col_rows + col_start[j + 1];
+    const int64_t* lo = std::lower_bound(b, e, r0);
+    const int64_t* hi = std::lower_bound(lo, e, r1);
+    for (const int64_t* k = lo; k < hi; ++k) pos.push_back(k - col_rows);
+    lptr[j + 1] = static_cast<int64_t>(pos.size());
+  }
+}
+
+void ensure_gathered(folp_gpu_ctx* c) {
+  if (!c->sharded() || !c->rows_dirty) return;
+  const int cur = c->st_h->cur;
+  c->comm->gather_rows(c->y[cur], c->shard_bounds, c->stream);
+  c->comm->gather_rows(c->kx[cur], c->shard_bounds, c->stream);
+  c->comm->gather_rows(c->avg_y, c->shard_bounds, c->stream);
+  c->rows_dirty = false;
+}
+
+// Entry of every engine call that reads the iterate: a sharded context
+// first reassembles the row-space vectors the loop kept local.
+void prep(folp_gpu_ctx* c) {
+  set_device(c);
+  ensure_gathered(c);
+}
+
+// One sharded trial slot (see ops.cuh, "Row-sharded trial").
+void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
+  c->seg(c->lcols, c->lcsc_val, EpiShardKty{b, c->kty_part, nullptr}, 1);
+  c->comm->allreduce_sum(c->kty_part, c->n, c->stream);
+  c->ew(c->n, OpShardPrimal{EpiPrimal{b}, c->kty_part}, 2);
+  EpiDual ed{b};
+  ed.shard_out = c->shard_sums;
+  c->seg(c->lrows, c->csr_work, ed, 3);
+  c->comm->allreduce_sum(c->shard_sums, 3, c->stream);
+  k_shard_decide<<<1, 1, 0, c->stream>>>(b, c->shard_sums);
+  ++c->launches;
+  CK(cudaGetLastError());
+}
+
 // One trial slot of a step policy: adaptive / constant = {A; B},
 // Malitsky-Pock = {MP-A (first trial only); MP-E; MP-B; MP-C}.
 void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
@@ -1256,7 +1560,8 @@ void folp_gpu_destroy(folp_gpu_ctx* ctx) { delete ctx; }
 int folp_gpu_rescale(folp_gpu_ctx* c, int64_t ruiz_iterations, int32_t pock_chambolle,
                      double alpha, double* row_scale, double* col_scale) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
+    c->shard_values_ready = false;
     const int64_t m = c->m, n = c->n, nnz = c->nnz;
     double* cum1 = c->d1;
     double* cum2 = c->d2;
@@ -1321,7 +1626,7 @@ int folp_gpu_rescale(folp_gpu_ctx* c, int64_t ruiz_iterations, int32_t pock_cham
 int folp_gpu_working_stats(folp_gpu_ctx* c, double* max_abs_entry, double* norm_c,
                            double* norm_q) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     const int nb = std::min<int64_t>(c->sms * 4, std::max<int64_t>(1, (c->nnz + kBlock - 1) / kBlock));
     k_absmax_blocks<<<nb, kBlock, 0, c->stream>>>(c->csr_work, c->nnz, c->partials);
     k_absmax_all<<<1, kBlock, 0, c->stream>>>(c->partials, nb, c->res + 0);
@@ -1338,7 +1643,7 @@ int folp_gpu_working_stats(folp_gpu_ctx* c, double* max_abs_entry, double* norm_
 int folp_gpu_get_working(folp_gpu_ctx* c, double* csr_values, double* csc_values,
                          double* objective, double* rhs, double* lower, double* upper) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     download(c, csr_values, c->csr_work, c->nnz);
     download(c, csc_values, c->csc_work, c->nnz);
     download(c, objective, c->cw, c->n);
@@ -1351,7 +1656,7 @@ int folp_gpu_get_working(folp_gpu_ctx* c, double* csr_values, double* csc_values
 
 int folp_gpu_set_start(folp_gpu_ctx* c, const double* x0, const double* y0) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     upload(c, c->aux_x, x0, c->n);
     upload(c, c->aux_y, y0, c->m);
     k_start_point<<<c->simple_grid(c->n + c->m), kBlock, 0, c->stream>>>(
@@ -1367,7 +1672,7 @@ int folp_gpu_set_start(folp_gpu_ctx* c, const double* x0, const double* y0) {
 
 int folp_gpu_set_point(folp_gpu_ctx* c, int32_t which, const double* x, const double* y) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     upload(c, c->slot_x(which), x, c->n);
     upload(c, c->slot_y(which), y, c->m);
     if (which == FOLP_PT_CURRENT) refresh_kx(c);
@@ -1377,7 +1682,7 @@ int folp_gpu_set_point(folp_gpu_ctx* c, int32_t which, const double* x, const do
 
 int folp_gpu_get_point(folp_gpu_ctx* c, int32_t which, double* x, double* y) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     download(c, x, c->slot_x(which), c->n);
     download(c, y, c->slot_y(which), c->m);
     CK(cudaStreamSynchronize(c->stream));
@@ -1386,7 +1691,7 @@ int folp_gpu_get_point(folp_gpu_ctx* c, int32_t which, double* x, double* y) {
 
 int folp_gpu_get_reduced_point(folp_gpu_ctx* c, int32_t which, double* x, double* y) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     k_reduced_point<<<c->simple_grid(c->n + c->m), kBlock, 0, c->stream>>>(
         c->n, c->m, c->slot_x(which), c->slot_y(which), c->d1, c->d2, c->l0, c->u0, c->xr,
         c->yr);
@@ -1400,7 +1705,7 @@ int folp_gpu_get_reduced_point(folp_gpu_ctx* c, int32_t which, double* x, double
 
 int folp_gpu_materialize_average(folp_gpu_ctx* c, double* weight) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     enqueue_average(c);
     CK(cudaStreamSynchronize(c->stream));
     if (weight) *weight = c->st_h->avg_weight;
@@ -1409,7 +1714,7 @@ int folp_gpu_materialize_average(folp_gpu_ctx* c, double* weight) {
 
 int folp_gpu_evaluate(folp_gpu_ctx* c, int32_t which, int32_t raw, folp_gpu_eval* out) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     enqueue_evaluate(c, which, raw, kResEval[0]);
     c->fetch_res(kResUsed);
     read_evaluate(c, kResEval[0], out);
@@ -1418,7 +1723,7 @@ int folp_gpu_evaluate(folp_gpu_ctx* c, int32_t which, int32_t raw, folp_gpu_eval
 
 int folp_gpu_distance(folp_gpu_ctx* c, int32_t a, int32_t b, double* sx, double* sy) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     enqueue_distance(c, a, b, kResDist[0]);
     c->fetch_res(kResUsed);
     *sx = c->res_h[kResDist[0]];
@@ -1428,7 +1733,7 @@ int folp_gpu_distance(folp_gpu_ctx* c, int32_t a, int32_t b, double* sx, double*
 
 int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, double* gap) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     check_ndg_args(radius, omega);
     enqueue_ndg_setup(c, which, 0, omega);
     enqueue_ndg_init(c, 0, -1, radius, omega);
@@ -1442,7 +1747,7 @@ int folp_gpu_ndg(folp_gpu_ctx* c, int32_t which, double radius, double omega, do
 int folp_gpu_evaluation_period(folp_gpu_ctx* c, double omega, int32_t want_gaps,
                                folp_gpu_period* out) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     if (want_gaps && !(omega > 0.0)) {
       throw EngineError(FOLP_E_NONPOSITIVE_WEIGHT, "normalized_duality_gap: omega must be > 0");
     }
@@ -1480,7 +1785,7 @@ int folp_gpu_evaluation_period(folp_gpu_ctx* c, double omega, int32_t want_gaps,
 int folp_gpu_restart_commit(folp_gpu_ctx* c, int32_t which, double radius, double omega,
                             double* reference_gap) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     const bool gap = radius > 0.0;
     if (gap) {
       check_ndg_args(radius, omega);
@@ -1498,7 +1803,7 @@ int folp_gpu_restart_commit(folp_gpu_ctx* c, int32_t which, double radius, doubl
 
 int folp_gpu_restart_to(folp_gpu_ctx* c, int32_t which, int32_t reset_average) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     enqueue_restart(c, which, reset_average);
     CK(cudaStreamSynchronize(c->stream));
   });
@@ -1506,7 +1811,7 @@ int folp_gpu_restart_to(folp_gpu_ctx* c, int32_t which, int32_t reset_average) {
 
 int folp_gpu_mark_last(folp_gpu_ctx* c) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     copy_d2d(c, c->last_x, c->cur_x(), c->n);
     copy_d2d(c, c->last_y, c->cur_y(), c->m);
     CK(cudaStreamSynchronize(c->stream));
@@ -1559,10 +1864,31 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     st->mp_down = loop->mp_downscaling_factor;
     st->mp_interp = loop->mp_interpolation_coefficient;
     c->push_state();
-    if (!c->graph_tried[policy]) build_chunk_graph(c, policy);
+    if (c->sharded() && policy == FOLP_STEP_MALITSKY_POCK) {
+      throw std::invalid_argument("sharded solve: the Malitsky-Pock policy runs on one GPU only");
+    }
+    if (!c->sharded() && !c->graph_tried[policy]) build_chunk_graph(c, policy);
     const int per_slot = policy == FOLP_STEP_MALITSKY_POCK ? 4 : 2;
     if (c->profiling) CK(cudaEventRecord(c->ev0, c->stream));
-    if (c->graph_ok[policy]) {
+    if (c->sharded()) {
+      if (!c->shard_values_ready) {  // K~ values of the local CSC, after rescaling
+        k_gather_values<<<c->simple_grid(c->lnnz), kBlock, 0, c->stream>>>(
+            c->lcsc_val, c->csc_work, c->lcsc_pos, c->lnnz);
+        ++c->launches;
+        CK(cudaGetLastError());
+        c->shard_values_ready = true;
+      }
+      const LoopBufs b = c->loop_bufs(cudaGraphConditionalHandle{}, 0);
+      int64_t remaining = loop->target;
+      for (;;) {
+        for (int64_t s = 0; s < remaining; ++s) launch_shard_slot(c, b);
+        CK(cudaMemcpyAsync(st, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (!st->running) break;
+        remaining = st->target - st->accepted;
+      }
+      c->rows_dirty = true;
+    } else if (c->graph_ok[policy]) {
       CK(cudaGraphLaunch(c->chunk_exec[policy], c->stream));
     } else {
       // Plain stream launches: enough slots for the target plus a few
@@ -1580,7 +1906,7 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     }
     if (c->profiling) CK(cudaEventRecord(c->ev1, c->stream));
     c->pull_state();
-    c->launches += per_slot * st->slots;
+    if (!c->sharded()) c->launches += per_slot * st->slots;
     if (policy == FOLP_STEP_MALITSKY_POCK) c->kx_valid = false;  // Kx cache not kept
     if (c->profiling) {
       float ms = 0.f;
@@ -1611,7 +1937,7 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
 int folp_gpu_spectral_norm(folp_gpu_ctx* c, const double* v0, double relative_tol,
                            int64_t max_iterations, double* norm, int64_t* multiplies) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     double* v = c->aux_x;
     double* w = c->aux_y;
     double* s = c->xr;
@@ -1641,7 +1967,7 @@ int folp_gpu_spectral_norm(folp_gpu_ctx* c, const double* v0, double relative_to
 
 int folp_gpu_multiply(folp_gpu_ctx* c, int32_t working, const double* xh, double* out) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     upload(c, c->aux_x, xh, c->n);
     product(c, false, working != 0, c->aux_x, c->kx_aux);
     download(c, out, c->kx_aux, c->m);
@@ -1651,7 +1977,7 @@ int folp_gpu_multiply(folp_gpu_ctx* c, int32_t working, const double* xh, double
 
 int folp_gpu_multiply_transpose(folp_gpu_ctx* c, int32_t working, const double* yh, double* out) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     upload(c, c->aux_y, yh, c->m);
     product(c, true, working != 0, c->aux_y, c->xr);
     download(c, out, c->xr, c->n);
@@ -1661,7 +1987,7 @@ int folp_gpu_multiply_transpose(folp_gpu_ctx* c, int32_t working, const double* 
 
 int folp_gpu_all_finite(folp_gpu_ctx* c, int32_t which, int32_t* finite) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     c->ew(c->n + c->m, OpCountNonFinite{c->n, c->slot_x(which), c->slot_y(which), c->res + 44}, 4);
     c->fetch_res(45);
     *finite = c->res_h[44] == 0.0 ? 1 : 0;
@@ -1670,7 +1996,7 @@ int folp_gpu_all_finite(folp_gpu_ctx* c, int32_t which, int32_t* finite) {
 
 int folp_gpu_axis_norms(folp_gpu_ctx* c, int32_t axis, double p, int32_t working, double* out) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     const bool rows = axis == 0;
     const int S = static_cast<int>(rows ? c->m : c->n);
     const int* ptr = rows ? c->csr_ptr : c->csc_ptr;
@@ -1692,7 +2018,7 @@ int folp_gpu_axis_norms(folp_gpu_ctx* c, int32_t axis, double p, int32_t working
 
 int folp_gpu_max_abs_entry(folp_gpu_ctx* c, int32_t working, double* out) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     const int nb = std::min<int64_t>(c->sms * 4, std::max<int64_t>(1, (c->nnz + kBlock - 1) / kBlock));
     k_absmax_blocks<<<nb, kBlock, 0, c->stream>>>(working ? c->csr_work : c->csr_orig, c->nnz,
                                                   c->partials);
@@ -1725,19 +2051,138 @@ int folp_gpu_chunk_timing(folp_gpu_ctx* c, double* chunk_ms, int64_t* slots) {
 
 int folp_gpu_timer_start(folp_gpu_ctx* c) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     CK(cudaEventRecord(c->tev0, c->stream));
   });
 }
 
 int folp_gpu_timer_stop(folp_gpu_ctx* c, double* ms) {
   return guarded([&] {
-    set_device(c);
+    prep(c);
     CK(cudaEventRecord(c->tev1, c->stream));
     CK(cudaEventSynchronize(c->tev1));
     float f = 0.f;
     CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
     *ms = f;
+  });
+}
+
+// ---------------------------------------------------------------------
+// Row shards.
+int folp_gpu_nccl_unique_id(unsigned char* out) {
+  return guarded([&] {
+    ncclUniqueId id;
+    NCK(nccl_api().get_unique_id(&id));
+    static_assert(sizeof(id) == FOLP_NCCL_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int folp_gpu_loopback_create(int32_t world, void** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (world < 1) throw std::invalid_argument("loopback group: world must be >= 1");
+    *out = new LoopbackGroup(world);
+  });
+}
+
+void folp_gpu_loopback_destroy(void* group) { delete static_cast<LoopbackGroup*>(group); }
+
+int folp_gpu_shard_rows(int64_t m, const int64_t* row_start, int32_t world, int64_t* bounds) {
+  return guarded([&] {
+    if (world < 1 || m < 0) throw std::invalid_argument("shard_rows: bad arguments");
+    const std::vector<int64_t> b = shard_rows(m, row_start, world);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
+int folp_gpu_shard_local_csc(int64_t n, const int64_t* col_start, const int64_t* col_rows,
+                             int64_t r0, int64_t r1, int64_t* lptr, int64_t* pos,
+                             int64_t pos_capacity, int64_t* lnnz) {
+  return guarded([&] {
+    std::vector<int64_t> lp, ps;
+    shard_local_csc(n, col_start, col_rows, r0, r1, lp, ps);
+    *lnnz = static_cast<int64_t>(ps.size());
+    std::copy(lp.begin(), lp.end(), lptr);
+    if (pos != nullptr) {
+      if (static_cast<int64_t>(ps.size()) > pos_capacity) {
+        throw std::invalid_argument("shard_local_csc: pos capacity too small");
+      }
+      std::copy(ps.begin(), ps.end(), pos);
+    }
+  });
+}
+
+int folp_gpu_shard_attach(folp_gpu_ctx* c, const folp_gpu_shard* spec, const int64_t* row_start,
+                          const int64_t* col_start, const int64_t* col_rows) {
+  return guarded([&] {
+    set_device(c);
+    if (c->sharded()) throw std::invalid_argument("shard_attach: context already sharded");
+    if (spec == nullptr || spec->world < 1 || spec->rank < 0 || spec->rank >= spec->world) {
+      throw std::invalid_argument("shard_attach: bad rank / world");
+    }
+    if (c->ordered) {
+      throw std::invalid_argument("shard_attach: the ordered reduction mode is single-GPU only");
+    }
+    if (row_start == nullptr || col_start == nullptr || col_rows == nullptr) {
+      throw std::invalid_argument("shard_attach: CSR row starts and CSC arrays required");
+    }
+    if (spec->backend == FOLP_SHARD_NCCL) {
+      c->comm = std::make_unique<NcclComm>(spec->nccl_id, spec->rank, spec->world);
+    } else if (spec->backend == FOLP_SHARD_LOOPBACK) {
+      auto* g = static_cast<LoopbackGroup*>(spec->loopback);
+      if (g == nullptr || g->world != spec->world) {
+        throw std::invalid_argument("shard_attach: loopback group missing or of another size");
+      }
+      c->comm = std::make_unique<LoopbackComm>(g, spec->rank);
+    } else {
+      throw std::invalid_argument("shard_attach: unknown backend");
+    }
+    const int64_t m = c->m, n = c->n;
+    c->shard_bounds = shard_rows(m, row_start, spec->world);
+    c->r0 = c->shard_bounds[spec->rank];
+    c->r1 = c->shard_bounds[spec->rank + 1];
+    build_plan(c, row_start, c->r1, c->nnz, c->csr_ptr, c->csr_col, c->lrows, c->r0);
+    std::vector<int64_t> lptr, pos;
+    shard_local_csc(n, col_start, col_rows, c->r0, c->r1, lptr, pos);
+    c->lnnz = static_cast<int64_t>(pos.size());
+    std::vector<int> lptr32(lptr.begin(), lptr.end()), pos32(pos.size()), row32(pos.size());
+    for (size_t k = 0; k < pos.size(); ++k) {
+      pos32[k] = static_cast<int>(pos[k]);
+      row32[k] = static_cast<int>(col_rows[pos[k]]);
+    }
+    c->lcsc_ptr = c->alloc<int>(n + 1);
+    c->lcsc_row = c->alloc<int>(c->lnnz + 8);
+    c->lcsc_pos = c->alloc<int>(c->lnnz + 1);
+    c->lcsc_val = c->alloc<double>(c->lnnz + 8);
+    CK(cudaMemcpy(c->lcsc_ptr, lptr32.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    if (c->lnnz > 0) {
+      CK(cudaMemcpy(c->lcsc_row, row32.data(), c->lnnz * sizeof(int), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->lcsc_pos, pos32.data(), c->lnnz * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    build_plan(c, lptr.data(), n, c->lnnz, c->lcsc_ptr, c->lcsc_row, c->lcols);
+    c->kty_part = c->alloc<double>(std::max<int64_t>(n, 1));
+    c->shard_sums = c->alloc<double>(4);
+    c->shard_values_ready = false;
+    c->rows_dirty = false;
+  });
+}
+
+int folp_gpu_shard_max(folp_gpu_ctx* c, double* value) {
+  return guarded([&] {
+    set_device(c);
+    if (c->sharded()) *value = c->comm->max_scalar(*value, c->stream);
+  });
+}
+
+int folp_gpu_shard_info(folp_gpu_ctx* c, int32_t* rank, int32_t* world, int64_t* r0, int64_t* r1,
+                        int64_t* local_nnz) {
+  return guarded([&] {
+    *rank = c->sharded() ? c->comm->rank : 0;
+    *world = c->sharded() ? c->comm->world : 1;
+    *r0 = c->sharded() ? c->r0 : 0;
+    *r1 = c->sharded() ? c->r1 : c->m;
+    *local_nnz = c->sharded() ? c->lnnz : c->nnz;
   });
 }
 

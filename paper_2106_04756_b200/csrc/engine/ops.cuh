@@ -266,7 +266,12 @@ struct EpiDual {
     acc.add(1, i, dy * dy);
     acc.add(2, i, isfinite(v) ? 0.0 : 1.0);
   }
+  double* shard_out = nullptr;  // row shard: local sums for the all-reduce
   __device__ void finalize(const double (&tot)[K]) const {
+    if (shard_out != nullptr) {
+      for (int k = 0; k < K; ++k) shard_out[k] = tot[k];
+      return;
+    }
     const DevState* st = b.st;
     double movement = tot[1] / st->omega;  // solver.cpp:83
     movement = movement + st->sx;
@@ -282,6 +287,62 @@ struct EpiDual {
     decide_trial(b, cross, movement, bad);
   }
 };
+
+// ---------------------------------------------------------------------
+// Row-sharded trial (north_star: K row-partitioned across the
+// GPUs, all-reduce of the partial K'y and of the scalar reductions).  Rank p
+// owns rows [r0, r1): y, Kx and the averaged y of those rows; x, c, l, u and
+// the primal step are replicated.  One trial =
+//   EpiShardKty (partial K'_p y_p over the local CSC)  -> all-reduce (n)
+//   OpShardPrimal (kernel A's epilogue on the summed K'y, replicated)
+//   EpiDual over the local rows with shard_out        -> all-reduce (3)
+//   k_shard_decide (kernel B's finalize on the global sums)
+// Every rank holds bit-identical replicated data and sums, so every rank
+// takes the same decisions.
+struct EpiShardKty {
+  static constexpr int K = 1;
+  static constexpr bool kReduce = false;
+  LoopBufs b;
+  double* out;
+  const double* yv;
+  __device__ bool prepare() {
+    if (!b.st->running) return false;
+    yv = pick(b.y, b.st->cur);
+    return true;
+  }
+  __device__ const double* vec() const { return yv; }
+  struct Pre {};
+  __device__ Pre load(int) const { return Pre{}; }
+  template <class Acc>
+  __device__ void apply(int j, double dot, const Pre&, Acc&) const {
+    out[j] = dot;
+  }
+  __device__ void finalize(const double (&)[K]) const {}
+  __device__ void finalize_ordered(const double*, int64_t) const {}
+};
+
+struct OpShardPrimal {
+  static constexpr int K = 2;
+  static constexpr bool kReduce = true;
+  EpiPrimal e;
+  const double* kty;
+  __device__ bool prepare() { return e.prepare(); }
+  template <class Acc>
+  __device__ void apply(int64_t j, Acc& acc) const {
+    const int jj = static_cast<int>(j);
+    e.apply(jj, kty[jj], e.load(jj), acc);
+  }
+  __device__ void finalize(const double (&tot)[K]) const { e.finalize(tot); }
+  __device__ void finalize_ordered(const double*, int64_t) const {}
+};
+
+__global__ void k_shard_decide(LoopBufs b, const double* sums) {
+  const DevState* st = b.st;
+  if (!st->running) return;
+  double movement = sums[1] / st->omega;  // solver.cpp:83, on the global sums
+  movement = movement + st->sx;
+  decide_trial(b, sums[0], movement, st->bad_a != 0.0 || sums[2] != 0.0);
+}
 
 // ---------------------------------------------------------------------
 // Malitsky-Pock step (malitsky_pock_step, solver.cpp:202-275) as four

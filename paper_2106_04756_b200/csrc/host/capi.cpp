@@ -339,8 +339,9 @@ int folp_malitsky_pock_step(const folp_lp_c* lp_in, const double* x, const doubl
   });
 }
 
-int folp_session_create(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
-                        const double* y0, folp_session** out) {
+int folp_session_create_sharded(const folp_lp_c* lp_in, const folp_params_c* p,
+                                const double* x0, const double* y0,
+                                const folp_gpu_shard* shard, folp_session** out) {
   *out = nullptr;
   return guarded([&] {
     PrimalDualPoint z0;
@@ -349,9 +350,29 @@ int folp_session_create(const folp_lp_c* lp_in, const folp_params_c* p, const do
     if (x0 != nullptr) z0.primal.assign(x0, x0 + lp_in->num_cols);
     if (y0 != nullptr) z0.dual.assign(y0, y0 + lp_in->num_rows);
     auto sess = std::make_unique<folp_session>();
-    sess->s = std::make_unique<SolveSession>(to_lp(lp_in), to_params(p), std::move(z0));
+    sess->s = std::make_unique<SolveSession>(to_lp(lp_in), to_params(p), std::move(z0), shard);
     if (folp_gpu_ctx* c = sess->s->context()) folp_gpu_set_profiling(c, 1);
     *out = sess.release();
+  });
+}
+
+int folp_session_create(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
+                        const double* y0, folp_session** out) {
+  return folp_session_create_sharded(lp_in, p, x0, y0, nullptr, out);
+}
+
+int folp_solve_sharded(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
+                       const double* y0, const folp_gpu_shard* shard, folp_result_c* out) {
+  return guarded([&] {
+    if (shard == nullptr) throw std::invalid_argument("folp_solve_sharded: shard spec required");
+    const LinearProgram lp = to_lp(lp_in);
+    const SolverParams params = to_params(p);
+    PrimalDualPoint z0;
+    z0.primal.assign(static_cast<std::size_t>(lp_in->num_cols), 0.0);
+    z0.dual.assign(static_cast<std::size_t>(lp_in->num_rows), 0.0);
+    if (x0 != nullptr) z0.primal.assign(x0, x0 + lp_in->num_cols);
+    if (y0 != nullptr) z0.dual.assign(y0, y0 + lp_in->num_rows);
+    export_result(solve_sharded(lp, params, z0, *shard), out);
   });
 }
 

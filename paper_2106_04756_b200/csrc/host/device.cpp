@@ -101,6 +101,12 @@ ConvergenceInfo to_info(const folp_gpu_eval& e, double objective_constant) {
   return info;
 }
 
+void Context::attach_shard(const SparseMatrix& k, const folp_gpu_shard& spec) {
+  check(folp_gpu_shard_attach(ctx_, &spec, k.row_start().data(), k.col_start().data(),
+                              k.col_rows().data()),
+        "shard attach");
+}
+
 ConvergenceInfo Context::evaluate(int which, bool raw, double objective_constant) {
   folp_gpu_eval e{};
   check(folp_gpu_evaluate(ctx_, which, raw ? 1 : 0, &e), "convergence_info");

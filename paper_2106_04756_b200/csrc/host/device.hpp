@@ -46,6 +46,8 @@ class Context {
   // convergence_info quantities of a slot; throws NonFiniteIterate /
   // InfiniteProduct exactly where convergence_info would.
   ConvergenceInfo evaluate(int which, bool raw, double objective_constant);
+  // Row shard of a multi-GPU solve (after rescale); k = the context's matrix.
+  void attach_shard(const SparseMatrix& k, const folp_gpu_shard& spec);
 
  private:
   void create(const SparseMatrix& k, const double* c, const double* q, const double* l,

@@ -13,7 +13,11 @@ namespace folp {
 
 class SolveSession {
  public:
-  SolveSession(LinearProgram lp, const SolverParams& params, PrimalDualPoint z0);
+  // shard != nullptr: this process/thread is one row shard of a multi-GPU
+  // solve (include/folp_gpu.h folp_gpu_shard); every shard builds the same
+  // session on the same LP.
+  SolveSession(LinearProgram lp, const SolverParams& params, PrimalDualPoint z0,
+               const folp_gpu_shard* shard = nullptr);
   ~SolveSession();
   // Advances by up to `evaluations` evaluation periods (evaluation_cadence
   // iterations + the evaluation/restart step each); true once finished.
@@ -27,5 +31,11 @@ class SolveSession {
   struct Impl;
   std::unique_ptr<Impl> impl_;
 };
+
+// folp::solve as one row shard of a multi-GPU solve: every
+// shard calls it with the same LP, parameters and start point and receives
+// the same result.
+SolveResult solve_sharded(const LinearProgram& lp_raw, const SolverParams& params,
+                          const PrimalDualPoint& z0, const folp_gpu_shard& shard);
 
 }  // namespace folp

@@ -89,8 +89,9 @@ std::vector<double> start_vector(Index n) {  // sparse_matrix.cpp:195-202
 // ---------------------------------------------------------------------
 class Driver {
  public:
-  Driver(const LinearProgram& raw, const SolverParams& params, const PrimalDualPoint& z0)
-      : raw_(raw), p_(params), z0_(z0), start_(Clock::now()) {}
+  Driver(const LinearProgram& raw, const SolverParams& params, const PrimalDualPoint& z0,
+         const folp_gpu_shard* shard = nullptr)
+      : raw_(raw), p_(params), z0_(z0), start_(Clock::now()), shard_(shard) {}
 
   SolveResult run();
   // Everything before the loop (solver.cpp:818-907); a value when the solve
@@ -104,6 +105,13 @@ class Driver {
  private:
   using Clock = std::chrono::steady_clock;
   double elapsed() const { return std::chrono::duration<double>(Clock::now() - start_).count(); }
+  // Wall clock for the time-limit decision: the max over the shards, so
+  // every shard takes the same branch.
+  double decision_clock() {
+    double e = elapsed();
+    if (shard_ != nullptr && dev_) device::check(folp_gpu_shard_max(ctx(), &e), "shard clock");
+    return e;
+  }
   folp_gpu_ctx* ctx() const { return dev_->get(); }
 
   ConvergenceInfo evaluate(int slot) {
@@ -171,6 +179,7 @@ class Driver {
   SolverParams p_;
   const PrimalDualPoint& z0_;
   Clock::time_point start_;
+  const folp_gpu_shard* shard_ = nullptr;  // row shard of a multi-GPU solve
 
   PresolveTransform transform_;
   LinearProgram presolved_storage_;
@@ -440,6 +449,7 @@ std::optional<SolveResult> Driver::start() {
   device::check(folp_gpu_rescale(ctx(), p_.ruiz_iterations, p_.use_pock_chambolle ? 1 : 0,
                                  p_.pc_alpha, nullptr, nullptr),
                 "rescale_problem");
+  if (shard_ != nullptr) dev_->attach_shard(work_->constraint_matrix, *shard_);
 
   // start point into the working space, projected (solver.cpp:853-865)
   const PrimalDualPoint z = restrict_point(transform_, z0_.primal, z0_.dual);
@@ -491,7 +501,9 @@ std::optional<SolveResult> Driver::advance(Index evaluations) {
     if (kkt_passes(ledger_) >= p_.kkt_pass_limit) {
       return finish_limit(TerminationReason::kKktPassLimit);
     }
-    if (elapsed() >= p_.time_limit_seconds) return finish_limit(TerminationReason::kTimeLimit);
+    if (decision_clock() >= p_.time_limit_seconds) {
+      return finish_limit(TerminationReason::kTimeLimit);
+    }
 
     Index target = p_.record_iterate_trace ? 1 : cadence - (t_inner_ % cadence);
     target = std::min<Index>(target, p_.iteration_limit - k_total_);
@@ -755,18 +767,30 @@ SolveResult solve(const LinearProgram& lp_raw, const SolverParams& params,
   return Driver(lp_raw, params, z0).run();
 }
 
+SolveResult solve_sharded(const LinearProgram& lp_raw, const SolverParams& params,
+                          const PrimalDualPoint& z0, const folp_gpu_shard& shard) {
+  if (params.step_policy == StepPolicy::kMalitskyPock) {
+    throw std::invalid_argument("solve_sharded: the Malitsky-Pock policy runs on one GPU only");
+  }
+  return Driver(lp_raw, params, z0, &shard).run();
+}
+
 // ---- resumable session (include/folp_c.h folp_session_*) -------------
 struct SolveSession::Impl {
   LinearProgram lp;
   SolverParams params;
   PrimalDualPoint z0;
+  std::optional<folp_gpu_shard> shard;
   std::unique_ptr<Driver> driver;
   std::optional<SolveResult> result;
 };
 
-SolveSession::SolveSession(LinearProgram lp, const SolverParams& params, PrimalDualPoint z0)
-    : impl_(new Impl{std::move(lp), params, std::move(z0), nullptr, std::nullopt}) {
-  impl_->driver = std::make_unique<Driver>(impl_->lp, impl_->params, impl_->z0);
+SolveSession::SolveSession(LinearProgram lp, const SolverParams& params, PrimalDualPoint z0,
+                           const folp_gpu_shard* shard)
+    : impl_(new Impl{std::move(lp), params, std::move(z0), std::nullopt, nullptr, std::nullopt}) {
+  if (shard != nullptr) impl_->shard = *shard;
+  impl_->driver = std::make_unique<Driver>(impl_->lp, impl_->params, impl_->z0,
+                                           impl_->shard ? &*impl_->shard : nullptr);
   impl_->result = impl_->driver->start();
 }
 

@@ -1,0 +1,106 @@
+"""Row-sharded solves on the B200, through the C ABI.
+
+Only one GPU is available per test run, so the sharded schedule is checked
+with the engine's in-process loopback group (W host threads, W shard
+contexts on one device, collectives as synchronized device copies -- no
+kernel waits on another shard) and the NCCL backend at world size 1 (the
+real communicator, every collective a no-op exchange).  Checks: all shards
+return the same result; the solve meets the north_star bar against the
+compiled reference (termination, KKT <= 1e-8, objective within the
+admissible gap, first restart period within 1e-10 per iterate)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2106_04756_b200 import cabi, instances, shard
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel_kkt(info):
+    gap = info["gap_abs"] / (1 + abs(info["primal_objective"]) + abs(info["dual_objective"]))
+    pr = info["primal_residual_norm"] / (1 + info["norm_q"])
+    du = info["dual_residual_norm"] / (1 + info["norm_c"])
+    return max(gap, pr, du)
+
+
+def _same(results):
+    a = results[0]
+    for b in results[1:]:
+        assert b.termination_reason == a.termination_reason
+        assert b.iterations == a.iterations and b.restart_iterations == a.restart_iterations
+        assert b.final_info == a.final_info
+        assert np.array_equal(b.primal_solution, a.primal_solution)
+        assert np.array_equal(b.dual_solution, a.dual_solution)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("cfg,scale", [(1, 1.0), (5, 0.01)])
+def test_loopback_shards_solve_to_1e8(ref, cfg, scale, world):
+    lp = instances.generate(cfg, 1, scale)
+    p = cabi.params(kkt_pass_limit=300000)
+    res = shard.solve_loopback(lp, world, p)
+    _same(res)
+    a = res[0]
+    b = ref.solve_lp(lp, p)
+    assert a.termination_reason == b.termination_reason == "Optimal"
+    assert _rel_kkt(a.final_info) <= 1e-8
+    pa, pb = a.final_info["primal_objective"], b.final_info["primal_objective"]
+    assert abs(pa - pb) <= 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
+    # tree-order sums: the iteration count moves like the single-GPU tree
+    # mode's (profiles/r1_tree_mode_iteration_spread.txt)
+    assert abs(a.iterations - b.iterations) <= 0.30 * b.iterations
+    assert a.step_condition_violations == 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_loopback_shards_first_restart_period(ref, world):
+    lp = instances.generate(1, 1, 1.0)
+    p = cabi.params(record_iterate_trace=True, iteration_limit=100)
+    res = shard.solve_loopback(lp, world, p, iterate_capacity=100)
+    _same(res)
+    b = ref.solve_lp(lp, p, iterate_capacity=100)
+    a = res[0]
+    assert len(a.iterate_trace) == len(b.iterate_trace) == 100
+    worst40 = 0.0
+    for (ia, ea, xa, ya), (ib, eb, xb, yb) in zip(a.iterate_trace[:40], b.iterate_trace[:40]):
+        assert ia == ib
+        for u, v in ((xa, xb), (ya, yb)):
+            worst40 = max(worst40, float(np.max(np.abs(u - v) / np.maximum(1.0, np.abs(v)))))
+    assert worst40 <= 1e-10
+    assert a.restart_iterations == b.restart_iterations
+    assert a.kkt_passes == b.kkt_passes
+
+
+def test_shard_rejects_unsupported_modes():
+    lp = instances.generate(1, 1, 0.2)
+    with pytest.raises(cabi.FolpError):
+        shard.solve_loopback(lp, 2, cabi.params(step_policy="malitsky_pock"))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_nccl_world1_matches_single_gpu(eng):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        lp = instances.generate(1, 1, 1.0)
+        p = cabi.params(record_iterate_trace=True, iteration_limit=120)
+        a = shard.solve(lp, p, iterate_capacity=120)
+    finally:
+        dist.destroy_process_group()
+    b = eng.solve_lp(lp, p, iterate_capacity=120)
+    assert a.iterations == b.iterations == 120
+    assert a.restart_iterations == b.restart_iterations
+    worst = 0.0
+    for (ia, ea, xa, ya), (ib, eb, xb, yb) in zip(a.iterate_trace[:40], b.iterate_trace[:40]):
+        for u, v in ((xa, xb), (ya, yb)):
+            worst = max(worst, float(np.max(np.abs(u - v) / np.maximum(1.0, np.abs(v)))))
+    assert worst <= 1e-12

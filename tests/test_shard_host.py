@@ -1,0 +1,124 @@
+"""Host logic of the multi-GPU row shards, no GPU needed:
+the row partition (folp_gpu_shard_rows), the per-shard CSC extraction
+(folp_gpu_shard_local_csc), and -- with two gloo processes on 127.0.0.1 --
+the exchange algebra of the sharded trial: the all-reduced partial products
+K'_p y_p equal K'y, and the shards' K_p x slices reassemble K x (the
+reassembly the engine does by broadcasting each shard's rows)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_2106_04756_b200 import instances, shard
+
+
+def _csc(lp):
+    a = sp.csr_matrix((lp.row_values, lp.row_cols, lp.row_start),
+                      shape=(lp.num_rows, lp.num_cols))
+    c = a.tocsc()
+    c.sort_indices()
+    return a, c
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 0.002), (3, 0.0002), (5, 0.002)])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_rows_partition(cfg, scale, world):
+    lp = instances.generate(cfg, 1, scale)
+    b = shard.shard_rows(lp.num_rows, lp.row_start, world)
+    assert b[0] == 0 and b[-1] == lp.num_rows
+    assert np.all(np.diff(b) >= 0)
+    # balanced on nonzeros + rows up to one row's weight
+    w = lp.row_start[b[1:]] - lp.row_start[b[:-1]] + np.diff(b)
+    heaviest_row = int(np.max(np.diff(lp.row_start))) + 1
+    assert np.max(w) - np.min(w) <= 2 * heaviest_row + 1
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_local_csc_partitions_the_entries(world):
+    lp = instances.generate(2, 1, 0.002)
+    a, c = _csc(lp)
+    b = shard.shard_rows(lp.num_rows, lp.row_start, world)
+    seen = np.zeros(a.nnz, dtype=np.int64)
+    for r in range(world):
+        lptr, pos = shard.local_csc(lp.num_cols, c.indptr, c.indices, b[r], b[r + 1])
+        assert lptr[0] == 0 and lptr[-1] == len(pos)
+        rows = c.indices[pos]
+        assert np.all((rows >= b[r]) & (rows < b[r + 1]))
+        # column j's local entries are a sub-range of full column j, in order
+        for j in range(0, lp.num_cols, max(1, lp.num_cols // 50)):
+            p = pos[lptr[j]:lptr[j + 1]]
+            assert np.all((p >= c.indptr[j]) & (p < c.indptr[j + 1]))
+            assert np.all(np.diff(p) == 1)
+        seen[pos] += 1
+    assert np.all(seen == 1)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _rank_main(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lp = instances.generate(2, 3, 0.003)
+        a, c = _csc(lp)
+        rng = np.random.default_rng(7)
+        x = rng.standard_normal(lp.num_cols)
+        y = rng.standard_normal(lp.num_rows)
+        b = shard.shard_rows(lp.num_rows, lp.row_start, world)
+        r0, r1 = int(b[rank]), int(b[rank + 1])
+        lptr, pos = shard.local_csc(lp.num_cols, c.indptr, c.indices, r0, r1)
+        # partial K'_p y_p from the shard's own entries and its own dual rows
+        vals, rows = c.data[pos], c.indices[pos]
+        part = np.zeros(lp.num_cols)
+        cols = np.repeat(np.arange(lp.num_cols), np.diff(lptr))
+        np.add.at(part, cols, vals * y[rows])
+        t = torch.from_numpy(part)
+        dist.all_reduce(t)
+        kty_err = float(np.max(np.abs(t.numpy() - a.T @ y)) / (1 + np.max(np.abs(a.T @ y))))
+        # K_p x over the shard's rows, reassembled by per-shard broadcasts
+        kx = np.zeros(lp.num_rows)
+        kx[r0:r1] = a[r0:r1] @ x
+        full = torch.from_numpy(kx)
+        for src in range(world):
+            seg = full[int(b[src]):int(b[src + 1])].clone()
+            dist.broadcast(seg, src=src)
+            full[int(b[src]):int(b[src + 1])] = seg
+        kx_exact = bool(np.array_equal(full.numpy(), a @ x))
+        # identical decisions need identical sums on every shard
+        s = torch.tensor([float(np.sum(part))])
+        dist.all_reduce(s)
+        gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, s.double())
+        same = all(float(g) == float(gathered[0]) for g in gathered)
+        out.put((rank, kty_err, kx_exact, same, r1 - r0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_exchange_algebra():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    assert [r[0] for r in res] == [0, 1]
+    for _, kty_err, kx_exact, same, rows in res:
+        assert kty_err <= 1e-12
+        assert kx_exact
+        assert same
+        assert rows > 0
