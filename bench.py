@@ -19,8 +19,12 @@ session (include/folp_c.h folp_session_*).
 
 ``--impl reference`` times the reference CPU solver (oracle/_ref, compiled
 from the reference sources) on all host cores: one independent solve per core,
-aggregate iterations/s.  Multi-GPU (torchrun): independent replicas of the
-config per rank ("replicas only" for config 2).
+aggregate iterations/s.  Multi-GPU (torchrun): `--parallelism replicas`
+runs an independent copy of the workload per rank ("replicas only" for
+configs 1-2; weak scaling); `--parallelism shards` runs ONE
+solve row-partitioned over the ranks (NCCL collectives issued by the engine,
+include/folp_gpu.h folp_gpu_shard; strong scaling).  `auto` shards configs
+3-5 when N > 1.
 """
 from __future__ import annotations
 
@@ -201,6 +205,21 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def use_shards(args, world: int) -> bool:
+    if args.parallelism == "shards":
+        return True
+    if args.parallelism == "replicas":
+        return False
+    return world > 1 and args.config >= 3
+
+
+def rel_kkt(info: dict) -> float:
+    gap = info["gap_abs"] / (1 + abs(info["primal_objective"]) + abs(info["dual_objective"]))
+    pr = info["primal_residual_norm"] / (1 + info["norm_q"])
+    du = info["dual_residual_norm"] / (1 + info["norm_c"])
+    return max(gap, pr, du)
+
+
 def config_block(lp, args) -> dict:
     from paper_2106_04756_b200 import instances
 
@@ -211,7 +230,14 @@ def config_block(lp, args) -> dict:
             "step": f"{CADENCE} accepted PDHG iterations + evaluation/restart check",
             "l2": f"resident working set ~{working_mb:.0f} MB (K~ CSR+CSC, original values, "
                   f"iterate vectors) > 126 MB L2; no flush",
-            "parallelism": "replicas" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single"}
+            "parallelism": parallelism_name(args)}
+
+
+def parallelism_name(args) -> str:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if use_shards(args, world):
+        return f"rows{world} (row-sharded K, NCCL all-reduce of K'y + trial sums)"
+    return f"replicas{world}" if world > 1 else "single"
 
 
 def run_b200(args, world, rank, local):
@@ -221,9 +247,16 @@ def run_b200(args, world, rank, local):
     lp = instances.generate(args.config, args.seed, 1.0)
     m, n, nnz = lp.num_rows, lp.num_cols, lp.nnz
     p = cabi.params(eps_optimal=args.eps)
+    sharded = use_shards(args, world)
+    spec = None
+    if sharded:
+        from paper_2106_04756_b200 import shard
+        spec = shard.nccl_spec()
+    # replicas: every rank runs its own solve (work x world); shards: one solve
+    jobs = 1 if sharded else world
 
     # ---- device-resident loop: W untimed + K timed evaluation periods ----
-    sess = eng.session(lp, p)
+    sess = eng.session(lp, p, shard=spec)
     if args.warmup:
         sess.advance(args.warmup)
     s0 = sess.stats()
@@ -240,7 +273,7 @@ def run_b200(args, world, rank, local):
     total_ms = float(sum(step_ms))
     iters = s1["iterations"] - s0["iterations"]
     max_ms = allreduce_max(total_ms, world)
-    value = iters * world / (max_ms / 1000.0)
+    value = iters * jobs / (max_ms / 1000.0)
     slots = s1["loop_slots"] - s0["loop_slots"]
     loop_ms = s1["loop_ms"] - s0["loop_ms"]
     launches = s1["launches"] - s0["launches"]
@@ -251,8 +284,10 @@ def run_b200(args, world, rank, local):
     # ---- end to end: folp_solve() on host arrays, transfers inside --------
     e2e_iters = CADENCE * args.steps
     t = time.perf_counter()
+    if sharded:
+        spec = shard.nccl_spec()  # a fresh communicator for the new solve
     r = eng.solve_lp(lp, cabi.params(eps_optimal=args.eps, iteration_limit=e2e_iters),
-                     trace_capacity=1)
+                     trace_capacity=1, shard=spec)
     e2e_s = time.perf_counter() - t
     e2e_s = allreduce_max(e2e_s, world)
     # CSR+CSC pointers and int64 indices + values, c/l/u/q, start point
@@ -263,8 +298,9 @@ def run_b200(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": len(step_ms), "warmup": args.warmup,
         "ms_per_step": max_ms / max(1, len(step_ms)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator, BASELINE.json configs[1])",
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded generator, BASELINE.json configs[{args.config - 1}])",
         "config": config_block(lp, args),
         "iterations_timed": iters, "trial_slots_timed": slots,
         "gpu_launches": launches,
@@ -273,7 +309,7 @@ def run_b200(args, world, rank, local):
                      "kernel": "segdot_kernel<EpiPrimal> + segdot_kernel<EpiDual> (one trial)",
                      "bytes_per_launch_pair": b_trial,
                      "kernel_ms_per_trial": loop_ms / max(1, slots), "peak_source": peak_src},
-        "e2e": {"value": e2e_iters * world / e2e_s, "unit": UNIT,
+        "e2e": {"value": e2e_iters * jobs / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
                 "seconds": e2e_s, "iterations": r.iterations,
                 "termination": r.termination_reason},
@@ -290,16 +326,40 @@ def run_b200(args, world, rank, local):
                       f"{2 * CADENCE} PDHG iterations timed as the difference of "
                       f"{3 * CADENCE}- and {CADENCE}-iteration solves "
                       f"({big[0][0]:.1f}s - {small[0][0]:.1f}s)"}
-    if args.time_to_tol and rank == 0:
-        t = time.perf_counter()
-        r = eng.solve_lp(lp, cabi.params(eps_optimal=1e-8, time_limit_seconds=args.time_to_tol),
-                         trace_capacity=1)
-        line["time_to_1e-8"] = {"seconds": time.perf_counter() - t,
-                                "termination": r.termination_reason,
-                                "iterations": r.iterations, "kkt_passes": r.kkt_passes,
-                                "restarts": r.restarts}
+    if args.time_to_tol and rank == 0 and world == 1:
+        line["convergence"] = convergence_block(eng, lp, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def convergence_block(eng, lp, args) -> dict:
+    """Solves to 1e-8 relative KKT: config 1 end to end on the B200 and on the
+    reference CPU solver (1 core), and the workload itself under a time limit
+    (the relative KKT error it reaches)."""
+    from oracle import ref
+    from paper_2106_04756_b200 import cabi, instances
+
+    out = {}
+    lp1 = instances.generate(1, args.seed, 1.0)
+    t = time.perf_counter()
+    a = eng.solve_lp(lp1, cabi.params(eps_optimal=1e-8), trace_capacity=1)
+    gpu_s = time.perf_counter() - t
+    t = time.perf_counter()
+    b = ref.binding().solve_lp(lp1, cabi.params(eps_optimal=1e-8), trace_capacity=1)
+    cpu_s = time.perf_counter() - t
+    out["config1_to_1e-8"] = {
+        "b200_seconds": gpu_s, "b200_iterations": a.iterations, "b200": a.termination_reason,
+        "b200_rel_kkt": rel_kkt(a.final_info),
+        "reference_cpu_seconds": cpu_s, "reference_iterations": b.iterations,
+        "reference": b.termination_reason}
+    t = time.perf_counter()
+    r = eng.solve_lp(lp, cabi.params(eps_optimal=1e-8, time_limit_seconds=args.time_to_tol),
+                     trace_capacity=1)
+    out[f"config{args.config}_time_limited"] = {
+        "seconds": time.perf_counter() - t, "time_limit": args.time_to_tol,
+        "termination": r.termination_reason, "iterations": r.iterations,
+        "rel_kkt_reached": rel_kkt(r.final_info), "restarts": r.restarts}
+    return out
 
 
 def main():
@@ -313,8 +373,10 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-8)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--ref-threads", type=int, default=0)
-    ap.add_argument("--time-to-tol", type=float, default=120.0,
-                    help="also solve to 1e-8 with this time limit (s); 0 disables")
+    ap.add_argument("--time-to-tol", type=float, default=60.0,
+                    help="also solve config 1 to 1e-8 (B200 and reference CPU) and the "
+                         "workload with this time limit (s); 0 disables")
+    ap.add_argument("--parallelism", choices=["auto", "replicas", "shards"], default="auto")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     try:

@@ -73,9 +73,12 @@ def nccl_spec(group=None) -> cabi.ShardC:
     """Shard spec of this rank: rank 0 creates the NCCL unique id, every rank
     receives it through torch.distributed (any backend)."""
     import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    obj = [nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0, group=group)
+    if not dist.is_available() or not dist.is_initialized():
+        rank, world, obj = 0, 1, [nccl_unique_id()]  # a one-rank communicator
+    else:
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
     spec = cabi.ShardC()
     spec.rank, spec.world, spec.backend = rank, world, cabi.SHARD_NCCL
     C.memmove(spec.nccl_id, obj[0], 128)
