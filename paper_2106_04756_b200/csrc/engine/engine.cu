@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cmath>
 #include <cstdio>
@@ -34,6 +35,7 @@
 #include "ops.cuh"
 
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 using namespace folpgpu;
 
@@ -288,12 +290,85 @@ struct LoopbackComm final : ShardComm {
 };
 
 
+// Process-wide cache of device and pinned host blocks keyed by (device,
+// bytes).  A solve context holds ~60 buffers; repeated solves of one size
+// (bench e2e, batched solves, the session API) reuse them instead of paying
+// cudaMalloc / cudaFree / cudaMallocHost every time (~100 ms per context on
+// B200 for config 2).  Cached bytes are capped; beyond the cap blocks are
+// released.  Blocks come back uninitialized, like cudaMalloc's.
+struct BlockCache {
+  std::mutex mu;
+  std::unordered_multimap<uint64_t, void*> free_dev, free_host;
+  std::unordered_map<void*, uint64_t> live;
+  uint64_t cached_bytes = 0;
+  static constexpr uint64_t kCap = uint64_t(16) << 30;
+};
+BlockCache& block_cache() {
+  static BlockCache* bc = new BlockCache();  // process lifetime
+  return *bc;
+}
+uint64_t block_key(size_t bytes, bool host) {
+  int dev = 0;
+  if (!host) cudaGetDevice(&dev);
+  return static_cast<uint64_t>(bytes) | (static_cast<uint64_t>(dev) << 56);
+}
+void* block_alloc(size_t bytes, bool host) {
+  BlockCache& bc = block_cache();
+  const uint64_t key = block_key(bytes, host);
+  auto& pool = host ? bc.free_host : bc.free_dev;
+  {
+    std::lock_guard<std::mutex> lk(bc.mu);
+    auto it = pool.find(key);
+    if (it != pool.end()) {
+      void* p = it->second;
+      pool.erase(it);
+      bc.cached_bytes -= bytes;
+      bc.live[p] = key | (host ? (uint64_t(1) << 55) : 0);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (host) {
+    CK(cudaMallocHost(&p, bytes));
+  } else {
+    CK(cudaMalloc(&p, bytes));
+  }
+  std::lock_guard<std::mutex> lk(bc.mu);
+  bc.live[p] = key | (host ? (uint64_t(1) << 55) : 0);
+  return p;
+}
+void block_free(void* p) {
+  if (p == nullptr) return;
+  BlockCache& bc = block_cache();
+  std::unique_lock<std::mutex> lk(bc.mu);
+  auto it = bc.live.find(p);
+  if (it == bc.live.end()) return;
+  const bool host = (it->second >> 55) & 1;
+  const uint64_t key = it->second & ~(uint64_t(1) << 55);
+  const uint64_t bytes = key & ((uint64_t(1) << 55) - 1);
+  bc.live.erase(it);
+  if (bc.cached_bytes + bytes > BlockCache::kCap) {
+    lk.unlock();
+    if (host) {
+      cudaFreeHost(p);
+    } else {
+      cudaFree(p);
+    }
+    return;
+  }
+  (host ? bc.free_host : bc.free_dev).emplace(key, p);
+  bc.cached_bytes += bytes;
+}
+
 template <class T>
 T* dalloc(size_t count) {
-  T* p = nullptr;
   if (count == 0) count = 1;
-  CK(cudaMalloc(&p, count * sizeof(T)));
-  return p;
+  return static_cast<T*>(block_alloc(count * sizeof(T), false));
+}
+template <class T>
+void halloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  *p = static_cast<T*>(block_alloc(count * sizeof(T), true));
 }
 
 // ---------------------------------------------------------------------
@@ -729,17 +804,18 @@ struct folp_gpu_ctx {
     if (device >= 0) cudaSetDevice(device);
     for (auto& e : chunk_exec)
       if (e) cudaGraphExecDestroy(e);
-    for (void* p : owned) cudaFree(p);
-    for (void* p : rows.owned) cudaFree(p);
-    for (void* p : cols.owned) cudaFree(p);
-    for (void* p : lrows.owned) cudaFree(p);
-    for (void* p : lcols.owned) cudaFree(p);
+    if (stream) cudaStreamSynchronize(stream);  // cached blocks must be idle
+    for (void* p : owned) block_free(p);
+    for (void* p : rows.owned) block_free(p);
+    for (void* p : cols.owned) block_free(p);
+    for (void* p : lrows.owned) block_free(p);
+    for (void* p : lcols.owned) block_free(p);
     comm.reset();
-    if (res_h) cudaFreeHost(res_h);
-    if (st_h) cudaFreeHost(st_h);
-    if (ndg_h) cudaFreeHost(ndg_h);
-    if (red_h) cudaFreeHost(red_h);
-    if (grow_h) cudaFreeHost(grow_h);
+    block_free(res_h);
+    block_free(st_h);
+    block_free(ndg_h);
+    block_free(red_h);
+    block_free(grow_h);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (tev0) cudaEventDestroy(tev0);
@@ -865,6 +941,89 @@ void copy_d2d(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
   if (count > 0 && dst != src) {
     CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   }
+}
+
+// CSR -> CSC on the device (the reference's counting
+// pass, sparse_matrix.cpp:82-102): a stable radix sort of the entries by
+// column keeps each column in increasing row order, i.e. exactly the
+// reference's layout.  Fills csc_ptr / csc_row / csc_orig and returns the
+// column starts on the host (for the unit plan).
+__global__ void k_row_ids(const int* ptr, int64_t m, int* rowid) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < m;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int k = ptr[r]; k < ptr[r + 1]; ++k) rowid[k] = static_cast<int>(r);
+  }
+}
+__global__ void k_iota(int* v, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    v[i] = static_cast<int>(i);
+  }
+}
+__global__ void k_col_counts(const int* col, int64_t nnz, int* counts) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    atomicAdd(&counts[col[i] + 1], 1);  // integer counts: order-free
+  }
+}
+__global__ void k_csc_fill(const int* order, const int* rowid, const double* vals, int64_t nnz,
+                           int* csc_row, double* csc_val) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = order[i];
+    csc_row[i] = rowid[k];
+    csc_val[i] = vals[k];
+  }
+}
+
+void device_transpose(folp_gpu_ctx* c, std::vector<int64_t>& col_start) {
+  const int64_t m = c->m, n = c->n, nnz = c->nnz;
+  cudaStream_t s = c->stream;
+  std::vector<void*> tmp;
+  auto scratch = [&](size_t bytes) {
+    void* p = block_alloc(std::max<size_t>(bytes, 16), false);
+    tmp.push_back(p);
+    return p;
+  };
+  try {
+    int* rowid = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* keys = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* order_in = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* order = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* counts = static_cast<int*>(scratch((n + 1) * sizeof(int)));
+    const int grid = c->simple_grid(std::max<int64_t>(m, nnz));
+    k_row_ids<<<c->simple_grid(m), kBlock, 0, s>>>(c->csr_ptr, m, rowid);
+    k_iota<<<grid, kBlock, 0, s>>>(order_in, nnz);
+    CK(cudaMemsetAsync(counts, 0, (n + 1) * sizeof(int), s));
+    k_col_counts<<<grid, kBlock, 0, s>>>(c->csr_col, nnz, counts);
+    c->launches += 3;
+    CK(cudaGetLastError());
+    int end_bit = 1;
+    while (end_bit < 31 && (int64_t(1) << end_bit) < n) ++end_bit;
+    size_t sort_bytes = 0, scan_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, c->csr_col, keys, order_in, order,
+                                       static_cast<int>(nnz), 0, end_bit, s));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, counts, c->csc_ptr,
+                                     static_cast<int>(n + 1), s));
+    void* sort_tmp = scratch(sort_bytes);
+    void* scan_tmp = scratch(scan_bytes);
+    CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, c->csr_col, keys, order_in, order,
+                                       static_cast<int>(nnz), 0, end_bit, s));
+    CK(cub::DeviceScan::InclusiveSum(scan_tmp, scan_bytes, counts, c->csc_ptr,
+                                     static_cast<int>(n + 1), s));
+    k_csc_fill<<<grid, kBlock, 0, s>>>(order, rowid, c->csr_orig, nnz, c->csc_row, c->csc_orig);
+    c->launches += 3;  // + the two cub passes' kernels, not counted
+    CK(cudaGetLastError());
+    std::vector<int> cs32(static_cast<size_t>(n) + 1);
+    CK(cudaMemcpyAsync(cs32.data(), c->csc_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    col_start.assign(cs32.begin(), cs32.end());
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    for (void* p : tmp) block_free(p);
+    throw;
+  }
+  for (void* p : tmp) block_free(p);
 }
 
 int pick_device(int device) {
@@ -1426,6 +1585,16 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       cudaGetLastError();
       throw EngineError(FOLP_E_NO_DEVICE, "folp_gpu_create: no CUDA device visible");
     }
+    const bool timing = std::getenv("FOLP_TIMING") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::string marks;
+    auto mark = [&](const char* stage) {
+      if (!timing) return;
+      char buf[64];
+      std::snprintf(buf, sizeof(buf), " %s %.4f", stage,
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      marks += buf;
+    };
     std::unique_ptr<folp_gpu_ctx> c(new folp_gpu_ctx());
     c->device = pick_device(device);
     c->ordered = g_default_ordered;
@@ -1433,14 +1602,13 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       c->ordered = std::strcmp(env, "ordered") == 0;
     }
     set_device(c.get());
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, c->device));
-    c->sms = prop.multiProcessorCount;
+    CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreate(&c->tev0));
     CK(cudaEventCreate(&c->tev1));
+    mark("stream");
     const int64_t m = p->num_rows, n = p->num_cols, nnz = p->nnz;
     c->m = m;
     c->n = n;
@@ -1448,16 +1616,11 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     c->nnz = nnz;
     c->objective_constant = p->objective_constant;
 
-    std::vector<int64_t> cs, cr;
-    std::vector<double> cv;
+    std::vector<int64_t> cs;
     const int64_t *col_start = p->col_start, *col_rows = p->col_rows;
     const double* col_values = p->col_values;
-    if (col_start == nullptr || col_rows == nullptr || col_values == nullptr) {
-      transpose_host(m, n, p->row_start, p->row_cols, p->row_values, cs, cr, cv);
-      col_start = cs.data();
-      col_rows = cr.data();
-      col_values = cv.data();
-    }
+    // No column mirror from the host: transpose on the device (below).
+    const bool device_csc = col_start == nullptr || col_rows == nullptr || col_values == nullptr;
 
     // value / index streams padded by 8 entries: bulk tiles are staged in
     // 16-byte-aligned windows that may run up to 3 entries past the end
@@ -1475,23 +1638,33 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       try {
         upload_index(c.get(), p->row_start, c->csr_ptr, m + 1, stage, cap);
         upload_index(c.get(), p->row_cols, c->csr_col, nnz, stage, cap);
-        upload_index(c.get(), col_start, c->csc_ptr, n + 1, stage, cap);
-        upload_index(c.get(), col_rows, c->csc_row, nnz, stage, cap);
+        if (!device_csc) {
+          upload_index(c.get(), col_start, c->csc_ptr, n + 1, stage, cap);
+          upload_index(c.get(), col_rows, c->csc_row, nnz, stage, cap);
+        }
         CK(cudaStreamSynchronize(c->stream));
       } catch (...) {
-        cudaFree(stage);
+        block_free(stage);
         throw;
       }
-      cudaFree(stage);
+      block_free(stage);
     }
+    mark("indices");
     upload(c.get(), c->csr_orig, p->row_values, nnz);
-    upload(c.get(), c->csc_orig, col_values, nnz);
+    if (device_csc) {
+      device_transpose(c.get(), cs);
+      col_start = cs.data();
+    } else {
+      upload(c.get(), c->csc_orig, col_values, nnz);
+    }
     copy_d2d(c.get(), c->csr_work, c->csr_orig, nnz);
     copy_d2d(c.get(), c->csc_work, c->csc_orig, nnz);
 
+    mark("values");
     build_plan(c.get(), p->row_start, m, nnz, c->csr_ptr, c->csr_col, c->rows);
     build_plan(c.get(), col_start, n, nnz, c->csc_ptr, c->csc_row, c->cols);
 
+    mark("plans");
     auto vn = [&] { return c->alloc<double>(n); };
     auto vm = [&] { return c->alloc<double>(m); };
     c->c0 = vn(); c->l0 = vn(); c->u0 = vn(); c->q0 = vm();
@@ -1520,18 +1693,19 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     c->counters = c->alloc<unsigned>(kCounters);
     CK(cudaMemsetAsync(c->counters, 0, kCounters * sizeof(unsigned), c->stream));
     c->res = c->alloc<double>(kResSlots);
-    CK(cudaMallocHost(&c->res_h, kResSlots * sizeof(double)));
+    halloc(&c->res_h, kResSlots);
     c->st_d = c->alloc<DevState>(1);
-    CK(cudaMallocHost(&c->st_h, sizeof(DevState)));
+    halloc(&c->st_h, 1);
     std::memset(c->st_h, 0, sizeof(DevState));
     c->ndg_d = c->alloc<NdgState>(2);
-    CK(cudaMallocHost(&c->ndg_h, 2 * sizeof(NdgState)));
+    halloc(&c->ndg_h, 2);
     c->table_cap = 4096;
     c->red_d = c->alloc<double>(c->table_cap);
     c->grow_d = c->alloc<double>(c->table_cap);
-    CK(cudaMallocHost(&c->red_h, c->table_cap * sizeof(double)));
-    CK(cudaMallocHost(&c->grow_h, c->table_cap * sizeof(double)));
+    halloc(&c->red_h, c->table_cap);
+    halloc(&c->grow_h, c->table_cap);
 
+    mark("buffers");
     upload(c.get(), c->c0, p->objective, n);
     upload(c.get(), c->l0, p->variable_lower, n);
     upload(c.get(), c->u0, p->variable_upper, n);
@@ -1551,6 +1725,8 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     }
     zero_average(c.get());
     CK(cudaStreamSynchronize(c->stream));
+    mark("vectors");
+    if (timing) std::fprintf(stderr, "[folp timing] engine create:%s\n", marks.c_str());
     *out = c.release();
   });
 }

@@ -2,7 +2,10 @@
 //
 // Exceptions never cross this boundary: each entry maps the folp exception
 // type to its FOLP_E_* code and keeps the message for folp_last_error().
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <cstring>
 #include <exception>
@@ -241,7 +244,12 @@ void folp_params_default(folp_params_c* p) {
 int folp_solve(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
                const double* y0, folp_result_c* out) {
   return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
     const LinearProgram lp = to_lp(lp_in);
+    if (std::getenv("FOLP_TIMING") != nullptr) {
+      std::fprintf(stderr, "[folp timing] folp_solve to_lp %.4fs\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
     const SolverParams params = to_params(p);
     PrimalDualPoint z0;
     z0.primal.assign(static_cast<std::size_t>(lp_in->num_cols), 0.0);

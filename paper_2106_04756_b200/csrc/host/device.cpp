@@ -33,9 +33,13 @@ void Context::create(const SparseMatrix& k, const double* c, const double* q, co
   p.row_start = k.row_start().data();
   p.row_cols = k.row_cols().data();
   p.row_values = k.row_values().data();
-  p.col_start = k.col_start().data();
-  p.col_rows = k.col_rows().data();
-  p.col_values = k.col_values().data();
+  // The column mirror goes up only if the host already has it; otherwise
+  // the engine transposes K on the device.
+  if (k.has_column_mirror()) {
+    p.col_start = k.col_start().data();
+    p.col_rows = k.col_rows().data();
+    p.col_values = k.col_values().data();
+  }
   p.objective = c;
   p.right_hand_side = q;
   p.variable_lower = l;
@@ -47,7 +51,7 @@ void Context::create(const SparseMatrix& k, const double* c, const double* q, co
     zero_rows.assign(static_cast<std::size_t>(k.num_rows()) + 1, 0);
     p.row_start = zero_rows.data();
   }
-  if (k.col_start().empty()) {
+  if (p.col_start != nullptr && k.col_start().empty()) {
     zero_cols.assign(static_cast<std::size_t>(k.num_cols()) + 1, 0);
     p.col_start = zero_cols.data();
   }

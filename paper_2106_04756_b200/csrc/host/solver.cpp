@@ -18,6 +18,7 @@
 #include <memory>
 #include <ostream>
 #include <random>
+#include <string>
 
 #include "device.hpp"
 #include "session.hpp"
@@ -204,6 +205,13 @@ class Driver {
   double time_chunks_ = 0.0;  // host wall time in loop chunks / evaluations
   double time_evals_ = 0.0;   // (printed at finish when FOLP_TIMING is set)
   double time_setup_ = 0.0;
+  std::string setup_marks_;   // FOLP_TIMING: elapsed time at each setup stage
+  void mark(const char* stage) {
+    if (std::getenv("FOLP_TIMING") == nullptr) return;
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), " %s %.4f", stage, elapsed());
+    setup_marks_ += buf;
+  }
 };
 
 SolveResult Driver::finish_point(TerminationReason reason, const PrimalDualPoint& reduced,
@@ -236,9 +244,9 @@ SolveResult Driver::finish_point(TerminationReason reason, const PrimalDualPoint
   if (std::getenv("FOLP_TIMING") != nullptr) {
     std::fprintf(stderr,
                  "[folp timing] total %.4fs  setup %.4fs  chunks %.4fs  evaluations %.4fs  "
-                 "iterations %lld\n",
+                 "iterations %lld  setup stages:%s\n",
                  r.wall_seconds, time_setup_, time_chunks_, time_evals_,
-                 static_cast<long long>(r.iterations));
+                 static_cast<long long>(r.iterations), setup_marks_.c_str());
   }
   return r;
 }
@@ -416,8 +424,9 @@ std::optional<SolveResult> Driver::start() {
     throw std::invalid_argument("solve: invalid program: " + issue->message);
   }
 
+  mark("validated");
   if (p_.use_presolve) {
-    PresolveResult pre = presolve(raw_);
+    PresolveResult pre = presolve_for_solve(raw_);
     if (pre.status != PresolveStatus::kReduced) return finish_detected(pre.status);
     transform_ = std::move(pre.transform);
     if (transform_.is_identity() && pre.reduced.objective_constant == raw_.objective_constant) {
@@ -431,6 +440,7 @@ std::optional<SolveResult> Driver::start() {
     transform_.original_rows = raw_.num_rows();
     transform_.original_cols = raw_.num_variables();
   }
+  mark("presolved");
   if (work_->num_variables() == 0) return finish_trivial();
 
   if (p_.use_pock_chambolle) {
@@ -446,9 +456,11 @@ std::optional<SolveResult> Driver::start() {
   }
 
   dev_ = std::make_unique<device::Context>(*work_);
+  mark("context");
   device::check(folp_gpu_rescale(ctx(), p_.ruiz_iterations, p_.use_pock_chambolle ? 1 : 0,
                                  p_.pc_alpha, nullptr, nullptr),
                 "rescale_problem");
+  mark("rescaled");
   if (shard_ != nullptr) dev_->attach_shard(work_->constraint_matrix, *shard_);
 
   // start point into the working space, projected (solver.cpp:853-865)
@@ -481,6 +493,7 @@ std::optional<SolveResult> Driver::start() {
     mp_theta_ = 1.0;
   }
 
+  mark("stepsize");
   time_setup_ = elapsed();
   {
     const ConvergenceInfo info0 = evaluate(FOLP_PT_CURRENT);

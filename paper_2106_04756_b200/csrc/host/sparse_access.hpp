@@ -11,8 +11,8 @@ namespace folp {
 
 struct SparseMatrixAccess {
   // From a valid CSR (columns strictly increasing inside each row, no
-  // zeros): builds the column mirror by a counting pass, exactly the layout
-  // from_triplets produces for the same entries.
+  // zeros); the column mirror (the layout from_triplets produces) is built
+  // on first use.
   static SparseMatrix build(Index m, Index n, std::vector<Index> start, std::vector<Index> cols,
                             std::vector<double> vals);
   // Same structure as k, new values (CSR and CSC order).

@@ -143,12 +143,49 @@ SparseMatrix SparseMatrix::scaled(std::span<const double> row_scale,
       out.csr_values_[k] *= row_scale[r] * col_scale[csr_index_[k]];
     }
   }
+  const ColumnMirror& cm = columns();
+  auto mirror = std::make_shared<ColumnMirror>(cm);
   for (Index c = 0; c < num_cols_; ++c) {
-    for (Index k = csc_start_[c]; k < csc_start_[c + 1]; ++k) {
-      out.csc_values_[k] *= col_scale[c] * row_scale[csc_index_[k]];
+    for (Index k = cm.start[c]; k < cm.start[c + 1]; ++k) {
+      mirror->values[k] *= col_scale[c] * row_scale[cm.index[k]];
     }
   }
+  out.csc_ = std::move(mirror);
+  out.csc_mu_ = std::make_shared<std::mutex>();
   return out;
+}
+
+bool SparseMatrix::has_column_mirror() const {
+  if (!csc_mu_) return csc_ != nullptr;  // moved-from
+  std::lock_guard<std::mutex> lk(*csc_mu_);
+  return csc_ != nullptr;
+}
+
+// The column-compressed mirror by a counting pass in row order: columns in
+// increasing row order, the layout from_triplets produces
+// (sparse_matrix.cpp:82-102).
+const SparseMatrix::ColumnMirror& SparseMatrix::columns() const {
+  if (!csc_mu_) csc_mu_ = std::make_shared<std::mutex>();  // moved-from, single owner
+  std::lock_guard<std::mutex> lk(*csc_mu_);
+  if (!csc_) {
+    auto cm = std::make_shared<ColumnMirror>();
+    const Index nnz = static_cast<Index>(csr_values_.size());
+    cm->start.assign(static_cast<std::size_t>(num_cols_) + 1, 0);
+    cm->index.resize(static_cast<std::size_t>(nnz));
+    cm->values.resize(static_cast<std::size_t>(nnz));
+    for (Index e = 0; e < nnz; ++e) ++cm->start[csr_index_[e] + 1];
+    for (Index c = 0; c < num_cols_; ++c) cm->start[c + 1] += cm->start[c];
+    std::vector<Index> fill(cm->start.begin(), cm->start.end() - 1);
+    for (Index r = 0; r < num_rows_; ++r) {
+      for (Index e = csr_start_[r]; e < csr_start_[r + 1]; ++e) {
+        const Index slot = fill[csr_index_[e]]++;
+        cm->index[slot] = r;
+        cm->values[slot] = csr_values_[e];
+      }
+    }
+    csc_ = std::move(cm);
+  }
+  return *csc_;
 }
 
 SparseMatrix SparseMatrixAccess::build(Index m, Index n, std::vector<Index> start,
@@ -156,24 +193,10 @@ SparseMatrix SparseMatrixAccess::build(Index m, Index n, std::vector<Index> star
   SparseMatrix k;
   k.num_rows_ = m;
   k.num_cols_ = n;
-  const Index nnz = static_cast<Index>(vals.size());
-  k.csc_start_.assign(static_cast<std::size_t>(n) + 1, 0);
-  k.csc_index_.resize(static_cast<std::size_t>(nnz));
-  k.csc_values_.resize(static_cast<std::size_t>(nnz));
-  for (Index e = 0; e < nnz; ++e) ++k.csc_start_[cols[e] + 1];
-  for (Index c = 0; c < n; ++c) k.csc_start_[c + 1] += k.csc_start_[c];
-  std::vector<Index> fill(k.csc_start_.begin(), k.csc_start_.end() - 1);
-  for (Index r = 0; r < m; ++r) {
-    for (Index e = start[r]; e < start[r + 1]; ++e) {
-      const Index slot = fill[cols[e]]++;
-      k.csc_index_[slot] = r;
-      k.csc_values_[slot] = vals[e];
-    }
-  }
   k.csr_start_ = std::move(start);
   k.csr_index_ = std::move(cols);
   k.csr_values_ = std::move(vals);
-  return k;
+  return k;  // column mirror on first use
 }
 
 SparseMatrix SparseMatrixAccess::with_values(const SparseMatrix& k, std::vector<double> csr,
@@ -183,10 +206,13 @@ SparseMatrix SparseMatrixAccess::with_values(const SparseMatrix& k, std::vector<
   out.num_cols_ = k.num_cols_;
   out.csr_start_ = k.csr_start_;
   out.csr_index_ = k.csr_index_;
-  out.csc_start_ = k.csc_start_;
-  out.csc_index_ = k.csc_index_;
   out.csr_values_ = std::move(csr);
-  out.csc_values_ = std::move(csc);
+  const SparseMatrix::ColumnMirror& cm = k.columns();
+  auto mirror = std::make_shared<SparseMatrix::ColumnMirror>();
+  mirror->start = cm.start;
+  mirror->index = cm.index;
+  mirror->values = std::move(csc);
+  out.csc_ = std::move(mirror);
   return out;
 }
 
