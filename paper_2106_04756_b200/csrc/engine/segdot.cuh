@@ -239,8 +239,16 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   double* wbuf = s_prod[warp];
   const int nw = static_cast<int>(gridDim.x) * kWarps;
 
-  for (int u = blockIdx.x * kWarps + warp; u < p.n_units; u += nw) {
-    const int4 d = p.units[u];
+  // The next unit's descriptor is loaded one unit ahead: every dependent
+  // load waits behind the SM's whole gather queue, so the descriptor ->
+  // indices -> gathers chain is cut to indices -> gathers.  (Prefetching the
+  // index stream too -- in registers or by cp.async -- costs occupancy or
+  // data-pipe wavefronts and measured slower: profiles/r1_segpipe_experiments.md.)
+  int u = blockIdx.x * kWarps + warp;
+  int4 d_next = u < p.n_units ? p.units[u] : make_int4(0, 0, 0, 0);
+  for (; u < p.n_units; u += nw) {
+    const int4 d = d_next;
+    if (u + nw < p.n_units) d_next = p.units[u + nw];
     const int k0 = d.z, k1 = d.w;
     if (d.x >= 0 && k1 - k0 > kWarpTile) {
       // ordered plan: one long segment, summed by one lane in index order
