@@ -657,6 +657,7 @@ struct folp_gpu_ctx {
   double norm_q_sq = 0.0, norm_c_sq = 0.0;
   int max_giant = 0;
   int bisect_grid = 0;
+  int64_t ndg_count = 0, ndg_passes = 0, ndg_levels = 0;  // FOLP_TIMING statistics
   void* loop_block = nullptr;  // K~ values + indices of CSR and CSC (one block)
   size_t loop_block_bytes = 0;
 
@@ -803,6 +804,11 @@ struct folp_gpu_ctx {
   }
 
   ~folp_gpu_ctx() {
+    if (ndg_count > 0 && std::getenv("FOLP_TIMING") != nullptr) {
+      std::fprintf(stderr, "[folp timing] duality gaps %lld: %.1f passes, %.1f bisection levels each\n",
+                   static_cast<long long>(ndg_count), static_cast<double>(ndg_passes) / ndg_count,
+                   static_cast<double>(ndg_levels) / ndg_count);
+    }
     if (device >= 0) cudaSetDevice(device);
     for (auto& e : chunk_exec)
       if (e) cudaGraphExecDestroy(e);
@@ -1112,7 +1118,9 @@ __global__ void k_ndg_init(NdgState* st, const double* sums, const double* dist,
 // and replays the same decisions, so the bisection state never leaves
 // shared memory until the end.  Replaces up to ~70 launches per period.
 constexpr int kBisectThreads = 512;
-constexpr int kBisectVals = 2 * kNuCands;  // ||d||_w^2 and g'd per midpoint
+// ||d||_w^2 and g'd per midpoint, then the bracket sums of the analytic
+// finish: elements with a breakpoint inside, Q, H, S (ndg_finish_analytic)
+constexpr int kBisectVals = 2 * kNuCands + 4;
 
 struct BisectArgs {
   int64_t n, total;
@@ -1166,6 +1174,20 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
           acc[s][2 * p] += w * d * d;
           acc[s][2 * p + 1] += gs * d;
         }
+        if (gs != 0.0) {
+          const int side = primal ? 0 : 1;
+          const double ulo = gs * st[s].rcp_lo[side];  // |u| largest at nu_lo
+          const double uhi = gs * st[s].rcp_hi[side];
+          const bool clamped_lo = ulo < los || ulo > his;
+          const bool clamped_hi = uhi < los || uhi > his;
+          if (clamped_lo && !clamped_hi) acc[s][2 * kNuCands] += 1.0;
+          if (clamped_hi) {  // clamped over the whole bracket
+            const double cv = uhi > his ? his : los;
+            acc[s][2 * kNuCands + 1] += w * cv * cv;
+            acc[s][2 * kNuCands + 2] += gs * cv;
+          }
+          if (!clamped_lo) acc[s][2 * kNuCands + 3] += gs * gs * (primal ? winv : omega);
+        }
       }
     }
 #pragma unroll
@@ -1203,6 +1225,11 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
         gd[p] = tot[tid][2 * p + 1];
       }
       ndg_replay(&st[tid], nsq, gd, kNuLevels);
+      // no breakpoint inside this pass's bracket: none inside the narrower one
+      if (!st[tid].done && tot[tid][2 * kNuCands] == 0.0) {
+        ndg_finish_analytic(&st[tid], tot[tid][2 * kNuCands + 1], tot[tid][2 * kNuCands + 2],
+                            tot[tid][2 * kNuCands + 3]);
+      }
     }
     __syncthreads();
   }
@@ -1988,7 +2015,12 @@ int folp_gpu_evaluation_period(folp_gpu_ctx* c, double omega, int32_t want_gaps,
                      out->average.nonfinite || out->average.infinite_product;
     if (!want_gaps || bad) return;
     finish_ndg(c, {true, true}, {omega, omega});
-    for (int s = 0; s < 2; ++s) out->gap[s] = c->ndg_h[s].result;
+    for (int s = 0; s < 2; ++s) {
+      out->gap[s] = c->ndg_h[s].result;
+      c->ndg_count += 1;
+      c->ndg_passes += c->ndg_h[s].passes;
+      c->ndg_levels += c->ndg_h[s].it;
+    }
     out->gaps_valid = 1;
   });
 }

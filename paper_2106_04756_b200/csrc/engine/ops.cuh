@@ -863,6 +863,7 @@ struct NdgState {
   double rcp_primal[kNuCands];  // tree mode: RN(1 / (nu * omega))
   double rcp_dual[kNuCands];    // tree mode: RN(1 / (nu * (1/omega)))
   double omega, winv;
+  double rcp_lo[2], rcp_hi[2];  // tree mode: RN(1 / (nu_lo|hi * w)), primal / dual
   int32_t it;      // bisection iterations consumed (<= 200)
   int32_t done;
   int32_t passes;
@@ -893,6 +894,38 @@ __host__ __device__ inline void ndg_reciprocals(NdgState* st) {
     st->rcp_primal[i] = 1.0 / (st->nu[i] * st->omega);
     st->rcp_dual[i] = 1.0 / (st->nu[i] * st->winv);
   }
+  st->rcp_lo[0] = 1.0 / (st->nu_lo * st->omega);
+  st->rcp_lo[1] = 1.0 / (st->nu_lo * st->winv);
+  st->rcp_hi[0] = 1.0 / (st->nu_hi * st->omega);
+  st->rcp_hi[1] = 1.0 / (st->nu_hi * st->winv);
+}
+
+// Tree mode: once no element changes its clamping state inside the bracket
+// [nu_lo, nu_hi], ||d(nu)||_w^2 = Q + S / nu^2 and g'd(nu) = H + S / nu
+// exactly there (Q, H: the clamped elements' w c^2 and g c; S: the free
+// elements' g^2 / w), so the remaining levels of the reference bisection
+// (solver.cpp:356-368) are replayed from these three sums without another
+// pass over the data.
+__device__ inline void ndg_finish_analytic(NdgState* st, double q, double h, double sfree) {
+  const double r = st->radius;
+  const double r2 = r * r;
+  double lo_ = st->nu_lo, hi_ = st->nu_hi;
+  while (!st->done) {
+    const double nu = 0.5 * (lo_ + hi_);
+    const double nsq = q + sfree / (nu * nu);
+    const double gd = h + sfree / nu;
+    st->it += 1;
+    if (fabs(sqrt(nsq) - r) <= 1e-10 * r || st->it >= 200) {
+      st->result = gd / r;
+      st->done = 1;
+    } else if (nsq > r2) {
+      lo_ = nu;
+    } else {
+      hi_ = nu;
+    }
+  }
+  st->nu_lo = lo_;
+  st->nu_hi = hi_;
 }
 
 // Replays `levels` levels of the reference bisection (solver.cpp:356-368)
