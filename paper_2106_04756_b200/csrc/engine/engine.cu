@@ -615,6 +615,8 @@ int occupancy(const void* fn, int smem = 0) {
 constexpr int kResSlots = 96;
 constexpr int kCounters = 16;
 constexpr int kMaxGrid = 148 * 8;
+constexpr int kSmallThreads = 256;   // k_chunk_cluster CTA
+constexpr int kSmallCluster = 8;     // CTAs in its cluster (portable size)
 
 }  // namespace
 
@@ -657,6 +659,8 @@ struct folp_gpu_ctx {
   double norm_q_sq = 0.0, norm_c_sq = 0.0;
   int max_giant = 0;
   int bisect_grid = 0;
+  bool small_loop = false;        // k_chunk_cluster (tree mode, <= one unit per warp)
+  double* small_multi = nullptr;  // its multi-part epilogue slots
   int64_t ndg_count = 0, ndg_passes = 0, ndg_levels = 0;  // FOLP_TIMING statistics
   void* loop_block = nullptr;  // K~ values + indices of CSR and CSC (one block)
   size_t loop_block_bytes = 0;
@@ -1728,6 +1732,15 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);
       c->terms[1] = c->alloc<double>(5 * (n + m) + 8);
     }
+    {
+      const char* env = std::getenv("FOLP_SMALL_LOOP");
+      // every warp of the cluster owns at most one unit of each product
+      const int warps = kSmallCluster * (kSmallThreads / 32);
+      c->small_loop = !c->ordered && nnz > 0 && c->rows.sp.n_units <= warps &&
+                      c->cols.sp.n_units <= warps && (env == nullptr || std::atoi(env) > 0);
+      c->small_multi = c->alloc<double>(
+          static_cast<size_t>(std::max(c->rows.sp.n_multi, c->cols.sp.n_multi) + 1) * kMaxAcc);
+    }
     c->counters = c->alloc<unsigned>(kCounters);
     CK(cudaMemsetAsync(c->counters, 0, kCounters * sizeof(unsigned), c->stream));
     c->res = c->alloc<double>(kResSlots);
@@ -2110,10 +2123,28 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     if (c->sharded() && policy == FOLP_STEP_MALITSKY_POCK) {
       throw std::invalid_argument("sharded solve: the Malitsky-Pock policy runs on one GPU only");
     }
-    if (!c->sharded() && !c->graph_tried[policy]) build_chunk_graph(c, policy);
+    if (!c->sharded() && !c->small_loop && !c->graph_tried[policy]) build_chunk_graph(c, policy);
     const int per_slot = policy == FOLP_STEP_MALITSKY_POCK ? 4 : 2;
     if (c->profiling) CK(cudaEventRecord(c->ev0, c->stream));
-    if (c->sharded()) {
+    if (c->small_loop && policy != FOLP_STEP_MALITSKY_POCK) {
+      // small problem: the whole chunk in one cluster launch (k_chunk_cluster)
+      const LoopBufs b = c->loop_bufs(cudaGraphConditionalHandle{}, 0);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kSmallCluster);
+      cfg.blockDim = dim3(kSmallThreads);
+      cfg.stream = c->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kSmallCluster;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, k_chunk_cluster<kSmallThreads>, b, c->rows.sp, c->cols.sp,
+                            static_cast<const double*>(c->csr_work),
+                            static_cast<const double*>(c->csc_work), c->small_multi));
+      ++c->launches;
+    } else if (c->sharded()) {
       if (!c->shard_values_ready) {  // K~ values of the local CSC, after rescaling
         k_gather_values<<<c->simple_grid(c->lnnz), kBlock, 0, c->stream>>>(
             c->lcsc_val, c->csc_work, c->lcsc_pos, c->lnnz);
@@ -2149,7 +2180,9 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     }
     if (c->profiling) CK(cudaEventRecord(c->ev1, c->stream));
     c->pull_state();
-    if (!c->sharded()) c->launches += per_slot * st->slots;
+    if (!c->sharded() && !(c->small_loop && policy != FOLP_STEP_MALITSKY_POCK)) {
+      c->launches += per_slot * st->slots;
+    }
     if (policy == FOLP_STEP_MALITSKY_POCK) c->kx_valid = false;  // Kx cache not kept
     if (c->profiling) {
       float ms = 0.f;

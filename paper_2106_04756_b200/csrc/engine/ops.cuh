@@ -19,6 +19,8 @@
 
 #include "segdot.cuh"
 
+#include <cooperative_groups.h>
+
 namespace folpgpu {
 
 // Chunk status values (mirror folp_gpu.h).
@@ -345,6 +347,68 @@ __global__ void k_shard_decide(LoopBufs b, const double* sums) {
 }
 
 // ---------------------------------------------------------------------
+// Small problems (config 1: 10^4 nonzeros): a whole chunk of trials in ONE
+// launch of one thread-block cluster; kernel A and kernel B become
+// cluster-wide phases: every CTA reduces its units, CTA 0 folds the CTAs'
+// partials (distributed shared memory, rank order) and the multi-part slots
+// and runs the epilogue's finalize (kernel B: the step decision), cluster
+// barriers order the phases.  No kernel boundary or graph node per trial --
+// at this size the two-kernel trial is launch / tail bound.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_chunk_cluster(LoopBufs b, SegPlan rows, SegPlan cols,
+                                                      const double* csr_val, const double* csc_val,
+                                                      double* multi_scratch) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  const int ncta = static_cast<int>(cl.num_blocks());
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double wbuf[NT / 32][kWarpTile];
+  __shared__ double scratch[NT / 32][kMaxAcc];
+  __shared__ double parts[16 * kMaxAcc];  // CTA 0: partials of every CTA
+  __shared__ int running;
+  double* parts0 = cl.map_shared_rank(parts, 0);
+  const int u = rank * (NT / 32) + warp;  // this warp's unit in each plan
+  ResidentUnit ua, ub;
+  load_resident(cols, csc_val, u, lane, ua);
+  load_resident(rows, csr_val, u, lane, ub);
+  auto fold = [&](double* tot, int K, const SegPlan& p) {
+    for (int k = 0; k < K; ++k) {
+      double v = 0.0;
+      for (int r = 0; r < ncta; ++r) v += parts[r * kMaxAcc + k];
+      for (int q = 0; q < p.n_multi; ++q) v += multi_scratch[q * K + k];
+      tot[k] = v;
+    }
+  };
+  for (;;) {
+    if (threadIdx.x == 0) running = b.st->running;
+    __syncthreads();
+    if (!running) break;
+    EpiPrimal ea{b};
+    ea.prepare();
+    cluster_product<NT>(cols, ua, u, ea, rank, wbuf[warp], scratch, multi_scratch, parts0);
+    cl.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+      double t[EpiPrimal::K];
+      fold(t, EpiPrimal::K, cols);
+      ea.finalize(t);
+    }
+    cl.sync();
+    EpiDual eb{b};
+    eb.prepare();
+    cluster_product<NT>(rows, ub, u, eb, rank, wbuf[warp], scratch, multi_scratch, parts0);
+    cl.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+      double t[EpiDual::K];
+      fold(t, EpiDual::K, rows);
+      eb.finalize(t);  // decide_trial: accept / shrink / stop
+    }
+    cl.sync();
+  }
+}
+
+// ---------------------------------------------------------------------
+// Malitsky-Pock step (malitsky_pock_step// ---------------------------------------------------------------------
 // Malitsky-Pock step (malitsky_pock_step, solver.cpp:202-275) as four
 // kernels per trial: MP-A once per iteration (K'y, x' = clamp(x - tau(c -
 // K'y)), the first step-size candidate), MP-E (extrapolation), MP-B (K w,

@@ -333,6 +333,129 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   }
 }
 
+// A warp's unit of one plan held in registers for a whole chunk (small
+// problems: every warp of the cluster owns at most one unit per product, so
+// its descriptor, index stream, values and segment bounds never change
+// between trials and only the gathers and epilogue operands are loaded).
+struct ResidentUnit {
+  int4 d;
+  int b, e;  // this lane's segment bounds (tiles)
+  int ix[kWarpTile / 32];
+  double v[kWarpTile / 32];
+};
+
+__device__ __forceinline__ void load_resident(const SegPlan& p, const double* __restrict__ val,
+                                              int u, int lane, ResidentUnit& r) {
+  r.d = u < p.n_units ? p.units[u] : make_int4(0, 0, 0, 0);
+  r.b = r.e = 0;
+#pragma unroll
+  for (int j = 0; j < kWarpTile / 32; ++j) {
+    const int k = r.d.z + lane + 32 * j;
+    r.ix[j] = k < r.d.w ? p.idx[k] : 0;
+    r.v[j] = k < r.d.w ? val[k] : 0.0;
+  }
+  if (r.d.x >= 0 && r.d.x + lane < r.d.y) {
+    r.b = p.ptr[r.d.x + lane];
+    r.e = p.ptr[r.d.x + lane + 1];
+  }
+}
+
+// One product by a thread-block cluster from resident units (at most one per
+// warp); the CTA's partial sums go to CTA 0's `parts[rank]` (distributed
+// shared memory), folded there in rank order.
+template <int NT, class Epi>
+__device__ void cluster_product(const SegPlan& p, const ResidentUnit& r, int u, const Epi& epi,
+                                int rank, double* wbuf, double (*scratch)[kMaxAcc],
+                                double* multi_out, double* parts0) {
+  constexpr int K = Epi::K;
+  constexpr int NW = NT / 32;
+  constexpr int J = kWarpTile / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* __restrict__ vec = epi.vec();
+  TreeAcc<K> acc;
+  acc.zero();
+  const int4 d = r.d;
+  if (u < p.n_units && d.x >= 0) {
+    // tile: gathers and this lane's operands in one round
+    const int s_first = d.x + lane;
+    typename Epi::Pre pre_first{};
+    if (s_first < d.y) pre_first = epi.load(s_first);
+    double prod[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = d.z + lane + 32 * j;
+      prod[j] = k < d.w ? r.v[j] * __ldg(&vec[r.ix[j]]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = d.z + lane + 32 * j;
+      if (k < d.w) wbuf[k - d.z] = prod[j];
+    }
+    __syncwarp();
+    for (int s = s_first; s < d.y; s += 32) {
+      int b = r.b, e = r.e;
+      typename Epi::Pre pre = pre_first;
+      if (s != s_first) {
+        b = p.ptr[s];
+        e = p.ptr[s + 1];
+        pre = epi.load(s);
+      }
+      double sum = 0.0;
+      for (int k = b; k < e; ++k) sum += wbuf[k - d.z];
+      epi.apply(s, sum, pre, acc);
+    }
+    __syncwarp();
+  } else if (u < p.n_units) {
+    // part of a long segment (<= kWarpTile entries at this size)
+    const int multi = -d.x - 1;
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = d.z + lane + 32 * j;
+      if (k < d.w) sum += r.v[j] * __ldg(&vec[r.ix[j]]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
+    const int np = p.multi_parts[multi];
+    unsigned last = 0;
+    if (lane == 0) {
+      p.part_sums[u] = sum;
+      __threadfence();
+      last = atomicAdd(&p.arrivals[multi], 1u) == static_cast<unsigned>(np - 1) ? 1u : 0u;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence();
+      double total = 0.0;
+      for (int q = lane; q < np; q += 32) total += ld_cg(&p.part_sums[d.y + q]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) total += __shfl_down_sync(0xffffffffu, total, off);
+      if (lane == 0) {
+        const int seg = p.multi_seg[multi];
+        TreeAcc<K> macc;
+        macc.zero();
+        epi.apply(seg, total, epi.load(seg), macc);
+#pragma unroll
+        for (int k = 0; k < K; ++k) multi_out[multi * K + k] = macc.v[k];
+        p.arrivals[multi] = 0u;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double v = acc.v[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) scratch[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double v = 0.0;
+    for (int w = 0; w < NW; ++w) v += scratch[w][threadIdx.x];
+    parts0[rank * kMaxAcc + threadIdx.x] = v;  // remote store into CTA 0
+  }
+}
+
 // Elementwise kernel with the same deterministic reduction tail.
 // Op must provide K (>= 1), kReduce, prepare(), apply(i, acc), finalize(tot),
 // finalize_ordered(terms, n).
