@@ -594,6 +594,17 @@ struct PlanDev {
   std::vector<void*> owned;
 };
 
+// Window-blocked copy of one axis for the PDHG loop (EpiCarry / EpiCarryIn).
+struct BlockedAxis {
+  int windows = 0;                 // 0: the axis is not blocked
+  int64_t window = 0;              // gather indices per window
+  std::vector<PlanDev> plans;      // one unit plan per window
+  int* idx = nullptr;              // index stream, window-major
+  double* val = nullptr;           // working values, window-major
+  double* carry = nullptr;         // per-segment partial dots
+  std::vector<void*> owned;
+};
+
 bool g_default_ordered = false;
 std::mutex g_occ_mu;
 std::unordered_map<const void*, int> g_occ;
@@ -670,6 +681,8 @@ struct folp_gpu_ctx {
   std::vector<int64_t> shard_bounds;  // [world + 1]
   int64_t r0 = 0, r1 = 0, lnnz = 0;
   PlanDev lrows, lcols;               // local rows of the CSR; local CSC
+  BlockedAxis brows, bcols;           // window-blocked loop copies (large vectors)
+  bool blocked_checked = false;
   int* lcsc_ptr = nullptr;
   int* lcsc_row = nullptr;
   int* lcsc_pos = nullptr;            // local CSC entry -> full CSC position
@@ -822,6 +835,11 @@ struct folp_gpu_ctx {
     for (void* p : cols.owned) block_free(p);
     for (void* p : lrows.owned) block_free(p);
     for (void* p : lcols.owned) block_free(p);
+    for (BlockedAxis* ax : {&brows, &bcols}) {
+      for (PlanDev& pl : ax->plans)
+        for (void* p : pl.owned) block_free(p);
+      for (void* p : ax->owned) block_free(p);
+    }
     comm.reset();
     block_free(res_h);
     block_free(st_h);
@@ -1536,6 +1554,135 @@ void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
   CK(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------
+// Window-blocked loop copies (tree mode).  When the vector an axis gathers
+// from is larger than about half the L2 (config 4: x is 320 MB), its random
+// gathers become HBM sector reads (55 G gathers/s instead of ~270 G/s from
+// L2 -- tools/microbench/spmv_ceiling.cu on config 4).  The axis' entries
+// are then split by gather index into windows of kGatherWindow elements
+// (64 MB) and stored window-major; the product runs one phase per window,
+// so every phase gathers from an L2-resident slice (ops.cuh EpiCarry).
+constexpr int64_t kGatherWindow = int64_t(1) << 23;
+constexpr int64_t kBlockedMinVector = int64_t(12) << 20;  // elements (96 MB)
+
+__global__ void k_window_keys(const int* idx, int64_t nnz, int64_t window, int* keys) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    keys[i] = static_cast<int>(idx[i] / window);
+  }
+}
+__global__ void k_window_counts(const int* keys_sorted, const int* segid, const int* perm,
+                                int64_t nnz, int64_t segs, int* counts) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    atomicAdd(&counts[static_cast<int64_t>(keys_sorted[i]) * (segs + 1) + segid[perm[i]] + 1], 1);
+  }
+}
+__global__ void k_permute(const int* perm, const int* idx_in, const double* val_in, int64_t nnz,
+                          int* idx_out, double* val_out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = perm[i];
+    idx_out[i] = idx_in[k];
+    val_out[i] = val_in[k];
+  }
+}
+
+void build_blocked(folp_gpu_ctx* c, bool rows_axis) {
+  BlockedAxis& ax = rows_axis ? c->brows : c->bcols;
+  const int64_t S = rows_axis ? c->m : c->n;      // segments
+  const int64_t X = rows_axis ? c->n : c->m;      // gathered vector length
+  const int64_t nnz = c->nnz;
+  const char* env = std::getenv("FOLP_GATHER_WINDOW");
+  const int64_t window = env ? std::max<int64_t>(1024, std::atoll(env)) : kGatherWindow;
+  const char* thr = std::getenv("FOLP_BLOCKED_MIN");
+  const int64_t min_vec = thr ? std::atoll(thr) : kBlockedMinVector;
+  if (c->ordered || c->sharded() || X < min_vec || nnz == 0 || X <= window) return;
+  const int* ptr = rows_axis ? c->csr_ptr : c->csc_ptr;
+  const int* idx = rows_axis ? c->csr_col : c->csc_row;
+  const double* val = rows_axis ? c->csr_work : c->csc_work;
+  const int windows = static_cast<int>((X + window - 1) / window);
+  cudaStream_t st = c->stream;
+  std::vector<void*> tmp;
+  auto scratch = [&](size_t bytes) {
+    void* p = block_alloc(std::max<size_t>(bytes, 16), false);
+    tmp.push_back(p);
+    return p;
+  };
+  auto keep = [&](size_t bytes) {
+    void* p = block_alloc(std::max<size_t>(bytes, 16), false);
+    ax.owned.push_back(p);
+    return p;
+  };
+  int* segid = static_cast<int*>(scratch(nnz * sizeof(int)));
+  int* keys = static_cast<int*>(scratch(nnz * sizeof(int)));
+  int* keys_sorted = static_cast<int*>(scratch(nnz * sizeof(int)));
+  int* iota = static_cast<int*>(scratch(nnz * sizeof(int)));
+  int* perm = static_cast<int*>(scratch(nnz * sizeof(int)));
+  int* counts = static_cast<int*>(scratch(static_cast<size_t>(windows) * (S + 1) * sizeof(int)));
+  const int grid = c->simple_grid(nnz);
+  k_row_ids<<<c->simple_grid(S), kBlock, 0, st>>>(ptr, S, segid);
+  k_window_keys<<<grid, kBlock, 0, st>>>(idx, nnz, window, keys);
+  k_iota<<<grid, kBlock, 0, st>>>(iota, nnz);
+  c->launches += 3;
+  CK(cudaGetLastError());
+  int end_bit = 1;
+  while ((1 << end_bit) < windows) ++end_bit;
+  size_t sort_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys, keys_sorted, iota, perm,
+                                     static_cast<int>(nnz), 0, end_bit, st));
+  void* sort_tmp = scratch(sort_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, keys, keys_sorted, iota, perm,
+                                     static_cast<int>(nnz), 0, end_bit, st));
+  ax.idx = static_cast<int*>(keep((nnz + 8) * sizeof(int)));
+  ax.val = static_cast<double*>(keep((nnz + 8) * sizeof(double)));
+  ax.carry = static_cast<double*>(keep(S * sizeof(double)));
+  k_permute<<<grid, kBlock, 0, st>>>(perm, idx, val, nnz, ax.idx, ax.val);
+  CK(cudaMemsetAsync(counts, 0, static_cast<size_t>(windows) * (S + 1) * sizeof(int), st));
+  k_window_counts<<<grid, kBlock, 0, st>>>(keys_sorted, segid, perm, nnz, S, counts);
+  c->launches += 2;
+  CK(cudaGetLastError());
+  std::vector<int> cnt(static_cast<size_t>(windows) * (S + 1));
+  CK(cudaMemcpyAsync(cnt.data(), counts, cnt.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (void* p : tmp) block_free(p);
+  // absolute window-major segment starts, one unit plan per window
+  ax.plans.resize(windows);
+  std::vector<int64_t> ptr_abs(static_cast<size_t>(S) + 1);
+  std::vector<int> ptr32(static_cast<size_t>(S) + 1);
+  int64_t base = 0;
+  for (int w = 0; w < windows; ++w) {
+    const int* cw = cnt.data() + static_cast<size_t>(w) * (S + 1);
+    ptr_abs[0] = base;
+    for (int64_t sg = 0; sg < S; ++sg) ptr_abs[sg + 1] = ptr_abs[sg] + cw[sg + 1];
+    for (int64_t sg = 0; sg <= S; ++sg) ptr32[sg] = static_cast<int>(ptr_abs[sg]);
+    int* dptr = static_cast<int*>(keep((S + 1) * sizeof(int)));
+    CK(cudaMemcpy(dptr, ptr32.data(), (S + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    build_plan(c, ptr_abs.data(), S, nnz, dptr, ax.idx, ax.plans[w]);
+    base = ptr_abs[S];
+  }
+  ax.window = window;
+  ax.windows = windows;
+}
+
+void ensure_blocked(folp_gpu_ctx* c) {
+  if (c->blocked_checked) return;
+  c->blocked_checked = true;
+  build_blocked(c, true);
+  build_blocked(c, false);
+}
+
+// One product of the loop over a blocked axis: windows-1 carry phases, then
+// the epilogue phase.
+template <class Epi>
+void phased(folp_gpu_ctx* c, BlockedAxis& ax, const Epi& epi, int counter, int region) {
+  for (int w = 0; w + 1 < ax.windows; ++w) {
+    c->seg(ax.plans[w], ax.val, EpiCarry<Epi>{epi, w == 0 ? nullptr : ax.carry, ax.carry},
+           counter, region);
+  }
+  c->seg(ax.plans[ax.windows - 1], ax.val, EpiCarryIn<Epi>{epi, ax.carry}, counter, region);
+}
+
 // One trial slot of a step policy: adaptive / constant = {A; B},
 // Malitsky-Pock = {MP-A (first trial only); MP-E; MP-B; MP-C}.
 void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
@@ -1545,8 +1692,16 @@ void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
     c->seg(c->rows, c->csr_work, EpiMpDual{b}, 3, 1);
     c->seg(c->cols, c->csc_work, EpiMpCheck{b}, 6, 0);
   } else {
-    c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2, 0);
-    c->seg(c->rows, c->csr_work, EpiDual{b}, 3, 1);
+    if (c->bcols.windows > 0) {
+      phased(c, c->bcols, EpiPrimal{b}, 2, 0);
+    } else {
+      c->seg(c->cols, c->csc_work, EpiPrimal{b}, 2, 0);
+    }
+    if (c->brows.windows > 0) {
+      phased(c, c->brows, EpiDual{b}, 3, 1);
+    } else {
+      c->seg(c->rows, c->csr_work, EpiDual{b}, 3, 1);
+    }
   }
 }
 
@@ -1813,6 +1968,9 @@ int folp_gpu_rescale(folp_gpu_ctx* c, int64_t ruiz_iterations, int32_t pock_cham
   return guarded([&] {
     prep(c);
     c->shard_values_ready = false;
+    if (c->blocked_checked && (c->brows.windows > 0 || c->bcols.windows > 0)) {
+      throw std::invalid_argument("rescale: the loop's blocked copies are already built");
+    }
     const int64_t m = c->m, n = c->n, nnz = c->nnz;
     double* cum1 = c->d1;
     double* cum2 = c->d2;
@@ -2084,6 +2242,7 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
       throw std::invalid_argument("run_chunk: unknown step policy");
     }
     if (policy != FOLP_STEP_MALITSKY_POCK && !c->kx_valid) refresh_kx(c);
+    ensure_blocked(c);  // after rescaling: the working values are final
     if (loop->target > c->table_cap) {
       throw std::invalid_argument("run_chunk: target above the factor-table capacity");
     }

@@ -611,6 +611,56 @@ struct EpiStore {
   __device__ void finalize_ordered(const double*, int64_t) const {}
 };
 
+// ---------------------------------------------------------------------
+// Window-blocked products (tree mode, gathered vector larger than L2): the
+// entries of every segment are split by gather index into windows that fit
+// in L2 and the product runs one phase per window (config 4's
+// 320 MB x makes every random gather an HBM sector read).  Phases before the
+// last accumulate each segment's dot in `carry`; the last one runs the real
+// epilogue on carry + its own window's dot.  Sums stay deterministic (window
+// dots in window order), not sequential.
+template <class Epi>
+struct EpiCarry {
+  static constexpr int K = 1;
+  static constexpr bool kReduce = false;
+  Epi inner;            // gathered vector and running flag only
+  const double* carry;  // nullptr in the first phase
+  double* out;
+  __device__ bool prepare() { return inner.prepare(); }
+  __device__ const double* vec() const { return inner.vec(); }
+  struct Pre {
+    double c;
+  };
+  __device__ Pre load(int s) const { return Pre{carry != nullptr ? carry[s] : 0.0}; }
+  template <class Acc>
+  __device__ void apply(int s, double dot, const Pre& p, Acc&) const {
+    out[s] = p.c + dot;
+  }
+  __device__ void finalize(const double (&)[K]) const {}
+  __device__ void finalize_ordered(const double*, int64_t) const {}
+};
+
+template <class Epi>
+struct EpiCarryIn {
+  static constexpr int K = Epi::K;
+  static constexpr bool kReduce = Epi::kReduce;
+  Epi inner;
+  const double* carry;
+  __device__ bool prepare() { return inner.prepare(); }
+  __device__ const double* vec() const { return inner.vec(); }
+  struct Pre {
+    typename Epi::Pre p;
+    double c;
+  };
+  __device__ Pre load(int s) const { return Pre{inner.load(s), carry[s]}; }
+  template <class Acc>
+  __device__ void apply(int s, double dot, const Pre& p, Acc& acc) const {
+    inner.apply(s, p.c + dot, p.p, acc);
+  }
+  __device__ void finalize(const double (&t)[K]) const { inner.finalize(t); }
+  __device__ void finalize_ordered(const double* t, int64_t n) const { inner.finalize_ordered(t, n); }
+};
+
 // out = K v plus the power-iteration reductions v'out and ||out||^2
 // (estimate_spectral_norm, sparse_matrix.cpp:206-211).
 struct EpiStoreDotNorm {

@@ -156,3 +156,28 @@ def test_handcrafted_suite(eng, ref):
         assert a.termination_reason == "Optimal", lp.name
         assert abs(a.final_info["primal_objective"] - objective) <= 1e-6 * max(1, abs(objective))
         assert a.restart_iterations == b.restart_iterations, lp.name
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 0.01)])
+def test_window_blocked_products_solve(eng, ref, cfg, scale, monkeypatch):
+    """The window-blocked loop products (large gathered vectors, config 4)
+    forced onto small problems: tiny windows so every axis runs several
+    phases; same bar as the tree mode."""
+    monkeypatch.setenv("FOLP_BLOCKED_MIN", "1024")
+    monkeypatch.setenv("FOLP_GATHER_WINDOW", "1024")
+    lp = instances.generate(cfg, 1, scale)
+    p = cabi.params(kkt_pass_limit=300000)
+    a = eng.solve_lp(lp, p)
+    b = ref.solve_lp(lp, p)
+    assert a.termination_reason == b.termination_reason
+    if b.termination_reason == "Optimal":
+        assert _rel_kkt(a.final_info) <= 1e-8
+        pa, pb = a.final_info["primal_objective"], b.final_info["primal_objective"]
+        assert abs(pa - pb) <= 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
+        assert abs(a.iterations - b.iterations) <= 0.30 * b.iterations
+    assert a.step_condition_violations == 0
+    # first restart period stays within the tree-mode drift
+    p = cabi.params(record_iterate_trace=True, iteration_limit=40)
+    a = eng.solve_lp(lp, p, iterate_capacity=40)
+    b = ref.solve_lp(lp, p, iterate_capacity=40)
+    assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-9
