@@ -1560,9 +1560,9 @@ void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
 // gathers become HBM sector reads (55 G gathers/s instead of ~270 G/s from
 // L2 -- tools/microbench/spmv_ceiling.cu on config 4).  The axis' entries
 // are then split by gather index into windows of kGatherWindow elements
-// (64 MB) and stored window-major; the product runs one phase per window,
+// and stored window-major; the product runs one phase per window,
 // so every phase gathers from an L2-resident slice (ops.cuh EpiCarry).
-constexpr int64_t kGatherWindow = int64_t(1) << 23;
+constexpr int64_t kGatherWindow = int64_t(1) << 22;  // 32 MB: measured best on config 4 (2M: 13.2, 4M: 7.6, 8M: 8.1 ms per trial)
 constexpr int64_t kBlockedMinVector = int64_t(12) << 20;  // elements (96 MB)
 
 __global__ void k_window_keys(const int* idx, int64_t nnz, int64_t window, int* keys) {
