@@ -2,6 +2,7 @@
 //
 // Exceptions never cross this boundary: each entry maps the folp exception
 // type to its FOLP_E_* code and keeps the message for folp_last_error().
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -18,6 +19,7 @@
 #include "folp/termination.hpp"
 #include "folp_c.h"
 #include "session.hpp"
+#include "parallel.hpp"
 #include "sparse_access.hpp"
 
 namespace {
@@ -80,24 +82,34 @@ SparseMatrix matrix_from_csr(const folp_lp_c* in) {
       in->row_start[m] != nnz) {
     throw DimensionMismatch("folp_lp_c: inconsistent row_start");
   }
-  bool canonical = true;
-  for (int64_t r = 0; r < m && canonical; ++r) {
-    const int64_t b = in->row_start[r], e = in->row_start[r + 1];
-    if (e < b) throw DimensionMismatch("folp_lp_c: decreasing row_start");
-    for (int64_t k = b; k < e; ++k) {
-      const int64_t c = in->row_cols[k];
-      const double v = in->row_values[k];
-      if (c < 0 || c >= n || v == 0.0 || !std::isfinite(v) || (k > b && c <= in->row_cols[k - 1])) {
-        canonical = false;
-        break;
-      }
+  for (int64_t r = 0; r < m; ++r) {
+    if (in->row_start[r + 1] < in->row_start[r]) {
+      throw DimensionMismatch("folp_lp_c: decreasing row_start");
     }
   }
+  // canonical CSR (strictly increasing columns, finite nonzero values):
+  // taken as is, checked and copied on all host cores
+  std::vector<char> ok(64, 1);
+  host::parallel_for(m, [&](int64_t r0, int64_t r1, int t) {
+    for (int64_t r = r0; r < r1 && ok[t]; ++r) {
+      const int64_t b = in->row_start[r], e = in->row_start[r + 1];
+      for (int64_t k = b; k < e; ++k) {
+        const int64_t c = in->row_cols[k];
+        const double v = in->row_values[k];
+        if (c < 0 || c >= n || v == 0.0 || !std::isfinite(v) ||
+            (k > b && c <= in->row_cols[k - 1])) {
+          ok[t] = 0;
+          break;
+        }
+      }
+    }
+  });
+  const bool canonical = std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
   if (canonical) {
     std::vector<Index> start(in->row_start, in->row_start + m + 1);
-    std::vector<Index> cols(in->row_cols, in->row_cols + nnz);
-    std::vector<double> vals(in->row_values, in->row_values + nnz);
-    return SparseMatrixAccess::build(m, n, std::move(start), std::move(cols), std::move(vals));
+    return SparseMatrixAccess::build(m, n, std::move(start),
+                                     host::parallel_copy(in->row_cols, nnz),
+                                     host::parallel_copy(in->row_values, nnz));
   }
   std::vector<Triplet> t;
   t.reserve(static_cast<std::size_t>(nnz));
