@@ -14,7 +14,9 @@ session (include/folp_c.h folp_session_*).
                upload, rescaling, loop, download inside the timed region
   roofline   : fused step kernels (K'y+primal step, Kx'+dual step) --
                algorithmic bytes per trial slot 24*nnz + 68*(m+n)
-                over their CUDA-event time, vs measured HBM peak
+               (SURVEY.md 8d) over their CUDA-event time, vs measured HBM peak;
+               traffic = the DRAM bytes ncu measured for one trial
+               (profiles/r1_traffic.json, profiles/r1_step_kernels_ncu.txt)
   cpu_baseline: the compiled reference (oracle/_ref) on 1 host core
 
 ``--impl reference`` times the reference CPU solver (oracle/_ref, compiled
@@ -53,6 +55,16 @@ def bytes_per_trial(m: int, n: int, nnz: int) -> int:
     """Algorithmic HBM bytes of one trial slot (kernel A + kernel B), fp64 values,
     int32 indices/pointers, every vector touched once."""
     return 24 * nnz + 68 * (m + n)
+
+
+def measured_traffic(config: int):
+    """DRAM bytes per trial (kernel A + kernel B) from the committed ncu --set
+    full capture (profiles/r1_traffic.json), or None for other configs."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())
+        return d[f"config{config}"]["trial_dram_bytes"]
+    except Exception:
+        return None
 
 
 def measured_peak() -> tuple[float, str]:
@@ -305,7 +317,7 @@ def run_b200(args, world, rank, local):
         "iterations_timed": iters, "trial_slots_timed": slots,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": measured_traffic(args.config),
                      "kernel": "segdot_kernel<EpiPrimal> + segdot_kernel<EpiDual> (one trial)",
                      "bytes_per_launch_pair": b_trial,
                      "kernel_ms_per_trial": loop_ms / max(1, slots), "peak_source": peak_src},
