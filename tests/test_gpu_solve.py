@@ -181,3 +181,25 @@ def test_window_blocked_products_solve(eng, ref, cfg, scale, monkeypatch):
     a = eng.solve_lp(lp, p, iterate_capacity=40)
     b = ref.solve_lp(lp, p, iterate_capacity=40)
     assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-9
+
+
+@pytest.mark.parametrize("overrides", [dict(step_policy="constant"),
+                                       dict(step_policy="malitsky_pock"),
+                                       dict(restart_scheme="none"),
+                                       dict(restart_scheme="theory"),
+                                       dict(use_pock_chambolle=False, ruiz_iterations=3)])
+def test_ordered_mode_policies_bit_identical(eng, ref, overrides):
+    """Every step policy / restart scheme / scaling option of SolverParams
+    (solver.hpp:34-70), ordered reductions: the whole solve (bounded by a
+    KKT-pass limit) is bit-identical to the reference."""
+    lp = instances.generate(1, 2, 0.3)
+    p = cabi.params(kkt_pass_limit=20000, **overrides)
+    with reduction(eng, True):
+        a = eng.solve_lp(lp, p)
+    b = ref.solve_lp(lp, p)
+    assert a.termination_reason == b.termination_reason
+    assert a.iterations == b.iterations and a.restart_iterations == b.restart_iterations
+    assert a.kkt_passes == b.kkt_passes and a.step_trials == b.step_trials
+    assert a.final_info == b.final_info
+    assert np.array_equal(a.primal_solution, b.primal_solution)
+    assert np.array_equal(a.dual_solution, b.dual_solution)
