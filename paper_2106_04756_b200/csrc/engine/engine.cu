@@ -924,26 +924,6 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   c->max_giant = std::max(c->max_giant, p.n_multi);
 }
 
-// Host-side CSR -> CSC (counting sort), columns in increasing row order
-// (sparse_matrix.cpp:82-102 layout).
-void transpose_host(int64_t m, int64_t n, const int64_t* rs, const int64_t* rc, const double* rv,
-                    std::vector<int64_t>& cs, std::vector<int64_t>& cr, std::vector<double>& cv) {
-  const int64_t nnz = rs[m];
-  cs.assign(static_cast<size_t>(n) + 1, 0);
-  cr.resize(static_cast<size_t>(nnz));
-  cv.resize(static_cast<size_t>(nnz));
-  for (int64_t k = 0; k < nnz; ++k) cs[rc[k] + 1]++;
-  for (int64_t j = 0; j < n; ++j) cs[j + 1] += cs[j];
-  std::vector<int64_t> cursor(cs.begin(), cs.end() - 1);
-  for (int64_t r = 0; r < m; ++r) {
-    for (int64_t k = rs[r]; k < rs[r + 1]; ++k) {
-      const int64_t slot = cursor[rc[k]]++;
-      cr[slot] = r;
-      cv[slot] = rv[k];
-    }
-  }
-}
-
 void upload_index(folp_gpu_ctx* c, const int64_t* src, int* dst, int64_t count, int64_t* stage,
                   int64_t stage_cap) {
   for (int64_t off = 0; off < count; off += stage_cap) {
