@@ -671,6 +671,12 @@ struct folp_gpu_ctx {
   double norm_q_sq = 0.0, norm_c_sq = 0.0;
   int max_giant = 0;
   int bisect_grid = 0;
+  // evaluation period as a CUDA graph, one per CURRENT buffer parity
+  cudaGraphExec_t eval_exec[2] = {nullptr, nullptr};
+  bool eval_tried[2] = {false, false};
+  bool capturing_eval = false;    // enqueue_*: read omega / weights on device
+  double* eval_omega_h = nullptr;  // pinned: omega of the next graph launch
+  double* eval_omega_d = nullptr;
   bool small_loop = false;        // k_chunk_cluster (tree mode, <= one unit per warp)
   double* small_multi = nullptr;  // its multi-part epilogue slots
   int64_t ndg_count = 0, ndg_passes = 0, ndg_levels = 0;  // FOLP_TIMING statistics
@@ -830,6 +836,9 @@ struct folp_gpu_ctx {
     if (device >= 0) cudaSetDevice(device);
     for (auto& e : chunk_exec)
       if (e) cudaGraphExecDestroy(e);
+    for (auto& e : eval_exec)
+      if (e) cudaGraphExecDestroy(e);
+    block_free(eval_omega_h);
     if (stream) cudaStreamSynchronize(stream);  // cached blocks must be idle
     for (void* p : owned) block_free(p);
     for (void* p : rows.owned) block_free(p);
@@ -1235,7 +1244,8 @@ static_assert(kResUsed <= kResSlots, "result slots");
 // distance to LAST of restart_candidate (solver.cpp:378-386; a zero radius
 // gives a zero gap there without evaluating).
 __global__ void k_ndg_init(NdgState* st, const double* sums, const double* dist, double radius,
-                           double omega) {
+                           double omega, const double* omega_dev) {
+  if (omega_dev != nullptr) omega = *omega_dev;
   NdgState s{};
   s.omega = omega;
   s.winv = 1.0 / omega;
@@ -1388,6 +1398,8 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
   if (blockIdx.x == 0 && tid < 2 && a.active[tid]) *a.ns[tid] = st[tid];
 }
 
+__global__ void k_clear_pending(DevState* st) { st->pending = 0.0; }
+
 void enqueue_average(folp_gpu_ctx* c) {
   DevState* st = c->st_h;
   OpAverage op{};
@@ -1404,6 +1416,16 @@ void enqueue_average(folp_gpu_ctx* c) {
   op.inv = st->avg_weight > 0.0 ? 1.0 / st->avg_weight : 0.0;
   op.out_x = c->avgp_x;
   op.out_y = c->avgp_y;
+  if (c->capturing_eval) {
+    // graph: the weights are read on device at run time, then pending is
+    // cleared there (the host mirror is cleared before the launch)
+    op.st = c->st_d;
+    c->ew(c->n + c->m, op, 6);
+    k_clear_pending<<<1, 1, 0, c->stream>>>(c->st_d);
+    ++c->launches;
+    CK(cudaGetLastError());
+    return;
+  }
   c->ew(c->n + c->m, op, 6);
   st->pending = 0.0;
   c->push_state();
@@ -1475,6 +1497,7 @@ void enqueue_ndg_setup(folp_gpu_ctx* c, int which, int s, double omega) {
   double* py = c->slot_y(which);
   double* sums = c->res + kResNdg[s];
   EpiNdgPrimal ep{py, px, c->cw, c->lw, c->uw, omega, c->g[s], c->lo[s], c->hi[s], sums};
+  if (c->capturing_eval) ep.omega_dev = c->eval_omega_d;
   axis_product(c, false, true, ep, 13, 0);
   EpiNdgDual ed{};
   ed.x = px;
@@ -1487,6 +1510,7 @@ void enqueue_ndg_setup(folp_gpu_ctx* c, int which, int s, double omega) {
   ed.result = sums;
   ed.primal_terms = c->terms[0];
   ed.n = n;
+  if (c->capturing_eval) ed.omega_dev = c->eval_omega_d;
   if (which == FOLP_PT_CURRENT && c->kx_valid) {
     ed.kx_out = nullptr;
     c->ew(m, OpNdgDualCached{c->kx[c->st_h->cur], ed}, 14, 1);
@@ -1498,7 +1522,8 @@ void enqueue_ndg_setup(folp_gpu_ctx* c, int which, int s, double omega) {
 
 void enqueue_ndg_init(folp_gpu_ctx* c, int s, int dist_base, double radius, double omega) {
   const double* dist = dist_base >= 0 ? c->res + dist_base : nullptr;
-  k_ndg_init<<<1, 1, 0, c->stream>>>(c->ndg_d + s, c->res + kResNdg[s], dist, radius, omega);
+  k_ndg_init<<<1, 1, 0, c->stream>>>(c->ndg_d + s, c->res + kResNdg[s], dist, radius, omega,
+                                     c->capturing_eval ? c->eval_omega_d : nullptr);
   ++c->launches;
   CK(cudaGetLastError());
 }
@@ -1743,6 +1768,53 @@ void build_chunk_graph(folp_gpu_ctx* c, int policy) {
   }
 }
 
+// The evaluation period's device work (average, both evaluations, both
+// distances, both duality-gap setups, inits, the cooperative bisection and
+// the result read-back) captured once per CURRENT parity; omega and the
+// averaging weights are read on device at launch.  Replaces ~20 host-side
+// launches per period.  Tree mode, gaps wanted, Kx of CURRENT cached.
+void build_eval_graph(folp_gpu_ctx* c, int cur) {
+  c->eval_tried[cur] = true;
+  if (std::getenv("FOLP_EVAL_GRAPH") != nullptr && std::atoi(std::getenv("FOLP_EVAL_GRAPH")) == 0) {
+    return;
+  }
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  bool ok = true;
+  const int64_t before = c->launches;
+  c->capturing_eval = true;
+  try {
+    const int slots[2] = {FOLP_PT_CURRENT, FOLP_PT_AVERAGE};
+    CK(cudaMemcpyAsync(c->eval_omega_d, c->eval_omega_h, sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    enqueue_average(c);
+    for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s]);
+    for (int s = 0; s < 2; ++s) {
+      enqueue_distance(c, slots[s], FOLP_PT_LAST, kResDist[s]);
+      enqueue_ndg_setup(c, slots[s], s, 1.0);
+      enqueue_ndg_init(c, s, kResDist[s], 0.0, 1.0);
+    }
+    enqueue_ndg_solve(c, {true, true}, {1.0, 1.0});
+    CK(cudaMemcpyAsync(c->res_h, c->res, kResUsed * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+  } catch (...) {
+    ok = false;
+  }
+  c->capturing_eval = false;
+  c->launches = before;
+  ok = (cudaStreamEndCapture(c->stream, &graph) == cudaSuccess) && ok;
+  if (ok) ok = cudaGraphInstantiate(&c->eval_exec[cur], graph, 0) == cudaSuccess;
+  cudaGetLastError();
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok && c->eval_exec[cur]) {
+    cudaGraphExecDestroy(c->eval_exec[cur]);
+    c->eval_exec[cur] = nullptr;
+  }
+}
+
 }  // namespace
 
 // =====================================================================
@@ -1893,6 +1965,8 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     CK(cudaMemsetAsync(c->counters, 0, kCounters * sizeof(unsigned), c->stream));
     c->res = c->alloc<double>(kResSlots);
     halloc(&c->res_h, kResSlots);
+    halloc(&c->eval_omega_h, 1);
+    c->eval_omega_d = c->alloc<double>(1);
     c->st_d = c->alloc<DevState>(1);
     halloc(&c->st_h, 1);
     std::memset(c->st_h, 0, sizeof(DevState));
@@ -2154,17 +2228,29 @@ int folp_gpu_evaluation_period(folp_gpu_ctx* c, double omega, int32_t want_gaps,
       throw EngineError(FOLP_E_NONPOSITIVE_WEIGHT, "normalized_duality_gap: omega must be > 0");
     }
     const int slots[2] = {FOLP_PT_CURRENT, FOLP_PT_AVERAGE};
-    enqueue_average(c);
-    for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s]);
-    if (want_gaps) {
-      for (int s = 0; s < 2; ++s) {
-        enqueue_distance(c, slots[s], FOLP_PT_LAST, kResDist[s]);
-        enqueue_ndg_setup(c, slots[s], s, omega);
-        enqueue_ndg_init(c, s, kResDist[s], 0.0, omega);
+    const int cur = c->st_h->cur;
+    const bool graphable = !c->ordered && !c->sharded() && want_gaps && c->kx_valid &&
+                           c->norms_ready;
+    if (graphable && !c->eval_tried[cur]) build_eval_graph(c, cur);
+    if (graphable && c->eval_exec[cur] != nullptr) {
+      *c->eval_omega_h = omega;
+      c->st_h->pending = 0.0;  // the graph clears the device copy after averaging
+      CK(cudaGraphLaunch(c->eval_exec[cur], c->stream));
+      c->launches += 16;
+      CK(cudaStreamSynchronize(c->stream));
+    } else {
+      enqueue_average(c);
+      for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s]);
+      if (want_gaps) {
+        for (int s = 0; s < 2; ++s) {
+          enqueue_distance(c, slots[s], FOLP_PT_LAST, kResDist[s]);
+          enqueue_ndg_setup(c, slots[s], s, omega);
+          enqueue_ndg_init(c, s, kResDist[s], 0.0, omega);
+        }
+        enqueue_ndg_solve(c, {true, true}, {omega, omega});
       }
-      enqueue_ndg_solve(c, {true, true}, {omega, omega});
+      c->fetch_res(kResUsed);
     }
-    c->fetch_res(kResUsed);
     read_evaluate(c, kResEval[0], &out->current);
     read_evaluate(c, kResEval[1], &out->average);
     out->avg_weight = c->st_h->avg_weight;

@@ -870,7 +870,11 @@ struct EpiNdgPrimal {
   double* lo;
   double* hi;
   double* result;
-  __device__ bool prepare() { return true; }
+  const double* omega_dev = nullptr;  // graph-captured evaluation: omega read on device
+  __device__ bool prepare() {
+    if (omega_dev != nullptr) omega = *omega_dev;
+    return true;
+  }
   __device__ const double* vec() const { return y; }
   struct Pre {
     double x, c, l, u;
@@ -912,7 +916,11 @@ struct EpiNdgDual {
   double* result;    // [10]: primal half [0..5), dual half [5..10)
   const double* primal_terms;  // ordered mode: EpiNdgPrimal's terms [5 n]
   int64_t n;
-  __device__ bool prepare() { return true; }
+  const double* omega_dev = nullptr;  // graph-captured evaluation: 1/omega on device
+  __device__ bool prepare() {
+    if (omega_dev != nullptr) winv = 1.0 / *omega_dev;
+    return true;
+  }
   __device__ const double* vec() const { return x; }
   struct Pre {
     double y, q;
@@ -954,7 +962,7 @@ struct OpNdgDualCached {
   static constexpr bool kReduce = true;
   const double* kx;
   EpiNdgDual e;
-  __device__ bool prepare() { return true; }
+  __device__ bool prepare() { return e.prepare(); }
   template <class Acc>
   __device__ void apply(int64_t i, Acc& acc) const {
     e.apply(static_cast<int>(i), kx[i], e.load(static_cast<int>(i)), acc);
@@ -1185,7 +1193,15 @@ struct OpAverage {
   int copy_current;  // avg_weight <= 0: the average is the current point
   double* out_x;
   double* out_y;
-  __device__ bool prepare() { return true; }
+  const DevState* st = nullptr;  // graph-captured evaluation: weights read on device
+  __device__ bool prepare() {
+    if (st != nullptr) {
+      pending = st->pending;
+      copy_current = st->avg_weight <= 0.0 ? 1 : 0;
+      inv = st->avg_weight > 0.0 ? 1.0 / st->avg_weight : 0.0;
+    }
+    return true;
+  }
   template <class Acc>
   __device__ void apply(int64_t i, Acc&) const {
     if (i < n) {
