@@ -1609,6 +1609,11 @@ void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&om
       int occ = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ndg_bisect, kBisectThreads, 0));
       grid = std::max(1, std::min(c->sms * std::max(occ, 1), std::min(c->sms * 2, kMaxGrid / 2)));
+      // small problems: no more CTAs than 4 elements per thread -- a
+      // cooperative launch holds every CTA it spans, so concurrent solves of
+      // small programs would otherwise serialize on the whole GPU
+      const int64_t want = (c->n + c->m + int64_t(kBisectThreads) * 4 - 1) / (int64_t(kBisectThreads) * 4);
+      grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, want)));
     }
     void* args[] = {&a};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ndg_bisect), dim3(grid),
