@@ -671,6 +671,7 @@ struct folp_gpu_ctx {
   double norm_q_sq = 0.0, norm_c_sq = 0.0;
   int max_giant = 0;
   int bisect_grid = 0;
+  bool coop_ok = true;            // cooperative launches available (else OpNdgPass passes)
   // evaluation period as a CUDA graph, one per CURRENT buffer parity
   cudaGraphExec_t eval_exec[2] = {nullptr, nullptr};
   bool eval_tried[2] = {false, false};
@@ -1586,7 +1587,9 @@ void check_ndg_args(double radius, double omega) {
 }
 
 void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]) {
-  if (c->ordered) {
+  if (c->ordered || !c->coop_ok) {
+    // ordered mode, or no cooperative launch on this device/context: passes
+    // of OpNdgPass (finish_ndg continues them after the read-back)
     for (int i = 0, e = ndg_first_batch(c); i < e; ++i) {
       for (int s = 0; s < 2; ++s) {
         if (want[s]) enqueue_ndg_pass(c, s, omega[s]);
@@ -1616,8 +1619,17 @@ void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&om
       grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, want)));
     }
     void* args[] = {&a};
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ndg_bisect), dim3(grid),
-                                   dim3(kBisectThreads), args, 0, c->stream));
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ndg_bisect),
+                                                      dim3(grid), dim3(kBisectThreads), args, 0,
+                                                      c->stream);
+    if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported ||
+        e == cudaErrorNotPermitted) {
+      cudaGetLastError();
+      c->coop_ok = false;  // e.g. under MPS: fall back to pass kernels from now on
+      enqueue_ndg_solve(c, want, omega);
+      return;
+    }
+    CK(e);
     ++c->launches;
   }
   fetch_ndg(c);
@@ -1859,6 +1871,7 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     if (const char* env = std::getenv("FOLP_REDUCTION")) {
       c->ordered = std::strcmp(env, "ordered") == 0;
     }
+    if (const char* env = std::getenv("FOLP_NO_COOP")) c->coop_ok = std::atoi(env) == 0;
     set_device(c.get());
     CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

@@ -1099,7 +1099,14 @@ struct OpNdgPass {
   double omega, winv;
   NdgState* ns;
 
-  __device__ bool prepare() { return ns->done == 0; }
+  // the weights come from the bisection state (set by k_ndg_init), so a
+  // captured evaluation graph never bakes a stale omega into the pass
+  __device__ bool prepare() {
+    if (ns->done != 0) return false;
+    omega = ns->omega;
+    winv = ns->winv;
+    return true;
+  }
   template <class Acc>
   __device__ void apply(int64_t s, Acc& acc) const {
     const double gs = g[s];

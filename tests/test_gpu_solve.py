@@ -203,3 +203,17 @@ def test_ordered_mode_policies_bit_identical(eng, ref, overrides):
     assert a.final_info == b.final_info
     assert np.array_equal(a.primal_solution, b.primal_solution)
     assert np.array_equal(a.dual_solution, b.dual_solution)
+
+
+def test_tree_mode_without_cooperative_launch(eng, ref, monkeypatch):
+    """The duality-gap bisection falls back to pass kernels where cooperative
+    launches are unavailable (e.g. MPS); same results bar."""
+    monkeypatch.setenv("FOLP_NO_COOP", "1")
+    lp = instances.generate(5, 3, 0.02)
+    p = cabi.params(kkt_pass_limit=300000)
+    a = eng.solve_lp(lp, p)
+    b = ref.solve_lp(lp, p)
+    assert a.termination_reason == b.termination_reason
+    if b.termination_reason == "Optimal":
+        assert _rel_kkt(a.final_info) <= 1e-8
+        assert abs(a.iterations - b.iterations) <= 0.30 * b.iterations
