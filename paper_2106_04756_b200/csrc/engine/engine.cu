@@ -204,6 +204,7 @@ struct LoopbackGroup {
   std::condition_variable cv;
   int arrived = 0;
   int64_t generation = 0;
+  bool poisoned = false;  // a shard left early (error): the others must not wait forever
   std::vector<double*> ptrs;
   std::vector<double> scalars;
   explicit LoopbackGroup(int w) : world(w), ptrs(w, nullptr), scalars(w, 0.0) {}
@@ -215,8 +216,16 @@ struct LoopbackGroup {
       ++generation;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return generation != gen; });
+      cv.wait(lk, [&] { return generation != gen || poisoned; });
+      if (generation == gen) {
+        throw EngineError(FOLP_E_RUNTIME, "loopback shard group: another shard failed");
+      }
     }
+  }
+  void poison() {
+    std::lock_guard<std::mutex> lk(mu);
+    poisoned = true;
+    cv.notify_all();
   }
 };
 
@@ -230,6 +239,9 @@ struct LoopbackComm final : ShardComm {
     world = group->world;
   }
   ~LoopbackComm() override {
+    // a shard that leaves releases anyone still waiting (after the last
+    // collective nobody waits; before it, waiting would never end)
+    g->poison();
     if (d_ptrs) cudaFree(d_ptrs);
     if (d_sum) cudaFree(d_sum);
   }
