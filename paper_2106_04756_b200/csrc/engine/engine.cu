@@ -392,6 +392,10 @@ __global__ void k_axis_absmax(const int* __restrict__ ptr, const double* __restr
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int s = warp; s < S; s += nwarps) {
+    if (ptr[s + 1] - ptr[s] > kWarpTile) {  // long: k_long_absmax takes it
+      if (lane == 0) out[s] = 0.0;
+      continue;
+    }
     double a = 0.0;
     for (int k = ptr[s] + lane; k < ptr[s + 1]; k += 32) a = fmax(a, fabs(val[k]));
 #pragma unroll
@@ -400,35 +404,147 @@ __global__ void k_axis_absmax(const int* __restrict__ ptr, const double* __restr
   }
 }
 
+// The long segments of an axis by the units of its plan (parts, or the
+// ordered plan's single long units): warp maxima folded by an integer
+// atomicMax on the bit pattern (non-negative doubles order like their bits),
+// so the result is the exact maximum in any order.
+__device__ __forceinline__ int long_unit_segment(const SegPlan& p, const int4& d) {
+  if (d.x < 0) return p.multi_seg[-d.x - 1];
+  return d.w - d.z > kWarpTile ? d.x : -1;
+}
+
+__global__ void k_long_absmax(SegPlan p, const double* __restrict__ val, double* out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int u = warp; u < p.n_units; u += nwarps) {
+    const int4 d = p.units[u];
+    const int seg = long_unit_segment(p, d);
+    if (seg < 0) continue;
+    double a = 0.0;
+    for (int k = d.z + lane; k < d.w; k += 32) a = fmax(a, fabs(val[k]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a = fmax(a, __shfl_down_sync(0xffffffffu, a, off));
+    if (lane == 0) {
+      atomicMax(reinterpret_cast<unsigned long long*>(out + seg),
+                static_cast<unsigned long long>(__double_as_longlong(a)));
+    }
+  }
+}
+
 // Sequential per-segment p-norm in increasing index order: bit-identical to
 // the reference's loop for p = 0, 1, 2 (pow for other p is CUDA's).
+constexpr int kLongSeq = 1024;  // segments above this: k_axis_pnorm_long
+
+template <int MODE>
+__device__ __forceinline__ double pnorm_term(double v, double p) {
+  const double a = fabs(v);
+  if constexpr (MODE == 0) {
+    return 1.0;
+  } else if constexpr (MODE == 1) {
+    return a;
+  } else if constexpr (MODE == 2) {
+    return a * a;
+  } else {
+    return pow(a, p);
+  }
+}
+template <int MODE>
+__device__ __forceinline__ double pnorm_finish(double acc, double p) {
+  if constexpr (MODE == 2) {
+    return sqrt(acc);
+  } else if constexpr (MODE == 3) {
+    return (isfinite(p) && p > 1.0) ? pow(acc, 1.0 / p) : acc;
+  } else {
+    return acc;
+  }
+}
+
+// A long segment's norm, still one sequential sum in index order (the
+// reference's rounding), but its terms are staged into shared memory by the
+// whole warp (coalesced, double-buffered) so the single summing lane only
+// waits on its add chain, not on a global load per term.
+template <int MODE>
+__global__ void __launch_bounds__(32) k_axis_pnorm_long(const int* __restrict__ ptr,
+                                                        const double* __restrict__ val,
+                                                        const int* __restrict__ segs, double p,
+                                                        double* __restrict__ out) {
+  constexpr int kChunk = 1024;
+  __shared__ double buf[2][kChunk];
+  const int s = segs[blockIdx.x];
+  const int lane = threadIdx.x;
+  const int b = ptr[s], e = ptr[s + 1];
+  double acc = 0.0;
+  int slot = 0;
+  // a chunk's 32 loads per lane are issued back to back, then stored
+  auto stage = [&](int c0, double* dst) {
+    double v[kChunk / 32];
+#pragma unroll
+    for (int q = 0; q < kChunk / 32; ++q) {
+      const int k = c0 + lane + 32 * q;
+      v[q] = k < e ? val[k] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kChunk / 32; ++q) {
+      const int k = c0 + lane + 32 * q;
+      if (k < e) dst[lane + 32 * q] = pnorm_term<MODE>(v[q], p);
+    }
+  };
+  stage(b, buf[0]);
+  __syncwarp();
+  for (int c0 = b; c0 < e; c0 += kChunk, slot ^= 1) {
+    const int c1 = min(c0 + kChunk, e);
+    // stage the next chunk while lane 0 sums this one
+    if (c1 < e) stage(c1, buf[slot ^ 1]);
+    if (lane == 0) {
+      const double* t = buf[slot];
+      const int len = c1 - c0;
+      int j = 0;
+      for (; j + 16 <= len; j += 16) {  // loads hoisted ahead of the add chain
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = t[j + q];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc += v[q];
+      }
+      for (; j < len; ++j) acc += t[j];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) out[s] = pnorm_finish<MODE>(acc, p);
+}
+
+template <int MODE>  // 0: count, 1: sum |a|, 2: sqrt(sum a^2), 3: (sum |a|^p)^(1/p)
 __global__ void k_axis_pnorm_seq(const int* __restrict__ ptr, const double* __restrict__ val,
                                  int S, double p, double* __restrict__ out) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (int k = ptr[s]; k < ptr[s + 1]; ++k) {
-      const double a = fabs(val[k]);
-      if (p == 0.0) {
-        acc += 1.0;
-      } else if (p == 1.0) {
-        acc += a;
-      } else if (p == 2.0) {
-        acc += a * a;
-      } else {
-        acc += pow(a, p);
+    const int b = ptr[s], e = ptr[s + 1];
+    if (e - b > kLongSeq) continue;  // k_axis_pnorm_long
+    if constexpr (MODE == 0) {
+      for (int k = b; k < e; ++k) acc += 1.0;
+    } else {
+#pragma unroll 8
+      for (int k = b; k < e; ++k) {
+        const double a = fabs(val[k]);
+        if constexpr (MODE == 1) {
+          acc += a;
+        } else if constexpr (MODE == 2) {
+          acc += a * a;
+        } else {
+          acc += pow(a, p);
+        }
       }
     }
-    if (p == 2.0) {
+    if constexpr (MODE == 2) {
       acc = sqrt(acc);
-    } else if (isfinite(p) && p > 1.0 && p != 2.0) {
-      acc = pow(acc, 1.0 / p);
+    } else if constexpr (MODE == 3) {
+      if (isfinite(p) && p > 1.0) acc = pow(acc, 1.0 / p);
     }
     out[s] = acc;
   }
 }
 
-// reciprocal_sqrt (scaling.cpp:23-28) fused with the cumulative product
-// (scaling.cpp:58-65): d = v > 0 ? 1/sqrt(v) : 1; cum *= d.
 __global__ void k_recip_sqrt_cum(double* __restrict__ v, double* __restrict__ cum, int S) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
     const double x = v[s];
@@ -447,8 +563,24 @@ __global__ void k_scale_values(const int* __restrict__ ptr, const int* __restric
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int s = warp; s < S; s += nwarps) {
+    if (ptr[s + 1] - ptr[s] > kWarpTile) continue;  // long: k_long_scale
     const double ds = dseg[s];
     for (int k = ptr[s] + lane; k < ptr[s + 1]; k += 32) dst[k] = src[k] * (ds * didx[idx[k]]);
+  }
+}
+
+__global__ void k_long_scale(SegPlan p, const int* __restrict__ idx, const double* src,
+                             double* dst, const double* __restrict__ dseg,
+                             const double* __restrict__ didx) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int u = warp; u < p.n_units; u += nwarps) {
+    const int4 d = p.units[u];
+    const int seg = long_unit_segment(p, d);
+    if (seg < 0) continue;
+    const double ds = dseg[seg];
+    for (int k = d.z + lane; k < d.w; k += 32) dst[k] = src[k] * (ds * didx[idx[k]]);
   }
 }
 
@@ -604,6 +736,8 @@ struct OpNormSq {
 struct PlanDev {
   SegPlan sp{};
   std::vector<void*> owned;
+  const int* long_segs = nullptr;  // segments above kLongSeq entries (sequential norms)
+  int n_long = 0;
 };
 
 // Window-blocked copy of one axis for the PDHG loop (EpiCarry / EpiCarryIn).
@@ -929,6 +1063,14 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
     if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
     return d;
   };
+  {
+    std::vector<int> ls;
+    for (int64_t sg = s_begin; sg < S; ++sg) {
+      if (ptr[sg + 1] - ptr[sg] > kLongSeq) ls.push_back(static_cast<int>(sg));
+    }
+    out.n_long = static_cast<int>(ls.size());
+    if (!ls.empty()) out.long_segs = up(ls);
+  }
   SegPlan& p = out.sp;
   p.ptr = d_ptr;
   p.idx = d_idx;
@@ -981,10 +1123,14 @@ void copy_d2d(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
 // column keeps each column in increasing row order, i.e. exactly the
 // reference's layout.  Fills csc_ptr / csc_row / csc_orig and returns the
 // column starts on the host (for the unit plan).
-__global__ void k_row_ids(const int* ptr, int64_t m, int* rowid) {
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < m;
+// Segment id of every entry: a mark at each segment start (empty segments
+// stack their marks), then an inclusive scan -- no thread walks a whole
+// segment (config 3's dense row has 2M entries).
+__global__ void k_segment_marks(const int* ptr, int64_t S, int64_t nnz, int* marks) {
+  for (int64_t r = 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < S;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    for (int k = ptr[r]; k < ptr[r + 1]; ++k) rowid[k] = static_cast<int>(r);
+    const int k = ptr[r];
+    if (k < nnz) atomicAdd(&marks[k], 1);  // integer counts: order-free
   }
 }
 __global__ void k_iota(int* v, int64_t count) {
@@ -993,6 +1139,9 @@ __global__ void k_iota(int* v, int64_t count) {
     v[i] = static_cast<int>(i);
   }
 }
+void segment_ids(folp_gpu_ctx* c, const int* ptr, int64_t S, int64_t nnz, int* out,
+                 std::vector<void*>& tmp);
+
 __global__ void k_col_counts(const int* col, int64_t nnz, int* counts) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1007,6 +1156,22 @@ __global__ void k_csc_fill(const int* order, const int* rowid, const double* val
     csc_row[i] = rowid[k];
     csc_val[i] = vals[k];
   }
+}
+
+void segment_ids(folp_gpu_ctx* c, const int* ptr, int64_t S, int64_t nnz, int* out,
+                 std::vector<void*>& tmp) {
+  cudaStream_t st = c->stream;
+  int* marks = static_cast<int*>(block_alloc(std::max<size_t>(nnz * sizeof(int), 16), false));
+  tmp.push_back(marks);
+  CK(cudaMemsetAsync(marks, 0, nnz * sizeof(int), st));
+  k_segment_marks<<<c->simple_grid(S), kBlock, 0, st>>>(ptr, S, nnz, marks);
+  ++c->launches;
+  CK(cudaGetLastError());
+  size_t bytes = 0;
+  CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, marks, out, static_cast<int>(nnz), st));
+  void* t = block_alloc(std::max<size_t>(bytes, 16), false);
+  tmp.push_back(t);
+  CK(cub::DeviceScan::InclusiveSum(t, bytes, marks, out, static_cast<int>(nnz), st));
 }
 
 void device_transpose(folp_gpu_ctx* c, std::vector<int64_t>& col_start) {
@@ -1025,11 +1190,11 @@ void device_transpose(folp_gpu_ctx* c, std::vector<int64_t>& col_start) {
     int* order = static_cast<int*>(scratch(nnz * sizeof(int)));
     int* counts = static_cast<int*>(scratch((n + 1) * sizeof(int)));
     const int grid = c->simple_grid(std::max<int64_t>(m, nnz));
-    k_row_ids<<<c->simple_grid(m), kBlock, 0, s>>>(c->csr_ptr, m, rowid);
+    segment_ids(c, c->csr_ptr, m, nnz, rowid, tmp);
     k_iota<<<grid, kBlock, 0, s>>>(order_in, nnz);
     CK(cudaMemsetAsync(counts, 0, (n + 1) * sizeof(int), s));
     k_col_counts<<<grid, kBlock, 0, s>>>(c->csr_col, nnz, counts);
-    c->launches += 3;
+    c->launches += 2;
     CK(cudaGetLastError());
     int end_bit = 1;
     while (end_bit < 31 && (int64_t(1) << end_bit) < n) ++end_bit;
@@ -1134,10 +1299,10 @@ void build_blocked(folp_gpu_ctx* c, bool rows_axis) {
   int* perm = static_cast<int*>(scratch(nnz * sizeof(int)));
   int* counts = static_cast<int*>(scratch(static_cast<size_t>(windows) * (S + 1) * sizeof(int)));
   const int grid = c->simple_grid(nnz);
-  k_row_ids<<<c->simple_grid(S), kBlock, 0, st>>>(ptr, S, segid);
+  segment_ids(c, ptr, S, nnz, segid, tmp);
   k_window_keys<<<grid, kBlock, 0, st>>>(idx, nnz, window, keys);
   k_iota<<<grid, kBlock, 0, st>>>(iota, nnz);
-  c->launches += 3;
+  c->launches += 2;
   CK(cudaGetLastError());
   int end_bit = 1;
   while ((1 << end_bit) < windows) ++end_bit;
@@ -1214,6 +1379,64 @@ void axis_product(folp_gpu_ctx* c, bool rows_axis, bool working, const Epi& epi,
   } else {
     c->seg(c->cols, working ? c->csc_work : c->csc_orig, epi, counter, region);
   }
+}
+
+// Per-axis scaling primitives (SparseMatrix::axis_norms, ::scaled): short
+// segments one warp each, long ones by their plan's units (no warp walks
+// config 3's 2M-entry row alone).
+void axis_absmax(folp_gpu_ctx* c, bool rows_axis, const double* val, double* out) {
+  const int S = static_cast<int>(rows_axis ? c->m : c->n);
+  const PlanDev& plan = rows_axis ? c->rows : c->cols;
+  k_axis_absmax<<<c->simple_grid(static_cast<int64_t>(S) * 32), kBlock, 0, c->stream>>>(
+      rows_axis ? c->csr_ptr : c->csc_ptr, val, S, out);
+  k_long_absmax<<<c->simple_grid(static_cast<int64_t>(plan.sp.n_units) * 32), kBlock, 0,
+                  c->stream>>>(plan.sp, val, out);
+  c->launches += 2;
+  CK(cudaGetLastError());
+}
+
+void axis_scale(folp_gpu_ctx* c, bool rows_axis, const double* src, double* dst,
+                const double* dseg, const double* didx) {
+  const int S = static_cast<int>(rows_axis ? c->m : c->n);
+  const PlanDev& plan = rows_axis ? c->rows : c->cols;
+  const int* idx = rows_axis ? c->csr_col : c->csc_row;
+  k_scale_values<<<c->simple_grid(static_cast<int64_t>(S) * 32), kBlock, 0, c->stream>>>(
+      rows_axis ? c->csr_ptr : c->csc_ptr, idx, src, dst, S, dseg, didx);
+  k_long_scale<<<c->simple_grid(static_cast<int64_t>(plan.sp.n_units) * 32), kBlock, 0,
+                 c->stream>>>(plan.sp, idx, src, dst, dseg, didx);
+  c->launches += 2;
+  CK(cudaGetLastError());
+}
+
+// p-norms in each segment's index order (bit-identical to the reference for
+// p = 0, 1, 2); p = inf goes to axis_absmax.
+void axis_pnorm(folp_gpu_ctx* c, bool rows_axis, const double* val, double p, double* out) {
+  if (std::isinf(p)) {
+    axis_absmax(c, rows_axis, val, out);
+    return;
+  }
+  const int S = static_cast<int>(rows_axis ? c->m : c->n);
+  const int* ptr = rows_axis ? c->csr_ptr : c->csc_ptr;
+  const int grid = c->simple_grid(S);
+  const PlanDev& plan = rows_axis ? c->rows : c->cols;
+  auto run = [&](auto mode) {
+    constexpr int M = decltype(mode)::value;
+    k_axis_pnorm_seq<M><<<grid, kBlock, 0, c->stream>>>(ptr, val, S, p, out);
+    if (plan.n_long > 0) {
+      k_axis_pnorm_long<M><<<plan.n_long, 32, 0, c->stream>>>(ptr, val, plan.long_segs, p, out);
+    }
+  };
+  if (p == 0.0) {
+    run(std::integral_constant<int, 0>{});
+  } else if (p == 1.0) {
+    run(std::integral_constant<int, 1>{});
+  } else if (p == 2.0) {
+    run(std::integral_constant<int, 2>{});
+  } else {
+    run(std::integral_constant<int, 3>{});
+  }
+  c->launches += plan.n_long > 0 ? 2 : 1;
+  CK(cudaGetLastError());
 }
 
 // K x of the CURRENT point into kx[cur] (after a start or a restart).
@@ -2082,45 +2305,30 @@ int folp_gpu_rescale(folp_gpu_ctx* c, int64_t ruiz_iterations, int32_t pock_cham
       k_recip_sqrt_cum<<<c->simple_grid(m), kBlock, 0, c->stream>>>(step1, cum1, (int)m);
       k_recip_sqrt_cum<<<c->simple_grid(n), kBlock, 0, c->stream>>>(step2, cum2, (int)n);
       // working = working.scaled(step1, step2)   (scaling.cpp:57)
-      k_scale_values<<<c->simple_grid(m * 32), kBlock, 0, c->stream>>>(
-          c->csr_ptr, c->csr_col, c->csr_work, c->csr_work, (int)m, step1, step2);
-      k_scale_values<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(
-          c->csc_ptr, c->csc_row, c->csc_work, c->csc_work, (int)n, step2, step1);
-      c->launches += 4;
+      axis_scale(c, true, c->csr_work, c->csr_work, step1, step2);
+      axis_scale(c, false, c->csc_work, c->csc_work, step2, step1);
+      c->launches += 2;
       CK(cudaGetLastError());
     };
     for (int64_t it = 0; it < ruiz_iterations; ++it) {
       // ruiz_step (scaling.cpp:32-36): inf-norms of the running matrix.
-      k_axis_absmax<<<c->simple_grid(m * 32), kBlock, 0, c->stream>>>(c->csr_ptr, c->csr_work,
-                                                                     (int)m, step1);
-      k_axis_absmax<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(c->csc_ptr, c->csc_work,
-                                                                     (int)n, step2);
-      c->launches += 2;
+      axis_absmax(c, true, c->csr_work, step1);
+      axis_absmax(c, false, c->csc_work, step2);
       apply_step();
     }
     if (pock_chambolle) {
       // pock_chambolle_step (scaling.cpp:38-46)
       const double row_p = 2.0 - alpha;
-      k_axis_pnorm_seq<<<c->simple_grid(m), kBlock, 0, c->stream>>>(c->csr_ptr, c->csr_work,
-                                                                   (int)m, row_p, step1);
-      if (std::isinf(alpha)) {
-        k_axis_absmax<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(c->csc_ptr, c->csc_work,
-                                                                       (int)n, step2);
-      } else {
-        k_axis_pnorm_seq<<<c->simple_grid(n), kBlock, 0, c->stream>>>(c->csc_ptr, c->csc_work,
-                                                                     (int)n, alpha, step2);
-      }
-      c->launches += 2;
+      axis_pnorm(c, true, c->csr_work, row_p, step1);
+      axis_pnorm(c, false, c->csc_work, alpha, step2);
       apply_step();
     }
     // K~ = K .scaled(D1, D2) from the original values in one shot (scaling.cpp:75-76)
-    k_scale_values<<<c->simple_grid(m * 32), kBlock, 0, c->stream>>>(
-        c->csr_ptr, c->csr_col, c->csr_orig, c->csr_work, (int)m, cum1, cum2);
-    k_scale_values<<<c->simple_grid(n * 32), kBlock, 0, c->stream>>>(
-        c->csc_ptr, c->csc_row, c->csc_orig, c->csc_work, (int)n, cum2, cum1);
+    axis_scale(c, true, c->csr_orig, c->csr_work, cum1, cum2);
+    axis_scale(c, false, c->csc_orig, c->csc_work, cum2, cum1);
     k_scale_vectors<<<c->simple_grid(n + m), kBlock, 0, c->stream>>>(
         n, m, c->c0, c->l0, c->u0, c->q0, cum1, cum2, c->cw, c->lw, c->uw, c->qw);
-    c->launches += 3;
+    c->launches += 1;
     CK(cudaGetLastError());
     download(c, row_scale, cum1, m);
     download(c, col_scale, cum2, n);
@@ -2547,14 +2755,8 @@ int folp_gpu_axis_norms(folp_gpu_ctx* c, int32_t axis, double p, int32_t working
     const double* val = rows ? (working ? c->csr_work : c->csr_orig)
                              : (working ? c->csc_work : c->csc_orig);
     double* dst = rows ? c->yr : c->xr;
-    if (std::isinf(p)) {
-      k_axis_absmax<<<c->simple_grid(static_cast<int64_t>(S) * 32), kBlock, 0, c->stream>>>(
-          ptr, val, S, dst);
-    } else {
-      k_axis_pnorm_seq<<<c->simple_grid(S), kBlock, 0, c->stream>>>(ptr, val, S, p, dst);
-    }
-    ++c->launches;
-    CK(cudaGetLastError());
+    (void)ptr;
+    axis_pnorm(c, rows, val, p, dst);
     download(c, out, dst, S);
     CK(cudaStreamSynchronize(c->stream));
   });
