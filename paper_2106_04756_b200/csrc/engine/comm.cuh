@@ -1,0 +1,226 @@
+// comm.cuh -- collectives of the row-sharded loop (NCCL, in-process loopback).
+// Fragment of engine.cu: included inside its anonymous namespace, after
+// the pieces it uses (one translation unit; see engine.cu for the order).
+#pragma once
+
+// ---------------------------------------------------------------------
+// Collectives of the row-sharded loop.  One process (or, for
+// the loopback group, one host thread) per shard; every shard calls the same
+// collectives in the same order because every shard takes the same
+// decisions.
+struct ShardComm {
+  int rank = 0, world = 1;
+  virtual ~ShardComm() = default;
+  // in-place sum over the shards, identical result on every shard
+  virtual void allreduce_sum(double* buf, int64_t count, cudaStream_t s) = 0;
+  // in-place: every shard receives root's buf[0..count)
+  virtual void broadcast(double* buf, int64_t count, int root, cudaStream_t s) = 0;
+  // host scalar max over the shards (wall-clock limit checks)
+  virtual double max_scalar(double v, cudaStream_t s) = 0;
+  // in-place: rows [bounds[r], bounds[r+1]) of buf from shard r, for every r
+  virtual void gather_rows(double* buf, const std::vector<int64_t>& bounds, cudaStream_t s) = 0;
+};
+
+// NCCL, loaded at run time: the single-GPU path has no NCCL dependency, and
+// a process that already loaded torch's libnccl.so.2 shares it.
+struct NcclApi {
+  void* handle = nullptr;
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclBroadcast) bcast = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return;
+    api.handle = h;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    api.bcast = reinterpret_cast<decltype(api.bcast)>(dlsym(h, "ncclBroadcast"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  });
+  if (api.handle == nullptr || api.comm_init_rank == nullptr || api.all_reduce == nullptr ||
+      api.bcast == nullptr || api.get_unique_id == nullptr) {
+    throw EngineError(FOLP_E_RUNTIME, "NCCL (libnccl.so.2) is not loadable");
+  }
+  return api;
+}
+
+#define NCK(call)                                                                  \
+  do {                                                                             \
+    ncclResult_t r_ = (call);                                                      \
+    if (r_ != ncclSuccess) {                                                       \
+      throw EngineError(FOLP_E_RUNTIME, std::string(#call) + ": " +                \
+                                            nccl_api().error_string(r_));          \
+    }                                                                              \
+  } while (0)
+
+struct NcclComm final : ShardComm {
+  ncclComm_t comm = nullptr;
+  double* scratch = nullptr;
+  NcclComm(const unsigned char* id_bytes, int r, int w) {
+    rank = r;
+    world = w;
+    const NcclApi& api = nccl_api();
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, sizeof(id));
+    NCK(api.comm_init_rank(&comm, w, id, r));
+    CK(cudaMalloc(&scratch, sizeof(double)));
+  }
+  ~NcclComm() override {
+    if (scratch) cudaFree(scratch);
+    if (comm) nccl_api().comm_destroy(comm);
+  }
+  void allreduce_sum(double* buf, int64_t count, cudaStream_t s) override {
+    if (count > 0) NCK(nccl_api().all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm, s));
+  }
+  void broadcast(double* buf, int64_t count, int root, cudaStream_t s) override {
+    if (count > 0) NCK(nccl_api().bcast(buf, buf, count, ncclFloat64, root, comm, s));
+  }
+  void gather_rows(double* buf, const std::vector<int64_t>& bounds, cudaStream_t s) override {
+    const NcclApi& api = nccl_api();
+    NCK(api.group_start());
+    for (int r = 0; r < world; ++r) {
+      const int64_t count = bounds[r + 1] - bounds[r];
+      if (count > 0) {
+        NCK(api.bcast(buf + bounds[r], buf + bounds[r], count, ncclFloat64, r, comm, s));
+      }
+    }
+    NCK(api.group_end());
+  }
+  double max_scalar(double v, cudaStream_t s) override {
+    CK(cudaMemcpyAsync(scratch, &v, sizeof(double), cudaMemcpyHostToDevice, s));
+    NCK(nccl_api().all_reduce(scratch, scratch, 1, ncclFloat64, ncclMax, comm, s));
+    CK(cudaMemcpyAsync(&v, scratch, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+  }
+};
+
+// In-process group: W shards driven by W host threads of one process, all
+// on one device (parity tests of the sharded schedule on a single GPU).
+// Every collective synchronizes the caller's stream first and exchanges
+// through plain device copies, so no kernel ever waits on another shard.
+__global__ void k_sum_shards(double* const* parts, int world, int64_t count, double* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = parts[0][i];
+    for (int r = 1; r < world; ++r) s += parts[r][i];
+    out[i] = s;
+  }
+}
+
+struct LoopbackGroup {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t generation = 0;
+  bool poisoned = false;  // a shard left early (error): the others must not wait forever
+  std::vector<double*> ptrs;
+  std::vector<double> scalars;
+  explicit LoopbackGroup(int w) : world(w), ptrs(w, nullptr), scalars(w, 0.0) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen || poisoned; });
+      if (generation == gen) {
+        throw EngineError(FOLP_E_RUNTIME, "loopback shard group: another shard failed");
+      }
+    }
+  }
+  void poison() {
+    std::lock_guard<std::mutex> lk(mu);
+    poisoned = true;
+    cv.notify_all();
+  }
+};
+
+struct LoopbackComm final : ShardComm {
+  LoopbackGroup* g;
+  double** d_ptrs = nullptr;
+  double* d_sum = nullptr;
+  int64_t sum_cap = 0;
+  LoopbackComm(LoopbackGroup* group, int r) : g(group) {
+    rank = r;
+    world = group->world;
+  }
+  ~LoopbackComm() override {
+    // a shard that leaves releases anyone still waiting (after the last
+    // collective nobody waits; before it, waiting would never end)
+    g->poison();
+    if (d_ptrs) cudaFree(d_ptrs);
+    if (d_sum) cudaFree(d_sum);
+  }
+  void allreduce_sum(double* buf, int64_t count, cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));
+    g->ptrs[rank] = buf;
+    g->barrier();
+    if (rank == 0 && count > 0) {
+      if (d_ptrs == nullptr) CK(cudaMalloc(&d_ptrs, world * sizeof(double*)));
+      if (sum_cap < count) {
+        if (d_sum) cudaFree(d_sum);
+        CK(cudaMalloc(&d_sum, count * sizeof(double)));
+        sum_cap = count;
+      }
+      CK(cudaMemcpyAsync(d_ptrs, g->ptrs.data(), world * sizeof(double*), cudaMemcpyHostToDevice, s));
+      k_sum_shards<<<static_cast<int>(std::min<int64_t>((count + 255) / 256, 1184)), 256, 0, s>>>(
+          d_ptrs, world, count, d_sum);
+      CK(cudaGetLastError());
+      for (int r = 0; r < world; ++r) {
+        CK(cudaMemcpyAsync(g->ptrs[r], d_sum, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      }
+      CK(cudaStreamSynchronize(s));
+    }
+    g->barrier();
+  }
+  void broadcast(double* buf, int64_t count, int root, cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));
+    g->ptrs[rank] = buf;
+    g->barrier();
+    if (rank != root && count > 0) {
+      CK(cudaMemcpyAsync(buf, g->ptrs[root], count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    g->barrier();
+  }
+  void gather_rows(double* buf, const std::vector<int64_t>& bounds, cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));
+    g->ptrs[rank] = buf;
+    g->barrier();
+    for (int r = 0; r < world; ++r) {
+      const int64_t count = bounds[r + 1] - bounds[r];
+      if (r != rank && count > 0) {
+        CK(cudaMemcpyAsync(buf + bounds[r], g->ptrs[r] + bounds[r], count * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    CK(cudaStreamSynchronize(s));
+    g->barrier();
+  }
+  double max_scalar(double v, cudaStream_t) override {
+    g->scalars[rank] = v;
+    g->barrier();
+    double m = g->scalars[0];
+    for (int r = 1; r < world; ++r) m = std::max(m, g->scalars[r]);
+    g->barrier();
+    return m;
+  }
+};

@@ -1,0 +1,430 @@
+// evaluation.cuh -- the evaluation period: convergence info, distances, duality gaps, restarts.
+// Fragment of engine.cu: included inside its anonymous namespace, after
+// the pieces it uses (one translation unit; see engine.cu for the order).
+#pragma once
+
+// ---------------------------------------------------------------------
+// Evaluation period (solver.cpp:751-816) as one asynchronous sequence.
+// Result-slot blocks of the period's reductions:
+constexpr int kResEval[2] = {32, 44};  // [0] c'x [1] q'y [2] non-finite [3] primal^2
+                                        // [4] dual^2 [5] bound terms [6] inf product
+                                        // [10] dual objective (ordered)
+constexpr int kResNorms = 56;           // ||q||^2, ||c||^2
+constexpr int kResDist[2] = {60, 62};   // sum dx^2, sum dy^2 to LAST
+constexpr int kResNdg[2] = {64, 74};    // duality-gap setup sums (10 each)
+constexpr int kResUsed = 84;
+static_assert(kResUsed <= kResSlots, "result slots");
+
+// Bracket of one normalized_duality_gap evaluation from its setup sums
+// (solver.cpp:318-355).  The radius is either given or the weighted
+// distance to LAST of restart_candidate (solver.cpp:378-386; a zero radius
+// gives a zero gap there without evaluating).
+__global__ void k_ndg_init(NdgState* st, const double* sums, const double* dist, double radius,
+                           double omega, const double* omega_dev) {
+  if (omega_dev != nullptr) omega = *omega_dev;
+  NdgState s{};
+  s.omega = omega;
+  s.winv = 1.0 / omega;
+  const double r = dist != nullptr ? sqrt(omega * dist[0] + dist[1] / omega) : radius;
+  s.radius = r;
+  if (r == 0.0 || sums[0] + sums[5] == 0.0) {  // solver.cpp:324
+    s.done = 1;
+    s.result = 0.0;
+    *st = s;
+    return;
+  }
+  if (sums[2] + sums[7] == 0.0) {  // bounded corner, solver.cpp:339-341
+    const double norm_sq = sums[3] + sums[8];
+    if (sqrt(norm_sq) <= r * (1.0 + 1e-12)) {
+      s.done = 1;
+      s.result = (sums[4] + sums[9]) / r;
+      *st = s;
+      return;
+    }
+  }
+  s.nu_lo = 0.0;
+  s.nu_hi = sqrt(sums[1] + sums[6]) / r;
+  ndg_candidates(s.nu_lo, s.nu_hi, s.nu);
+  ndg_reciprocals(&s);
+  *st = s;
+}
+
+// Tree-mode bisection of up to two duality gaps in ONE cooperative launch
+// (solver.cpp:356-368).  Every pass evaluates the 7 midpoints of the next
+// 3 levels per scratch set; the block partials are published, the grid
+// synchronizes once, and every block sums the partials in the same order
+// and replays the same decisions, so the bisection state never leaves
+// shared memory until the end.  Replaces up to ~70 launches per period.
+constexpr int kBisectThreads = 512;
+// ||d||_w^2 and g'd per midpoint, then the bracket sums of the analytic
+// finish: elements with a breakpoint inside, Q, H, S (ndg_finish_analytic)
+constexpr int kBisectVals = 2 * kNuCands + 4;
+
+struct BisectArgs {
+  int64_t n, total;
+  const double* g[2];
+  const double* lo[2];
+  const double* hi[2];
+  NdgState* ns[2];
+  int active[2];
+  double* partials;  // [2 parity][2 sets][kBisectVals][grid]
+};
+
+__global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ NdgState st[2];
+  __shared__ double wsum[kBisectThreads / 32][2][kBisectVals];
+  __shared__ double tot[2][kBisectVals];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = gridDim.x;
+  if (tid < 2) {
+    st[tid] = *a.ns[tid];
+    if (!a.active[tid]) st[tid].done = 1;
+  }
+  __syncthreads();
+  for (int parity = 0;; parity ^= 1) {
+    const bool run[2] = {st[0].done == 0, st[1].done == 0};
+    if (!run[0] && !run[1]) break;  // same state in every block
+    double acc[2][kBisectVals];
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int k = 0; k < kBisectVals; ++k) acc[s][k] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!run[s]) continue;
+      const double* g = a.g[s];
+      const double* lo = a.lo[s];
+      const double* hi = a.hi[s];
+      const double omega = st[s].omega, winv = st[s].winv;
+      for (int64_t i = static_cast<int64_t>(blockIdx.x) * kBisectThreads + tid; i < a.total;
+           i += static_cast<int64_t>(nb) * kBisectThreads) {
+        const double gs = g[i];
+        const bool primal = i < a.n;
+        const double w = primal ? omega : winv;
+        const double los = lo[i];
+        const double his = primal ? hi[i] : INFINITY;
+        const double* rcp = primal ? st[s].rcp_primal : st[s].rcp_dual;
+#pragma unroll
+        for (int p = 0; p < kNuCands; ++p) {
+          const double d = ref_min(ref_max(gs * rcp[p], los), his);
+          acc[s][2 * p] += w * d * d;
+          acc[s][2 * p + 1] += gs * d;
+        }
+        if (gs != 0.0) {
+          const int side = primal ? 0 : 1;
+          const double ulo = gs * st[s].rcp_lo[side];  // |u| largest at nu_lo
+          const double uhi = gs * st[s].rcp_hi[side];
+          const bool clamped_lo = ulo < los || ulo > his;
+          const bool clamped_hi = uhi < los || uhi > his;
+          if (clamped_lo && !clamped_hi) acc[s][2 * kNuCands] += 1.0;
+          if (clamped_hi) {  // clamped over the whole bracket
+            const double cv = uhi > his ? his : los;
+            acc[s][2 * kNuCands + 1] += w * cv * cv;
+            acc[s][2 * kNuCands + 2] += gs * cv;
+          }
+          if (!clamped_lo) acc[s][2 * kNuCands + 3] += gs * gs * (primal ? winv : omega);
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int k = 0; k < kBisectVals; ++k) {
+        double v = acc[s][k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) wsum[warp][s][k] = v;
+      }
+    __syncthreads();
+    double* part = a.partials + static_cast<size_t>(parity) * 2 * kBisectVals * nb;
+    if (tid < 2 * kBisectVals) {
+      const int s = tid / kBisectVals, k = tid % kBisectVals;
+      double v = 0.0;
+      for (int w = 0; w < kBisectThreads / 32; ++w) v += wsum[w][s][k];
+      part[static_cast<size_t>(tid) * nb + blockIdx.x] = v;
+    }
+    grid.sync();
+    // every block: totals in block order, one warp per (set, value) pair
+    for (int pair = warp; pair < 2 * kBisectVals; pair += kBisectThreads / 32) {
+      const double* src = part + static_cast<size_t>(pair) * nb;
+      double v = 0.0;
+      for (int b = lane; b < nb; b += 32) v += src[b];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) tot[pair / kBisectVals][pair % kBisectVals] = v;
+    }
+    __syncthreads();
+    if (tid < 2 && run[tid]) {
+      double nsq[kNuCands], gd[kNuCands];
+      for (int p = 0; p < kNuCands; ++p) {
+        nsq[p] = tot[tid][2 * p];
+        gd[p] = tot[tid][2 * p + 1];
+      }
+      ndg_replay(&st[tid], nsq, gd, kNuLevels);
+      // no breakpoint inside this pass's bracket: none inside the narrower one
+      if (!st[tid].done && tot[tid][2 * kNuCands] == 0.0) {
+        ndg_finish_analytic(&st[tid], tot[tid][2 * kNuCands + 1], tot[tid][2 * kNuCands + 2],
+                            tot[tid][2 * kNuCands + 3]);
+      }
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid < 2 && a.active[tid]) *a.ns[tid] = st[tid];
+}
+
+__global__ void k_clear_pending(DevState* st) { st->pending = 0.0; }
+
+void enqueue_average(folp_gpu_ctx* c) {
+  DevState* st = c->st_h;
+  OpAverage op{};
+  op.n = c->n;
+  op.m1 = c->m1;
+  op.x = c->cur_x();
+  op.y = c->cur_y();
+  op.ax = c->avg_x;
+  op.ay = c->avg_y;
+  op.l = c->lw;
+  op.u = c->uw;
+  op.pending = st->pending;
+  op.copy_current = st->avg_weight <= 0.0 ? 1 : 0;
+  op.inv = st->avg_weight > 0.0 ? 1.0 / st->avg_weight : 0.0;
+  op.out_x = c->avgp_x;
+  op.out_y = c->avgp_y;
+  if (c->capturing_eval) {
+    // graph: the weights are read on device at run time, then pending is
+    // cleared there (the host mirror is cleared before the launch)
+    op.st = c->st_d;
+    c->ew(c->n + c->m, op, 6);
+    k_clear_pending<<<1, 1, 0, c->stream>>>(c->st_d);
+    ++c->launches;
+    CK(cudaGetLastError());
+    return;
+  }
+  c->ew(c->n + c->m, op, 6);
+  st->pending = 0.0;
+  c->push_state();
+}
+
+// convergence_info reductions of a slot into the block at res[base].
+void enqueue_evaluate(folp_gpu_ctx* c, int which, int raw, int base) {
+  OpEvalPoint op{};
+  op.raw = raw != 0 ? 1 : 0;
+  op.n = c->n;
+  op.m = c->m;
+  op.xs = c->slot_x(which);
+  op.ys = c->slot_y(which);
+  op.d1 = c->d1;
+  op.d2 = c->d2;
+  op.l = c->l0;
+  op.u = c->u0;
+  op.c = c->c0;
+  op.q = c->q0;
+  op.xr = c->xr;
+  op.yr = c->yr;
+  op.result = c->res + base;
+  c->ew(c->n + c->m, op, 7);
+  axis_product(c, true, false, EpiPrimalResidual{c->xr, c->q0, c->m1, c->res + base + 3}, 8);
+  EpiDualResidual dres{c->yr, c->c0, c->l0, c->u0, c->res + base + 4};
+  dres.q_dot_y = c->res + base + 1;
+  dres.constant = c->objective_constant;
+  dres.dual_objective = c->res + base + 10;
+  axis_product(c, false, false, dres, 9);
+  if (!c->norms_ready) {
+    c->ew(c->m, OpNormSq{c->q0, c->res + kResNorms}, 10);
+    c->ew(c->n, OpNormSq{c->c0, c->res + kResNorms + 1}, 11);
+  }
+}
+
+// Reads a block written by enqueue_evaluate (after the sync).
+void read_evaluate(folp_gpu_ctx* c, int base, folp_gpu_eval* out) {
+  if (!c->norms_ready) {
+    c->norm_q_sq = c->res_h[kResNorms];
+    c->norm_c_sq = c->res_h[kResNorms + 1];
+    c->norms_ready = true;
+  }
+  const double* r = c->res_h + base;
+  out->c_dot_x = r[0];
+  out->q_dot_y = r[1];
+  out->nonfinite = r[2] != 0.0 ? 1 : 0;
+  out->primal_sq = r[3];
+  out->dual_sq = r[4];
+  out->bound_terms = r[5];
+  out->infinite_product = r[6] != 0.0 ? 1 : 0;
+  out->norm_q = std::sqrt(c->norm_q_sq);
+  out->norm_c = std::sqrt(c->norm_c_sq);
+  // lp_model.cpp:154-163; ordered mode folded it term by term on device
+  out->dual_objective =
+      c->ordered ? r[10] : (out->q_dot_y + c->objective_constant) + out->bound_terms;
+}
+
+void enqueue_distance(folp_gpu_ctx* c, int a, int b, int base) {
+  OpDistance op{c->n, c->slot_x(a), c->slot_x(b), c->slot_y(a), c->slot_y(b), c->res + base};
+  c->ew(c->n + c->m, op, 12);
+}
+
+// g, lo, hi of a slot into scratch set s with the setup sums
+// (solver.cpp:300-342); Kx of the point is cached for CURRENT and kept for
+// AVERAGE (a restart to it reuses it).
+void enqueue_ndg_setup(folp_gpu_ctx* c, int which, int s, double omega) {
+  const int64_t n = c->n, m = c->m;
+  double* px = c->slot_x(which);
+  double* py = c->slot_y(which);
+  double* sums = c->res + kResNdg[s];
+  EpiNdgPrimal ep{py, px, c->cw, c->lw, c->uw, omega, c->g[s], c->lo[s], c->hi[s], sums};
+  if (c->capturing_eval) ep.omega_dev = c->eval_omega_d;
+  axis_product(c, false, true, ep, 13, 0);
+  EpiNdgDual ed{};
+  ed.x = px;
+  ed.y = py;
+  ed.q = c->qw;
+  ed.m1 = c->m1;
+  ed.winv = 1.0 / omega;
+  ed.g = c->g[s] + n;
+  ed.lo = c->lo[s] + n;
+  ed.result = sums;
+  ed.primal_terms = c->terms[0];
+  ed.n = n;
+  if (c->capturing_eval) ed.omega_dev = c->eval_omega_d;
+  if (which == FOLP_PT_CURRENT && c->kx_valid) {
+    ed.kx_out = nullptr;
+    c->ew(m, OpNdgDualCached{c->kx[c->st_h->cur], ed}, 14, 1);
+  } else {
+    ed.kx_out = which == FOLP_PT_AVERAGE ? c->kx_avg : c->kx_aux;
+    axis_product(c, true, true, ed, 14, 1);
+  }
+}
+
+void enqueue_ndg_init(folp_gpu_ctx* c, int s, int dist_base, double radius, double omega) {
+  const double* dist = dist_base >= 0 ? c->res + dist_base : nullptr;
+  k_ndg_init<<<1, 1, 0, c->stream>>>(c->ndg_d + s, c->res + kResNdg[s], dist, radius, omega,
+                                     c->capturing_eval ? c->eval_omega_d : nullptr);
+  ++c->launches;
+  CK(cudaGetLastError());
+}
+
+// One bisection pass (3 levels in tree mode, 1 in ordered mode); a no-op
+// once the bisection of that scratch set is done.
+void enqueue_ndg_pass(folp_gpu_ctx* c, int s, double omega) {
+  OpNdgPass pass{};
+  pass.n = c->n;
+  pass.total = c->n + c->m;
+  pass.g = c->g[s];
+  pass.lo = c->lo[s];
+  pass.hi = c->hi[s];
+  pass.omega = omega;
+  pass.winv = 1.0 / omega;
+  pass.ns = c->ndg_d + s;
+  c->ew(c->n + c->m, pass, 15);
+}
+
+// Passes before the first look: 42 tree levels / 48 ordered levels cover
+// a typical evaluation (the bracket starts at ||g|| / r, the stop is 1e-10 r).
+int ndg_first_batch(const folp_gpu_ctx* c) { return c->ordered ? 48 : 14; }
+int ndg_next_batch(const folp_gpu_ctx* c) { return c->ordered ? 16 : 5; }
+
+// Starts the bisections of the wanted scratch sets and queues the readback
+// of their states: tree mode runs them to the end in one cooperative
+// launch, ordered mode (one reference level per pass) queues a first batch.
+void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]);
+
+void fetch_ndg(folp_gpu_ctx* c) {
+  CK(cudaMemcpyAsync(c->ndg_h, c->ndg_d, 2 * sizeof(NdgState), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// After a synchronized fetch: runs more passes on the scratch sets still
+// bisecting until all wanted ones are done.
+void finish_ndg(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]) {
+  for (int round = 0; round < 256; ++round) {
+    bool pending = false;
+    for (int s = 0; s < 2; ++s) pending = pending || (want[s] && !c->ndg_h[s].done);
+    if (!pending) return;
+    const int batch = ndg_next_batch(c);
+    for (int i = 0; i < batch; ++i) {
+      for (int s = 0; s < 2; ++s) {
+        if (want[s] && !c->ndg_h[s].done) enqueue_ndg_pass(c, s, omega[s]);
+      }
+    }
+    fetch_ndg(c);
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  throw EngineError(FOLP_E_RUNTIME, "normalized_duality_gap: bisection stalled");
+}
+
+void check_ndg_args(double radius, double omega) {
+  if (!(radius > 0.0)) {
+    throw EngineError(FOLP_E_NONPOSITIVE_RADIUS, "normalized_duality_gap: radius must be > 0");
+  }
+  if (!(omega > 0.0)) {
+    throw EngineError(FOLP_E_NONPOSITIVE_WEIGHT, "normalized_duality_gap: omega must be > 0");
+  }
+}
+
+void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]) {
+  if (c->ordered || !c->coop_ok) {
+    // ordered mode, or no cooperative launch on this device/context: passes
+    // of OpNdgPass (finish_ndg continues them after the read-back)
+    for (int i = 0, e = ndg_first_batch(c); i < e; ++i) {
+      for (int s = 0; s < 2; ++s) {
+        if (want[s]) enqueue_ndg_pass(c, s, omega[s]);
+      }
+    }
+  } else {
+    BisectArgs a{};
+    a.n = c->n;
+    a.total = c->n + c->m;
+    for (int s = 0; s < 2; ++s) {
+      a.g[s] = c->g[s];
+      a.lo[s] = c->lo[s];
+      a.hi[s] = c->hi[s];
+      a.ns[s] = c->ndg_d + s;
+      a.active[s] = want[s] ? 1 : 0;
+    }
+    a.partials = c->partials;
+    int& grid = c->bisect_grid;
+    if (grid == 0) {  // co-resident by construction (cooperative launch)
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ndg_bisect, kBisectThreads, 0));
+      grid = std::max(1, std::min(c->sms * std::max(occ, 1), std::min(c->sms * 2, kMaxGrid / 2)));
+      // small problems: no more CTAs than 4 elements per thread -- a
+      // cooperative launch holds every CTA it spans, so concurrent solves of
+      // small programs would otherwise serialize on the whole GPU
+      const int64_t want = (c->n + c->m + int64_t(kBisectThreads) * 4 - 1) / (int64_t(kBisectThreads) * 4);
+      grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, want)));
+    }
+    void* args[] = {&a};
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ndg_bisect),
+                                                      dim3(grid), dim3(kBisectThreads), args, 0,
+                                                      c->stream);
+    if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported ||
+        e == cudaErrorNotPermitted) {
+      cudaGetLastError();
+      c->coop_ok = false;  // e.g. under MPS: fall back to pass kernels from now on
+      enqueue_ndg_solve(c, want, omega);
+      return;
+    }
+    CK(e);
+    ++c->launches;
+  }
+  fetch_ndg(c);
+}
+
+// restart_to without the sync: copies of the restart point (solver.cpp:805-813).
+void enqueue_restart(folp_gpu_ctx* c, int which, int reset_average) {
+  DevState* st = c->st_h;
+  if (which != FOLP_PT_CURRENT) {
+    copy_d2d(c, c->cur_x(), c->slot_x(which), c->n);
+    copy_d2d(c, c->cur_y(), c->slot_y(which), c->m);
+    if (which == FOLP_PT_AVERAGE) {
+      copy_d2d(c, c->kx[st->cur], c->kx_avg, c->m);
+      c->kx_valid = true;
+    } else {
+      refresh_kx(c);
+    }
+  }
+  copy_d2d(c, c->last_x, c->cur_x(), c->n);
+  copy_d2d(c, c->last_y, c->cur_y(), c->m);
+  if (reset_average) zero_average(c);
+  c->push_state();
+}

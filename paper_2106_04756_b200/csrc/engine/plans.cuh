@@ -1,0 +1,223 @@
+// plans.cuh -- unit plans, uploads and the device CSR->CSC transpose.
+// Fragment of engine.cu: included inside its anonymous namespace, after
+// the pieces it uses (one translation unit; see engine.cu for the order).
+#pragma once
+
+// Warp units of one axis (see segdot.cuh): tiles of consecutive short
+// segments (<= kWarpTile nonzeros, <= 256 segments each) and fixed parts of
+// the longer ones, in index order.
+void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
+                const int* d_ptr, const int* d_idx, PlanDev& out, int64_t s_begin = 0) {
+  (void)nnz;
+  const bool ordered = c->ordered;
+  std::vector<int4> units;
+  std::vector<int> multi_seg, multi_parts;
+  int64_t seg0 = -1, tile_nnz = 0;
+  auto close = [&](int64_t seg_end) {
+    if (seg0 >= 0 && seg_end > seg0) {
+      units.push_back(make_int4(static_cast<int>(seg0), static_cast<int>(seg_end),
+                                static_cast<int>(ptr[seg0]), static_cast<int>(ptr[seg_end])));
+    }
+    seg0 = -1;
+    tile_nnz = 0;
+  };
+  for (int64_t s = s_begin; s < S; ++s) {
+    const int64_t len = ptr[s + 1] - ptr[s];
+    if (len <= kWarpTile) {
+      if (seg0 >= 0 && (tile_nnz + len > kWarpTile || s - seg0 >= kWarpTile)) close(s);
+      if (seg0 < 0) seg0 = s;
+      tile_nnz += len;
+      continue;
+    }
+    close(s);
+    if (ordered) {  // one lane sums the whole segment in index order
+      units.push_back(make_int4(static_cast<int>(s), static_cast<int>(s + 1),
+                                static_cast<int>(ptr[s]), static_cast<int>(ptr[s + 1])));
+      continue;
+    }
+    const int multi = static_cast<int>(multi_seg.size());
+    const int64_t part = len > kGiantMin ? kGiantPart : kWarpTile;
+    const int first = static_cast<int>(units.size());
+    for (int64_t b = ptr[s]; b < ptr[s + 1]; b += part) {
+      units.push_back(make_int4(-(multi + 1), first, static_cast<int>(b),
+                                static_cast<int>(std::min<int64_t>(b + part, ptr[s + 1]))));
+    }
+    multi_seg.push_back(static_cast<int>(s));
+    multi_parts.push_back(static_cast<int>(units.size()) - first);
+  }
+  close(S);
+  auto up = [&](const auto& v) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    T* d = dalloc<T>(v.size());
+    out.owned.push_back(d);
+    if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  };
+  {
+    std::vector<int> ls;
+    for (int64_t sg = s_begin; sg < S; ++sg) {
+      if (ptr[sg + 1] - ptr[sg] > kLongSeq) ls.push_back(static_cast<int>(sg));
+    }
+    out.n_long = static_cast<int>(ls.size());
+    if (!ls.empty()) out.long_segs = up(ls);
+  }
+  SegPlan& p = out.sp;
+  p.ptr = d_ptr;
+  p.idx = d_idx;
+  p.S = static_cast<int>(S);
+  p.units = up(units);
+  p.n_units = static_cast<int>(units.size());
+  p.multi_seg = up(multi_seg);
+  p.multi_parts = up(multi_parts);
+  p.n_multi = static_cast<int>(multi_seg.size());
+  p.part_sums = dalloc<double>(units.size());
+  out.owned.push_back(p.part_sums);
+  p.arrivals = dalloc<unsigned>(multi_seg.size());
+  out.owned.push_back(p.arrivals);
+  CK(cudaMemset(p.arrivals, 0, std::max<size_t>(1, multi_seg.size()) * sizeof(unsigned)));
+  c->max_giant = std::max(c->max_giant, p.n_multi);
+}
+
+void upload_index(folp_gpu_ctx* c, const int64_t* src, int* dst, int64_t count, int64_t* stage,
+                  int64_t stage_cap) {
+  for (int64_t off = 0; off < count; off += stage_cap) {
+    const int64_t len = std::min(stage_cap, count - off);
+    CK(cudaMemcpyAsync(stage, src + off, len * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    k_narrow<<<c->simple_grid(len), kBlock, 0, c->stream>>>(stage, dst + off, len);
+    ++c->launches;
+    CK(cudaGetLastError());
+  }
+}
+
+void upload(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
+  if (count <= 0) return;
+  if (src == nullptr) {
+    CK(cudaMemsetAsync(dst, 0, count * sizeof(double), c->stream));
+  } else {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+}
+void download(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
+  if (count > 0 && dst != nullptr) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+}
+void copy_d2d(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
+  if (count > 0 && dst != src) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  }
+}
+
+// CSR -> CSC on the device (the reference's counting
+// pass, sparse_matrix.cpp:82-102): a stable radix sort of the entries by
+// column keeps each column in increasing row order, i.e. exactly the
+// reference's layout.  Fills csc_ptr / csc_row / csc_orig and returns the
+// column starts on the host (for the unit plan).
+// Segment id of every entry: a mark at each segment start (empty segments
+// stack their marks), then an inclusive scan -- no thread walks a whole
+// segment (config 3's dense row has 2M entries).
+__global__ void k_segment_marks(const int* ptr, int64_t S, int64_t nnz, int* marks) {
+  for (int64_t r = 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < S;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = ptr[r];
+    if (k < nnz) atomicAdd(&marks[k], 1);  // integer counts: order-free
+  }
+}
+__global__ void k_iota(int* v, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    v[i] = static_cast<int>(i);
+  }
+}
+void segment_ids(folp_gpu_ctx* c, const int* ptr, int64_t S, int64_t nnz, int* out,
+                 std::vector<void*>& tmp);
+
+__global__ void k_col_counts(const int* col, int64_t nnz, int* counts) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    atomicAdd(&counts[col[i] + 1], 1);  // integer counts: order-free
+  }
+}
+__global__ void k_csc_fill(const int* order, const int* rowid, const double* vals, int64_t nnz,
+                           int* csc_row, double* csc_val) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = order[i];
+    csc_row[i] = rowid[k];
+    csc_val[i] = vals[k];
+  }
+}
+
+void segment_ids(folp_gpu_ctx* c, const int* ptr, int64_t S, int64_t nnz, int* out,
+                 std::vector<void*>& tmp) {
+  cudaStream_t st = c->stream;
+  int* marks = static_cast<int*>(block_alloc(std::max<size_t>(nnz * sizeof(int), 16), false));
+  tmp.push_back(marks);
+  CK(cudaMemsetAsync(marks, 0, nnz * sizeof(int), st));
+  k_segment_marks<<<c->simple_grid(S), kBlock, 0, st>>>(ptr, S, nnz, marks);
+  ++c->launches;
+  CK(cudaGetLastError());
+  size_t bytes = 0;
+  CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, marks, out, static_cast<int>(nnz), st));
+  void* t = block_alloc(std::max<size_t>(bytes, 16), false);
+  tmp.push_back(t);
+  CK(cub::DeviceScan::InclusiveSum(t, bytes, marks, out, static_cast<int>(nnz), st));
+}
+
+void device_transpose(folp_gpu_ctx* c, std::vector<int64_t>& col_start) {
+  const int64_t m = c->m, n = c->n, nnz = c->nnz;
+  cudaStream_t s = c->stream;
+  std::vector<void*> tmp;
+  auto scratch = [&](size_t bytes) {
+    void* p = block_alloc(std::max<size_t>(bytes, 16), false);
+    tmp.push_back(p);
+    return p;
+  };
+  try {
+    int* rowid = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* keys = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* order_in = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* order = static_cast<int*>(scratch(nnz * sizeof(int)));
+    int* counts = static_cast<int*>(scratch((n + 1) * sizeof(int)));
+    const int grid = c->simple_grid(std::max<int64_t>(m, nnz));
+    segment_ids(c, c->csr_ptr, m, nnz, rowid, tmp);
+    k_iota<<<grid, kBlock, 0, s>>>(order_in, nnz);
+    CK(cudaMemsetAsync(counts, 0, (n + 1) * sizeof(int), s));
+    k_col_counts<<<grid, kBlock, 0, s>>>(c->csr_col, nnz, counts);
+    c->launches += 2;
+    CK(cudaGetLastError());
+    int end_bit = 1;
+    while (end_bit < 31 && (int64_t(1) << end_bit) < n) ++end_bit;
+    size_t sort_bytes = 0, scan_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, c->csr_col, keys, order_in, order,
+                                       static_cast<int>(nnz), 0, end_bit, s));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, counts, c->csc_ptr,
+                                     static_cast<int>(n + 1), s));
+    void* sort_tmp = scratch(sort_bytes);
+    void* scan_tmp = scratch(scan_bytes);
+    CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, c->csr_col, keys, order_in, order,
+                                       static_cast<int>(nnz), 0, end_bit, s));
+    CK(cub::DeviceScan::InclusiveSum(scan_tmp, scan_bytes, counts, c->csc_ptr,
+                                     static_cast<int>(n + 1), s));
+    k_csc_fill<<<grid, kBlock, 0, s>>>(order, rowid, c->csr_orig, nnz, c->csc_row, c->csc_orig);
+    c->launches += 3;  // + the two cub passes' kernels, not counted
+    CK(cudaGetLastError());
+    std::vector<int> cs32(static_cast<size_t>(n) + 1);
+    CK(cudaMemcpyAsync(cs32.data(), c->csc_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    col_start.assign(cs32.begin(), cs32.end());
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    for (void* p : tmp) block_free(p);
+    throw;
+  }
+  for (void* p : tmp) block_free(p);
+}
+
+int pick_device(int device) {
+  if (device >= 0) return device;
+  const char* env = std::getenv("FOLP_DEVICE");
+  return env ? std::atoi(env) : 0;
+}
+
+void set_device(folp_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }

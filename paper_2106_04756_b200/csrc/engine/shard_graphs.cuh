@@ -1,0 +1,182 @@
+// shard_graphs.cuh -- row shards, the PDHG chunk graph and the evaluation graph.
+// Fragment of engine.cu: included inside its anonymous namespace, after
+// the pieces it uses (one translation unit; see engine.cu for the order).
+#pragma once
+
+// ---------------------------------------------------------------------
+// Row shards (north_star: K row-partitioned, all-reduce of the
+// partial K'y and of the scalar sums).
+__global__ void k_gather_values(double* out, const double* src, const int* pos, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    out[i] = src[pos[i]];
+  }
+}
+
+// Contiguous row ranges with about equal nonzeros + rows (so empty rows
+// still spread); monotone, covers [0, m).
+std::vector<int64_t> shard_rows(int64_t m, const int64_t* row_start, int world) {
+  std::vector<int64_t> b(static_cast<size_t>(world) + 1, 0);
+  const double total = static_cast<double>(row_start[m]) + static_cast<double>(m);
+  int64_t r = 0;
+  for (int p = 1; p < world; ++p) {
+    const double target = total * p / world;
+    while (r < m && static_cast<double>(row_start[r]) + static_cast<double>(r) < target) ++r;
+    b[p] = r;
+  }
+  b[world] = m;
+  return b;
+}
+
+// The entries of rows [r0, r1) in CSC order: within every column the rows
+// are increasing (sparse_matrix.cpp:82-102), so they form one sub-range.
+// lptr [n+1] local column starts; pos = full-CSC positions of the entries.
+void shard_local_csc(int64_t n, const int64_t* col_start, const int64_t* col_rows, int64_t r0,
+                     int64_t r1, std::vector<int64_t>& lptr, std::vector<int64_t>& pos) {
+  lptr.assign(static_cast<size_t>(n) + 1, 0);
+  pos.clear();
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t* b = col_rows + col_start[j];
+    const int64_t* e = col_rows + col_start[j + 1];
+    const int64_t* lo = std::lower_bound(b, e, r0);
+    const int64_t* hi = std::lower_bound(lo, e, r1);
+    for (const int64_t* k = lo; k < hi; ++k) pos.push_back(k - col_rows);
+    lptr[j + 1] = static_cast<int64_t>(pos.size());
+  }
+}
+
+void ensure_gathered(folp_gpu_ctx* c) {
+  if (!c->sharded() || !c->rows_dirty) return;
+  const int cur = c->st_h->cur;
+  c->comm->gather_rows(c->y[cur], c->shard_bounds, c->stream);
+  c->comm->gather_rows(c->kx[cur], c->shard_bounds, c->stream);
+  c->comm->gather_rows(c->avg_y, c->shard_bounds, c->stream);
+  c->rows_dirty = false;
+}
+
+// Entry of every engine call that reads the iterate: a sharded context
+// first reassembles the row-space vectors the loop kept local.
+void prep(folp_gpu_ctx* c) {
+  set_device(c);
+  ensure_gathered(c);
+}
+
+// One sharded trial slot (see ops.cuh, "Row-sharded trial").
+void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
+  c->seg(c->lcols, c->lcsc_val, EpiShardKty{b, c->kty_part, nullptr}, 1);
+  c->comm->allreduce_sum(c->kty_part, c->n, c->stream);
+  c->ew(c->n, OpShardPrimal{EpiPrimal{b}, c->kty_part}, 2);
+  EpiDual ed{b};
+  ed.shard_out = c->shard_sums;
+  c->seg(c->lrows, c->csr_work, ed, 3);
+  c->comm->allreduce_sum(c->shard_sums, 3, c->stream);
+  k_shard_decide<<<1, 1, 0, c->stream>>>(b, c->shard_sums);
+  ++c->launches;
+  CK(cudaGetLastError());
+}
+
+// One trial slot of a step policy: adaptive / constant = {A; B},
+// Malitsky-Pock = {MP-A (first trial only); MP-E; MP-B; MP-C}.
+void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
+  if (policy == FOLP_STEP_MALITSKY_POCK) {
+    c->seg(c->cols, c->csc_work, EpiMpPrimal{b}, 2, 0);
+    c->ew(c->n, OpMpExtrapolate{b}, 5, 1);
+    c->seg(c->rows, c->csr_work, EpiMpDual{b}, 3, 1);
+    c->seg(c->cols, c->csc_work, EpiMpCheck{b}, 6, 0);
+  } else {
+    axis_product(c, false, true, EpiPrimal{b}, 2, 0);
+    axis_product(c, true, true, EpiDual{b}, 3, 1);
+  }
+}
+
+// Builds the chunk graph of a policy: WHILE(running) { trial slot }.
+void build_chunk_graph(folp_gpu_ctx* c, int policy) {
+  c->graph_tried[policy] = true;
+  if (std::getenv("FOLP_NO_GRAPH") != nullptr) return;
+  cudaGraph_t graph = nullptr;
+  if (cudaGraphCreate(&graph, 0) != cudaSuccess) return;
+  cudaGraphConditionalHandle handle;
+  bool ok = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault) ==
+            cudaSuccess;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t node;
+  if (ok) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    ok = cudaGraphAddNode(&node, graph, nullptr, 0, &cp) == cudaSuccess;
+  }
+  if (ok) {
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ok = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      const LoopBufs b = c->loop_bufs(handle, 1);
+      const int64_t before = c->launches;
+      try {
+        launch_slot(c, policy, b);
+      } catch (...) {
+        ok = false;
+      }
+      c->launches = before;
+      cudaGraph_t captured = nullptr;
+      ok = (cudaStreamEndCapture(c->stream, &captured) == cudaSuccess) && ok;
+    }
+  }
+  if (ok) ok = cudaGraphInstantiate(&c->chunk_exec[policy], graph, 0) == cudaSuccess;
+  cudaGetLastError();  // clear a failed optional path
+  if (graph) cudaGraphDestroy(graph);
+  c->graph_ok[policy] = ok;
+  if (!ok && c->chunk_exec[policy]) {
+    cudaGraphExecDestroy(c->chunk_exec[policy]);
+    c->chunk_exec[policy] = nullptr;
+  }
+}
+
+// The evaluation period's device work (average, both evaluations, both
+// distances, both duality-gap setups, inits, the cooperative bisection and
+// the result read-back) captured once per CURRENT parity; omega and the
+// averaging weights are read on device at launch.  Replaces ~20 host-side
+// launches per period.  Tree mode, gaps wanted, Kx of CURRENT cached.
+void build_eval_graph(folp_gpu_ctx* c, int cur) {
+  c->eval_tried[cur] = true;
+  if (std::getenv("FOLP_EVAL_GRAPH") != nullptr && std::atoi(std::getenv("FOLP_EVAL_GRAPH")) == 0) {
+    return;
+  }
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  bool ok = true;
+  const int64_t before = c->launches;
+  c->capturing_eval = true;
+  try {
+    const int slots[2] = {FOLP_PT_CURRENT, FOLP_PT_AVERAGE};
+    CK(cudaMemcpyAsync(c->eval_omega_d, c->eval_omega_h, sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    enqueue_average(c);
+    for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s]);
+    for (int s = 0; s < 2; ++s) {
+      enqueue_distance(c, slots[s], FOLP_PT_LAST, kResDist[s]);
+      enqueue_ndg_setup(c, slots[s], s, 1.0);
+      enqueue_ndg_init(c, s, kResDist[s], 0.0, 1.0);
+    }
+    enqueue_ndg_solve(c, {true, true}, {1.0, 1.0});
+    CK(cudaMemcpyAsync(c->res_h, c->res, kResUsed * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+  } catch (...) {
+    ok = false;
+  }
+  c->capturing_eval = false;
+  c->launches = before;
+  ok = (cudaStreamEndCapture(c->stream, &graph) == cudaSuccess) && ok;
+  if (ok) ok = cudaGraphInstantiate(&c->eval_exec[cur], graph, 0) == cudaSuccess;
+  cudaGetLastError();
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok && c->eval_exec[cur]) {
+    cudaGraphExecDestroy(c->eval_exec[cur]);
+    c->eval_exec[cur] = nullptr;
+  }
+}
