@@ -3,6 +3,11 @@
 // the pieces it uses (one translation unit; see engine.cu for the order).
 #pragma once
 
+double tile_segs_cutoff() {
+  const char* env = std::getenv("FOLP_TILE_CUTOFF");
+  return env ? std::atof(env) : 0.0;  // mean segment length below which tiles hold <= 64 segments
+}
+
 // Warp units of one axis (see segdot.cuh): tiles of consecutive short
 // segments (<= kWarpTile nonzeros, <= 256 segments each) and fixed parts of
 // the longer ones, in index order.
@@ -10,6 +15,18 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
                 const int* d_ptr, const int* d_idx, PlanDev& out, int64_t s_begin = 0) {
   (void)nnz;
   const bool ordered = c->ordered;
+  // segments per tile: tree mode caps it when segments are very short (a
+  // lane then owns several segments, and every extra round waits behind the
+  // gather queue for its operands); FOLP_TILE_SEGS overrides
+  int64_t max_segs = kWarpTile;
+  if (!ordered && S > s_begin) {
+    const double mean = static_cast<double>(ptr[S] - ptr[s_begin]) / static_cast<double>(S - s_begin);
+    if (const char* env = std::getenv("FOLP_TILE_SEGS")) {
+      max_segs = std::max(1, std::atoi(env));
+    } else if (mean < tile_segs_cutoff()) {
+      max_segs = 64;
+    }
+  }
   std::vector<int4> units;
   std::vector<int> multi_seg, multi_parts;
   int64_t seg0 = -1, tile_nnz = 0;
@@ -24,7 +41,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   for (int64_t s = s_begin; s < S; ++s) {
     const int64_t len = ptr[s + 1] - ptr[s];
     if (len <= kWarpTile) {
-      if (seg0 >= 0 && (tile_nnz + len > kWarpTile || s - seg0 >= kWarpTile)) close(s);
+      if (seg0 >= 0 && (tile_nnz + len > kWarpTile || s - seg0 >= max_segs)) close(s);
       if (seg0 < 0) seg0 = s;
       tile_nnz += len;
       continue;
