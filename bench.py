@@ -24,9 +24,11 @@ from the reference sources) on all host cores: one independent solve per core,
 aggregate iterations/s.  Multi-GPU (torchrun): `--parallelism replicas`
 runs an independent copy of the workload per rank ("replicas only" for
 configs 1-2; weak scaling); `--parallelism shards` runs ONE
-solve row-partitioned over the ranks (NCCL collectives issued by the engine,
-include/folp_gpu.h folp_gpu_shard; strong scaling).  `auto` shards configs
-3-5 when N > 1.
+solve partitioned over the ranks (NCCL collectives issued by the engine,
+include/folp_gpu.h folp_gpu_shard; strong scaling) -- by rows (the north_star
+layout, all-reduce of n + 3 doubles per trial) or by columns (m + 2), per
+`--partition` (default: the shorter exchange).  `auto` shards configs 3-5
+when N > 1.
 """
 from __future__ import annotations
 
@@ -242,14 +244,24 @@ def config_block(lp, args) -> dict:
             "step": f"{CADENCE} accepted PDHG iterations + evaluation/restart check",
             "l2": f"resident working set ~{working_mb:.0f} MB (K~ CSR+CSC, original values, "
                   f"iterate vectors) > 126 MB L2; no flush",
-            "parallelism": parallelism_name(args)}
+            "parallelism": parallelism_name(args, lp)}
 
 
-def parallelism_name(args) -> str:
+def parallelism_name(args, lp) -> str:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if use_shards(args, world):
-        return f"rows{world} (row-sharded K, NCCL all-reduce of K'y + trial sums)"
+        return (f"cols{world} (column-sharded K, NCCL all-reduce of Kx' + trial sums)"
+                if shard_partition(args, lp) == "cols" else
+                f"rows{world} (row-sharded K, NCCL all-reduce of K'y + trial sums)")
     return f"replicas{world}" if world > 1 else "single"
+
+
+def shard_partition(args, lp) -> str:
+    """--partition auto: the engine's FOLP_SHARD_AUTO rule (columns when
+    m + 2 < n), resolved here for the config name."""
+    if args.partition != "auto":
+        return args.partition
+    return "cols" if lp.num_rows + 2 < lp.num_cols else "rows"
 
 
 def run_b200(args, world, rank, local):
@@ -263,7 +275,7 @@ def run_b200(args, world, rank, local):
     spec = None
     if sharded:
         from paper_2106_04756_b200 import shard
-        spec = shard.nccl_spec()
+        spec = shard.nccl_spec(partition=shard_partition(args, lp))
     # replicas: every rank runs its own solve (work x world); shards: one solve
     jobs = 1 if sharded else world
 
@@ -297,7 +309,7 @@ def run_b200(args, world, rank, local):
     e2e_iters = CADENCE * args.steps
     t = time.perf_counter()
     if sharded:
-        spec = shard.nccl_spec()  # a fresh communicator for the new solve
+        spec = shard.nccl_spec(partition=shard_partition(args, lp))  # a fresh communicator
     r = eng.solve_lp(lp, cabi.params(eps_optimal=args.eps, iteration_limit=e2e_iters),
                      trace_capacity=1, shard=spec)
     e2e_s = time.perf_counter() - t
@@ -389,6 +401,7 @@ def main():
                     help="also solve config 1 to 1e-8 (B200 and reference CPU) and the "
                          "workload with this time limit (s); 0 disables")
     ap.add_argument("--parallelism", choices=["auto", "replicas", "shards"], default="auto")
+    ap.add_argument("--partition", choices=["auto", "rows", "cols"], default="auto")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     try:

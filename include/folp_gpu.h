@@ -274,12 +274,19 @@ const char* folp_gpu_last_error(void);
 #define FOLP_SHARD_NCCL 1
 #define FOLP_SHARD_LOOPBACK 2
 #define FOLP_NCCL_ID_BYTES 128
+/* Partition axis.  ROWS (the north_star layout): rank p owns rows of K,
+ * exchanges the partial K'y (n doubles) and 3 sums per trial.  COLS: rank p
+ * owns columns, exchanges the partial Kx' and 2 sums (m + 2 doubles) -- the
+ * cheaper exchange when m < n (configs 2, 4, 5).  AUTO: the shorter one. */
+#define FOLP_SHARD_ROWS 0
+#define FOLP_SHARD_COLS 1
+#define FOLP_SHARD_AUTO 2
 
 typedef struct folp_gpu_shard {
   int32_t rank;
   int32_t world;
   int32_t backend; /* FOLP_SHARD_NCCL or FOLP_SHARD_LOOPBACK */
-  int32_t pad;
+  int32_t partition; /* FOLP_SHARD_ROWS (0), FOLP_SHARD_COLS or FOLP_SHARD_AUTO */
   unsigned char nccl_id[FOLP_NCCL_ID_BYTES]; /* folp_gpu_nccl_unique_id on rank 0 */
   void* loopback;                            /* folp_gpu_loopback_create(world) */
 } folp_gpu_shard;
@@ -304,6 +311,14 @@ int folp_gpu_shard_local_csc(int64_t n, const int64_t* col_start,
                              int64_t* lptr, int64_t* pos, int64_t pos_capacity,
                              int64_t* lnnz);
 
+/* Column partition: the CSC entries of columns [c0, c1) in CSR order
+ * (local row starts lptr [m+1], their full-CSC positions in pos).  Host
+ * only.  Column ranges come from folp_gpu_shard_rows(n, col_start, ...). */
+int folp_gpu_shard_local_csr(int64_t m, const int64_t* col_start,
+                             const int64_t* col_rows, int64_t c0, int64_t c1,
+                             int64_t* lptr, int64_t* pos, int64_t pos_capacity,
+                             int64_t* lnnz);
+
 /* Turns a context into shard spec->rank of spec->world (after create and
  * rescale; the host CSR row starts and CSC of the same matrix). */
 int folp_gpu_shard_attach(folp_gpu_ctx* ctx, const folp_gpu_shard* spec,
@@ -313,6 +328,10 @@ int folp_gpu_shard_attach(folp_gpu_ctx* ctx, const folp_gpu_shard* spec,
 /* *value = max over the shards (identity on an unsharded context). */
 int folp_gpu_shard_max(folp_gpu_ctx* ctx, double* value);
 
+/* The partition the context runs (FOLP_SHARD_ROWS for an unsharded one). */
+int folp_gpu_shard_partition(folp_gpu_ctx* ctx, int32_t* partition);
+
+/* r0, r1: the shard's range on its partition axis (rows or columns). */
 int folp_gpu_shard_info(folp_gpu_ctx* ctx, int32_t* rank, int32_t* world,
                         int64_t* r0, int64_t* r1, int64_t* local_nnz);
 

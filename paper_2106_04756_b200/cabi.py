@@ -202,11 +202,12 @@ class SolveResult:
 class ShardC(C.Structure):
     """include/folp_gpu.h folp_gpu_shard."""
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("backend", C.c_int32),
-                ("pad", C.c_int32), ("nccl_id", C.c_ubyte * 128), ("loopback", C.c_void_p)]
+                ("partition", C.c_int32), ("nccl_id", C.c_ubyte * 128), ("loopback", C.c_void_p)]
 
 
 SHARD_NCCL = 1
 SHARD_LOOPBACK = 2
+PARTITIONS = {"rows": 0, "cols": 1, "auto": 2}  # FOLP_SHARD_ROWS / COLS / AUTO
 
 
 class Binding:

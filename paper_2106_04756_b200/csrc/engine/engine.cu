@@ -195,11 +195,13 @@ struct folp_gpu_ctx {
   void* loop_block = nullptr;  // K~ values + indices of CSR and CSC (one block)
   size_t loop_block_bytes = 0;
 
-  // row shard: rows [r0, r1) of K~ are this shard's
+  // shard: rows [r0, r1) of K~ are this shard's, or columns
+  // [r0, r1) under the column partition
   std::unique_ptr<ShardComm> comm;
+  bool col_part = false;
   std::vector<int64_t> shard_bounds;  // [world + 1]
   int64_t r0 = 0, r1 = 0, lnnz = 0;
-  PlanDev lrows, lcols;               // local rows of the CSR; local CSC
+  PlanDev lrows, lcols;               // rows: own CSR rows, local CSC; cols: local CSR, own CSC columns
   BlockedAxis brows, bcols;           // window-blocked loop copies (large vectors)
   bool blocked_checked = false;
   int* lcsc_ptr = nullptr;
@@ -209,7 +211,7 @@ struct folp_gpu_ctx {
   double* kty_part = nullptr;
   double* shard_sums = nullptr;
   bool shard_values_ready = false;
-  bool rows_dirty = false;            // y, Kx, avg_y outside [r0, r1) stale
+  bool rows_dirty = false;            // partitioned vectors outside [r0, r1) stale
   bool sharded() const { return comm != nullptr; }
 
   cudaGraphExec_t chunk_exec[3] = {nullptr, nullptr, nullptr};  // per step policy
@@ -1175,6 +1177,23 @@ int folp_gpu_shard_local_csc(int64_t n, const int64_t* col_start, const int64_t*
   });
 }
 
+int folp_gpu_shard_local_csr(int64_t m, const int64_t* col_start, const int64_t* col_rows,
+                             int64_t c0, int64_t c1, int64_t* lptr, int64_t* pos,
+                             int64_t pos_capacity, int64_t* lnnz) {
+  return guarded([&] {
+    std::vector<int64_t> lp, ps;
+    shard_local_csr(m, col_start, col_rows, c0, c1, lp, ps);
+    *lnnz = static_cast<int64_t>(ps.size());
+    std::copy(lp.begin(), lp.end(), lptr);
+    if (pos != nullptr) {
+      if (static_cast<int64_t>(ps.size()) > pos_capacity) {
+        throw std::invalid_argument("shard_local_csr: pos capacity too small");
+      }
+      std::copy(ps.begin(), ps.end(), pos);
+    }
+  });
+}
+
 int folp_gpu_shard_attach(folp_gpu_ctx* c, const folp_gpu_shard* spec, const int64_t* row_start,
                           const int64_t* col_start, const int64_t* col_rows) {
   return guarded([&] {
@@ -1201,29 +1220,57 @@ int folp_gpu_shard_attach(folp_gpu_ctx* c, const folp_gpu_shard* spec, const int
       throw std::invalid_argument("shard_attach: unknown backend");
     }
     const int64_t m = c->m, n = c->n;
-    c->shard_bounds = shard_rows(m, row_start, spec->world);
+    int part = spec->partition;
+    if (part == FOLP_SHARD_AUTO) part = (m + 2 < n) ? FOLP_SHARD_COLS : FOLP_SHARD_ROWS;
+    if (part != FOLP_SHARD_ROWS && part != FOLP_SHARD_COLS) {
+      throw std::invalid_argument("shard_attach: unknown partition");
+    }
+    c->col_part = part == FOLP_SHARD_COLS;
+    // Both partitions keep one plan over the full matrix restricted to the
+    // own range (CSR rows, or CSC columns) and one over the local block in
+    // the other orientation (lcsc_* arrays: entries of the block and their
+    // full-CSC positions, for the value gather after rescaling).
+    const int64_t axis = c->col_part ? n : m;
+    c->shard_bounds = shard_rows(axis, c->col_part ? col_start : row_start, spec->world);
     c->r0 = c->shard_bounds[spec->rank];
     c->r1 = c->shard_bounds[spec->rank + 1];
-    build_plan(c, row_start, c->r1, c->nnz, c->csr_ptr, c->csr_col, c->lrows, c->r0);
     std::vector<int64_t> lptr, pos;
-    shard_local_csc(n, col_start, col_rows, c->r0, c->r1, lptr, pos);
-    c->lnnz = static_cast<int64_t>(pos.size());
-    std::vector<int> lptr32(lptr.begin(), lptr.end()), pos32(pos.size()), row32(pos.size());
-    for (size_t k = 0; k < pos.size(); ++k) {
-      pos32[k] = static_cast<int>(pos[k]);
-      row32[k] = static_cast<int>(col_rows[pos[k]]);
+    if (c->col_part) {
+      build_plan(c, col_start, c->r1, c->nnz, c->csc_ptr, c->csc_row, c->lcols, c->r0);
+      shard_local_csr(m, col_start, col_rows, c->r0, c->r1, lptr, pos);
+    } else {
+      build_plan(c, row_start, c->r1, c->nnz, c->csr_ptr, c->csr_col, c->lrows, c->r0);
+      shard_local_csc(n, col_start, col_rows, c->r0, c->r1, lptr, pos);
     }
-    c->lcsc_ptr = c->alloc<int>(n + 1);
+    c->lnnz = static_cast<int64_t>(pos.size());
+    const int64_t other = c->col_part ? m : n;
+    std::vector<int> lptr32(lptr.begin(), lptr.end()), pos32(pos.size()), idx32(pos.size());
+    for (size_t k = 0; k < pos.size(); ++k) pos32[k] = static_cast<int>(pos[k]);
+    if (c->col_part) {  // the column of each local entry, from the CSC range it sits in
+      const int64_t base = col_start[c->r0];
+      std::vector<int> col_of(static_cast<size_t>(col_start[c->r1] - base));
+      for (int64_t j = c->r0; j < c->r1; ++j) {
+        for (int64_t k = col_start[j]; k < col_start[j + 1]; ++k) {
+          col_of[static_cast<size_t>(k - base)] = static_cast<int>(j);
+        }
+      }
+      for (size_t k = 0; k < pos.size(); ++k) idx32[k] = col_of[static_cast<size_t>(pos[k] - base)];
+    } else {
+      for (size_t k = 0; k < pos.size(); ++k) idx32[k] = static_cast<int>(col_rows[pos[k]]);
+    }
+    c->lcsc_ptr = c->alloc<int>(other + 1);
     c->lcsc_row = c->alloc<int>(c->lnnz + 8);
     c->lcsc_pos = c->alloc<int>(c->lnnz + 1);
     c->lcsc_val = c->alloc<double>(c->lnnz + 8);
-    CK(cudaMemcpy(c->lcsc_ptr, lptr32.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->lcsc_ptr, lptr32.data(), (other + 1) * sizeof(int), cudaMemcpyHostToDevice));
     if (c->lnnz > 0) {
-      CK(cudaMemcpy(c->lcsc_row, row32.data(), c->lnnz * sizeof(int), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->lcsc_row, idx32.data(), c->lnnz * sizeof(int), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(c->lcsc_pos, pos32.data(), c->lnnz * sizeof(int), cudaMemcpyHostToDevice));
     }
-    build_plan(c, lptr.data(), n, c->lnnz, c->lcsc_ptr, c->lcsc_row, c->lcols);
-    c->kty_part = c->alloc<double>(std::max<int64_t>(n, 1));
+    build_plan(c, lptr.data(), other, c->lnnz, c->lcsc_ptr, c->lcsc_row,
+               c->col_part ? c->lrows : c->lcols);
+    // row partition: partial K'y [n]; column partition: partial Kx' [m] + sx, bad
+    c->kty_part = c->alloc<double>(std::max<int64_t>(c->col_part ? m + 2 : n, 1));
     c->shard_sums = c->alloc<double>(4);
     c->shard_values_ready = false;
     c->rows_dirty = false;
@@ -1237,13 +1284,19 @@ int folp_gpu_shard_max(folp_gpu_ctx* c, double* value) {
   });
 }
 
+int folp_gpu_shard_partition(folp_gpu_ctx* c, int32_t* partition) {
+  return guarded([&] {
+    *partition = c->sharded() && c->col_part ? FOLP_SHARD_COLS : FOLP_SHARD_ROWS;
+  });
+}
+
 int folp_gpu_shard_info(folp_gpu_ctx* c, int32_t* rank, int32_t* world, int64_t* r0, int64_t* r1,
                         int64_t* local_nnz) {
   return guarded([&] {
     *rank = c->sharded() ? c->comm->rank : 0;
     *world = c->sharded() ? c->comm->world : 1;
     *r0 = c->sharded() ? c->r0 : 0;
-    *r1 = c->sharded() ? c->r1 : c->m;
+    *r1 = c->sharded() ? c->r1 : (c->col_part ? c->n : c->m);
     *local_nnz = c->sharded() ? c->lnnz : c->nnz;
   });
 }

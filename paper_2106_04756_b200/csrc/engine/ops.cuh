@@ -144,7 +144,13 @@ struct EpiPrimal {
     acc.add(0, j, omega * dx * dx);
     acc.add(1, j, isfinite(xv) ? 0.0 : 1.0);
   }
+  double* shard_out = nullptr;  // column shard: local sums for the all-reduce
   __device__ void finalize(const double (&tot)[K]) const {
+    if (shard_out != nullptr) {
+      shard_out[0] = tot[0];
+      shard_out[1] = tot[1];
+      return;
+    }
     b.st->sx = tot[0];
     b.st->bad_a = tot[1];
   }
@@ -295,24 +301,28 @@ struct EpiDual {
 // GPUs, all-reduce of the partial K'y and of the scalar reductions).  Rank p
 // owns rows [r0, r1): y, Kx and the averaged y of those rows; x, c, l, u and
 // the primal step are replicated.  One trial =
-//   EpiShardKty (partial K'_p y_p over the local CSC)  -> all-reduce (n)
+//   EpiShardPart (partial K'_p y_p over the local CSC) -> all-reduce (n)
 //   OpShardPrimal (kernel A's epilogue on the summed K'y, replicated)
 //   EpiDual over the local rows with shard_out        -> all-reduce (3)
 //   k_shard_decide (kernel B's finalize on the global sums)
 // Every rank holds bit-identical replicated data and sums, so every rank
 // takes the same decisions.
-struct EpiShardKty {
+// Partial product of the own block, stored (no reduction): K'_p y_p over
+// the local CSC (row partition), or K_p x'_p over the local CSR of the own
+// columns (column partition, of the TRIAL primal).
+struct EpiShardPart {
   static constexpr int K = 1;
   static constexpr bool kReduce = false;
   LoopBufs b;
   double* out;
-  const double* yv;
+  const double* v;
+  bool trial_x;
   __device__ bool prepare() {
     if (!b.st->running) return false;
-    yv = pick(b.y, b.st->cur);
+    v = trial_x ? pick(b.x, b.st->cur ^ 1) : pick(b.y, b.st->cur);
     return true;
   }
-  __device__ const double* vec() const { return yv; }
+  __device__ const double* vec() const { return v; }
   struct Pre {};
   __device__ Pre load(int) const { return Pre{}; }
   template <class Acc>
@@ -345,6 +355,36 @@ __global__ void k_shard_decide(LoopBufs b, const double* sums) {
   movement = movement + st->sx;
   decide_trial(b, sums[0], movement, st->bad_a != 0.0 || sums[2] != 0.0);
 }
+
+// Column-sharded trial (the partition on the shorter axis
+// when m < n: the exchange is then m + 2 doubles instead of n).  Rank p owns
+// columns [c0, c1): x, the averaged x and c, l, u of those columns; y, Kx and
+// the dual step are replicated.  One trial =
+//   EpiPrimal over the own CSC columns, sums to shard_out (partial sx, bad)
+//   EpiShardPart: partial K_p x'_p over the own block in CSR order
+//   all-reduce (m + 2: the partial Kx' and the two primal sums)
+//   OpShardDual: kernel B's epilogue on the summed Kx' over all rows
+//     (replicated), whose finalize takes the step decision.
+struct OpShardDual {
+  static constexpr int K = 3;
+  static constexpr bool kReduce = true;
+  EpiDual e;
+  const double* kx;
+  const double* a_sums;  // global sx, bad of kernel A
+  __device__ bool prepare() { return e.prepare(); }
+  template <class Acc>
+  __device__ void apply(int64_t i, Acc& acc) const {
+    const int ii = static_cast<int>(i);
+    e.apply(ii, kx[ii], e.load(ii), acc);
+  }
+  __device__ void finalize(const double (&tot)[K]) const {
+    const DevState* st = e.b.st;
+    double movement = tot[1] / st->omega;  // solver.cpp:83, on the global sums
+    movement = movement + a_sums[0];
+    decide_trial(e.b, tot[0], movement, a_sums[1] != 0.0 || tot[2] != 0.0);
+  }
+  __device__ void finalize_ordered(const double*, int64_t) const {}
+};
 
 // ---------------------------------------------------------------------
 // Small problems (config 1: 10^4 nonzeros): a whole chunk of trials in ONE

@@ -1,4 +1,4 @@
-// shard_graphs.cuh -- row shards, the PDHG chunk graph and the evaluation graph.
+// shard_graphs.cuh -- row / column shards, the PDHG chunk graph and the evaluation graph.
 // Fragment of engine.cu: included inside its anonymous namespace, after
 // the pieces it uses (one translation unit; see engine.cu for the order).
 #pragma once
@@ -45,12 +45,32 @@ void shard_local_csc(int64_t n, const int64_t* col_start, const int64_t* col_row
   }
 }
 
+// Column partition: the entries of columns [c0, c1) in CSR order (a
+// counting pass by row over the CSC range; columns ascend within each row
+// because the range is walked column by column).  lptr [m+1] local row
+// starts; pos = full-CSC positions of the entries.
+void shard_local_csr(int64_t m, const int64_t* col_start, const int64_t* col_rows, int64_t c0,
+                     int64_t c1, std::vector<int64_t>& lptr, std::vector<int64_t>& pos) {
+  lptr.assign(static_cast<size_t>(m) + 1, 0);
+  const int64_t k0 = col_start[c0], k1 = col_start[c1];
+  for (int64_t k = k0; k < k1; ++k) ++lptr[static_cast<size_t>(col_rows[k]) + 1];
+  for (int64_t i = 0; i < m; ++i) lptr[i + 1] += lptr[i];
+  pos.assign(static_cast<size_t>(k1 - k0), 0);
+  std::vector<int64_t> fill(lptr.begin(), lptr.end() - 1);
+  for (int64_t k = k0; k < k1; ++k) pos[static_cast<size_t>(fill[col_rows[k]]++)] = k;
+}
+
 void ensure_gathered(folp_gpu_ctx* c) {
   if (!c->sharded() || !c->rows_dirty) return;
   const int cur = c->st_h->cur;
-  c->comm->gather_rows(c->y[cur], c->shard_bounds, c->stream);
-  c->comm->gather_rows(c->kx[cur], c->shard_bounds, c->stream);
-  c->comm->gather_rows(c->avg_y, c->shard_bounds, c->stream);
+  if (c->col_part) {  // y, Kx and avg_y are replicated; x and avg_x are not
+    c->comm->gather_rows(c->x[cur], c->shard_bounds, c->stream);
+    c->comm->gather_rows(c->avg_x, c->shard_bounds, c->stream);
+  } else {
+    c->comm->gather_rows(c->y[cur], c->shard_bounds, c->stream);
+    c->comm->gather_rows(c->kx[cur], c->shard_bounds, c->stream);
+    c->comm->gather_rows(c->avg_y, c->shard_bounds, c->stream);
+  }
   c->rows_dirty = false;
 }
 
@@ -61,9 +81,19 @@ void prep(folp_gpu_ctx* c) {
   ensure_gathered(c);
 }
 
-// One sharded trial slot (see ops.cuh, "Row-sharded trial").
+// One sharded trial slot (see ops.cuh, "Row-sharded trial" and
+// "Column-sharded trial").
 void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
-  c->seg(c->lcols, c->lcsc_val, EpiShardKty{b, c->kty_part, nullptr}, 1);
+  if (c->col_part) {
+    EpiPrimal ep{b};
+    ep.shard_out = c->kty_part + c->m;  // partial sx, bad ride with the partial Kx'
+    c->seg(c->lcols, c->csc_work, ep, 2);
+    c->seg(c->lrows, c->lcsc_val, EpiShardPart{b, c->kty_part, nullptr, true}, 1);
+    c->comm->allreduce_sum(c->kty_part, c->m + 2, c->stream);
+    c->ew(c->m, OpShardDual{EpiDual{b}, c->kty_part, c->kty_part + c->m}, 3);
+    return;
+  }
+  c->seg(c->lcols, c->lcsc_val, EpiShardPart{b, c->kty_part, nullptr, false}, 1);
   c->comm->allreduce_sum(c->kty_part, c->n, c->stream);
   c->ew(c->n, OpShardPrimal{EpiPrimal{b}, c->kty_part}, 2);
   EpiDual ed{b};

@@ -62,6 +62,23 @@ def local_csc(n: int, col_start: np.ndarray, col_rows: np.ndarray, r0: int, r1: 
     return lptr, pos[:lnnz.value].copy()
 
 
+def local_csr(m: int, col_start: np.ndarray, col_rows: np.ndarray, c0: int, c1: int):
+    """(lptr [m+1], pos [lnnz]): the CSC entries of columns [c0, c1) in CSR
+    order and their positions in the full CSC (folp_gpu_shard_local_csr)."""
+    cs = np.ascontiguousarray(col_start, dtype=np.int64)
+    cr = np.ascontiguousarray(col_rows, dtype=np.int64)
+    lptr = np.zeros(m + 1, dtype=np.int64)
+    pos = np.zeros(max(1, len(cr)), dtype=np.int64)
+    lnnz = C.c_int64()
+    b = engine()
+    p64 = C.POINTER(C.c_int64)
+    _check(b.lib.folp_gpu_shard_local_csr(
+        C.c_int64(m), cs.ctypes.data_as(p64), cr.ctypes.data_as(p64), C.c_int64(c0),
+        C.c_int64(c1), lptr.ctypes.data_as(p64), pos.ctypes.data_as(p64),
+        C.c_int64(len(pos)), C.byref(lnnz)))
+    return lptr, pos[:lnnz.value].copy()
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     b = engine()
@@ -69,9 +86,11 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def nccl_spec(group=None) -> cabi.ShardC:
+def nccl_spec(group=None, partition: str = "rows") -> cabi.ShardC:
     """Shard spec of this rank: rank 0 creates the NCCL unique id, every rank
-    receives it through torch.distributed (any backend)."""
+    receives it through torch.distributed (any backend).  partition: "rows"
+    (north_star: exchange n + 3 doubles per trial), "cols" (m + 2) or "auto"
+    (the shorter exchange)."""
     import torch.distributed as dist
     if not dist.is_available() or not dist.is_initialized():
         rank, world, obj = 0, 1, [nccl_unique_id()]  # a one-rank communicator
@@ -81,14 +100,16 @@ def nccl_spec(group=None) -> cabi.ShardC:
         dist.broadcast_object_list(obj, src=0, group=group)
     spec = cabi.ShardC()
     spec.rank, spec.world, spec.backend = rank, world, cabi.SHARD_NCCL
+    spec.partition = cabi.PARTITIONS[partition]
     C.memmove(spec.nccl_id, obj[0], 128)
     return spec
 
 
-def solve(lp: cabi.LP, p: Optional[dict] = None, x0=None, y0=None, group=None, **kw):
-    """folp::solve as this rank's row shard (torch.distributed initialized,
+def solve(lp: cabi.LP, p: Optional[dict] = None, x0=None, y0=None, group=None,
+          partition: str = "rows", **kw):
+    """folp::solve as this rank's shard (torch.distributed initialized,
     one process per GPU, FOLP_DEVICE / cuda current device = this rank's GPU)."""
-    return engine().solve_lp(lp, p, x0, y0, shard=nccl_spec(group), **kw)
+    return engine().solve_lp(lp, p, x0, y0, shard=nccl_spec(group, partition), **kw)
 
 
 class LoopbackGroup:
@@ -99,9 +120,10 @@ class LoopbackGroup:
         _check(b.lib.folp_gpu_loopback_create(C.c_int32(world), C.byref(h)))
         self.h, self.world = h, world
 
-    def spec(self, rank: int) -> cabi.ShardC:
+    def spec(self, rank: int, partition: str = "rows") -> cabi.ShardC:
         s = cabi.ShardC()
         s.rank, s.world, s.backend, s.loopback = rank, self.world, cabi.SHARD_LOOPBACK, self.h
+        s.partition = cabi.PARTITIONS[partition]
         return s
 
     def close(self):
@@ -112,8 +134,9 @@ class LoopbackGroup:
             self.h = None
 
 
-def solve_loopback(lp: cabi.LP, world: int, p: Optional[dict] = None, **kw) -> list:
-    """`world` row shards as threads of this process on one GPU; returns the
+def solve_loopback(lp: cabi.LP, world: int, p: Optional[dict] = None,
+                   partition: str = "rows", **kw) -> list:
+    """`world` shards as threads of this process on one GPU; returns the
     per-shard results (they must be identical)."""
     g = LoopbackGroup(world)
     out: list = [None] * world
@@ -121,7 +144,7 @@ def solve_loopback(lp: cabi.LP, world: int, p: Optional[dict] = None, **kw) -> l
 
     def run(r):
         try:
-            out[r] = engine().solve_lp(lp, p, shard=g.spec(r), **kw)
+            out[r] = engine().solve_lp(lp, p, shard=g.spec(r, partition), **kw)
         except BaseException as e:  # noqa: BLE001 -- re-raised below
             errs[r] = e
 

@@ -1,4 +1,4 @@
-"""Row-sharded solves on the B200, through the C ABI.
+"""Row- and column-sharded solves on the B200, through the C ABI.
 
 Only one GPU is available per test run, so the sharded schedule is checked
 with the engine's in-process loopback group (W host threads, W shard
@@ -36,12 +36,13 @@ def _same(results):
         assert np.array_equal(b.dual_solution, a.dual_solution)
 
 
+@pytest.mark.parametrize("partition", ["rows", "cols"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("cfg,scale", [(1, 1.0), (5, 0.01)])
-def test_loopback_shards_solve_to_1e8(ref, cfg, scale, world):
+def test_loopback_shards_solve_to_1e8(ref, cfg, scale, world, partition):
     lp = instances.generate(cfg, 1, scale)
     p = cabi.params(kkt_pass_limit=300000)
-    res = shard.solve_loopback(lp, world, p)
+    res = shard.solve_loopback(lp, world, p, partition=partition)
     _same(res)
     a = res[0]
     b = ref.solve_lp(lp, p)
@@ -55,11 +56,12 @@ def test_loopback_shards_solve_to_1e8(ref, cfg, scale, world):
     assert a.step_condition_violations == 0
 
 
+@pytest.mark.parametrize("partition", ["rows", "cols"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_loopback_shards_first_restart_period(ref, world):
+def test_loopback_shards_first_restart_period(ref, world, partition):
     lp = instances.generate(1, 1, 1.0)
     p = cabi.params(record_iterate_trace=True, iteration_limit=100)
-    res = shard.solve_loopback(lp, world, p, iterate_capacity=100)
+    res = shard.solve_loopback(lp, world, p, partition=partition, iterate_capacity=100)
     _same(res)
     b = ref.solve_lp(lp, p, iterate_capacity=100)
     a = res[0]
@@ -72,6 +74,20 @@ def test_loopback_shards_first_restart_period(ref, world):
     assert worst40 <= 1e-10
     assert a.restart_iterations == b.restart_iterations
     assert a.kkt_passes == b.kkt_passes
+
+
+@pytest.mark.parametrize("cfg,scale,want", [(5, 0.005, "cols"), (3, 0.0005, "rows")])
+def test_auto_partition_picks_the_shorter_exchange(cfg, scale, want):
+    """AUTO runs columns when m + 2 < n (config 5's shape) and rows otherwise:
+    its results are bit-identical to the explicit partition's (same
+    schedule, same sums) and differ from the other one's."""
+    lp = instances.generate(cfg, 1, scale)
+    p = cabi.params(iteration_limit=200)
+    auto = shard.solve_loopback(lp, 2, p, partition="auto")
+    same = shard.solve_loopback(lp, 2, p, partition=want)
+    _same(auto + same)
+    other = shard.solve_loopback(lp, 2, p, partition="cols" if want == "rows" else "rows")
+    assert not np.array_equal(other[0].primal_solution, auto[0].primal_solution)
 
 
 def test_shard_rejects_unsupported_modes():

@@ -1,9 +1,12 @@
-"""Host logic of the multi-GPU row shards, no GPU needed:
+"""Host logic of the multi-GPU shards, no GPU needed:
 the row partition (folp_gpu_shard_rows), the per-shard CSC extraction
-(folp_gpu_shard_local_csc), and -- with two gloo processes on 127.0.0.1 --
-the exchange algebra of the sharded trial: the all-reduced partial products
+(folp_gpu_shard_local_csc), the column partition's CSR extraction
+(folp_gpu_shard_local_csr), and -- with two gloo processes on 127.0.0.1 --
+the exchange algebra of the sharded trials: the all-reduced partial products
 K'_p y_p equal K'y, and the shards' K_p x slices reassemble K x (the
-reassembly the engine does by broadcasting each shard's rows)."""
+reassembly the engine does by broadcasting each shard's rows); for the
+column partition the all-reduced K_p x_p equal K x and the shards' x blocks
+reassemble x."""
 import os
 import socket
 
@@ -55,6 +58,28 @@ def test_local_csc_partitions_the_entries(world):
     assert np.all(seen == 1)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("cfg,scale", [(2, 0.002), (5, 0.002)])
+def test_local_csr_partitions_the_entries(cfg, scale, world):
+    lp = instances.generate(cfg, 1, scale)
+    a, c = _csc(lp)
+    b = shard.shard_rows(lp.num_cols, c.indptr, world)  # column ranges
+    assert b[0] == 0 and b[-1] == lp.num_cols
+    seen = np.zeros(a.nnz, dtype=np.int64)
+    for r in range(world):
+        lptr, pos = shard.local_csr(lp.num_rows, c.indptr, c.indices, b[r], b[r + 1])
+        assert lptr[0] == 0 and lptr[-1] == len(pos)
+        assert np.all((pos >= c.indptr[b[r]]) & (pos < c.indptr[b[r + 1]]))
+        rows = c.indices[pos]
+        want = np.repeat(np.arange(lp.num_rows), np.diff(lptr))
+        assert np.array_equal(rows, want)  # grouped by row
+        cols = np.searchsorted(c.indptr, pos, side="right") - 1
+        for i in range(0, lp.num_rows, max(1, lp.num_rows // 50)):
+            assert np.all(np.diff(cols[lptr[i]:lptr[i + 1]]) > 0)  # columns ascend
+        seen[pos] += 1
+    assert np.all(seen == 1)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -98,7 +123,28 @@ def _rank_main(rank, world, port, out):
         gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(gathered, s.double())
         same = all(float(g) == float(gathered[0]) for g in gathered)
-        out.put((rank, kty_err, kx_exact, same, r1 - r0))
+        # column partition: partial K_p x_p over the own columns, all-reduced
+        bc = shard.shard_rows(lp.num_cols, c.indptr, world)
+        c0, c1 = int(bc[rank]), int(bc[rank + 1])
+        lptr, pos = shard.local_csr(lp.num_rows, c.indptr, c.indices, c0, c1)
+        cols = np.searchsorted(c.indptr, pos, side="right") - 1
+        rows = np.repeat(np.arange(lp.num_rows), np.diff(lptr))
+        kxp = np.zeros(lp.num_rows)
+        np.add.at(kxp, rows, c.data[pos] * x[cols])
+        t = torch.from_numpy(kxp)
+        dist.all_reduce(t)
+        kx_ref = a @ x
+        kx_err = float(np.max(np.abs(t.numpy() - kx_ref)) / (1 + np.max(np.abs(kx_ref))))
+        # x blocks reassembled by per-shard broadcasts of the own columns
+        xs = np.zeros(lp.num_cols)
+        xs[c0:c1] = x[c0:c1]
+        fx = torch.from_numpy(xs)
+        for src in range(world):
+            seg = fx[int(bc[src]):int(bc[src + 1])].clone()
+            dist.broadcast(seg, src=src)
+            fx[int(bc[src]):int(bc[src + 1])] = seg
+        x_exact = bool(np.array_equal(fx.numpy(), x))
+        out.put((rank, kty_err, kx_exact and x_exact and kx_err <= 1e-12, same, r1 - r0))
     finally:
         dist.destroy_process_group()
 
