@@ -182,6 +182,7 @@ struct folp_gpu_ctx {
   double norm_q_sq = 0.0, norm_c_sq = 0.0;
   int max_giant = 0;
   int bisect_grid = 0;
+  int* ndg_list = nullptr;        // k_ndg_bisect active lists [2][n + m]
   bool coop_ok = true;            // cooperative launches available (else OpNdgPass passes)
   // evaluation period as a CUDA graph, one per CURRENT buffer parity
   cudaGraphExec_t eval_exec[2] = {nullptr, nullptr};
@@ -518,6 +519,7 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       c->lo[s] = c->alloc<double>(n + m);
       c->hi[s] = vn();
     }
+    if (!c->ordered) c->ndg_list = c->alloc<int>(2 * static_cast<size_t>(n + m) + 2);
     c->partials = c->alloc<double>(static_cast<size_t>(kMaxGrid + c->max_giant + 8) * kMaxAcc);
     if (c->ordered) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);

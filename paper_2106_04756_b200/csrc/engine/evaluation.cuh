@@ -55,9 +55,20 @@ __global__ void k_ndg_init(NdgState* st, const double* sums, const double* dist,
 // synchronizes once, and every block sums the partials in the same order
 // and replays the same decisions, so the bisection state never leaves
 // shared memory until the end.  Replaces up to ~70 launches per period.
+//
+// Active sets: an element whose clamping state cannot change inside the
+// current bracket [nu_lo, nu_hi] (clamped at nu_hi, hence over the whole
+// bracket; or free at nu_lo, hence free over it; or g = 0) leaves the
+// per-midpoint work for good -- its terms are the closed forms w*c^2, g*c
+// (clamped) and g^2/(w*nu^2), g^2/(w*nu) (free), kept as three running sums
+// Q, H, S per thread.  Each block compacts its own element range in place
+// (index list in global memory, order preserved), so after the first pass
+// only the elements with a breakpoint inside the bracket are read again;
+// once no block has any left, ndg_finish_analytic ends the bisection from
+// Q, H, S.
 constexpr int kBisectThreads = 512;
-// ||d||_w^2 and g'd per midpoint, then the bracket sums of the analytic
-// finish: elements with a breakpoint inside, Q, H, S (ndg_finish_analytic)
+// per set: ||d||_w^2 and g'd per midpoint over the active elements, the
+// number of active elements kept, and the running Q, H, S of the retired ones
 constexpr int kBisectVals = 2 * kNuCands + 4;
 
 struct BisectArgs {
@@ -67,6 +78,7 @@ struct BisectArgs {
   const double* hi[2];
   NdgState* ns[2];
   int active[2];
+  int* list[2];      // [total] per set: the blocks' active element lists
   double* partials;  // [2 parity][2 sets][kBisectVals][grid]
 };
 
@@ -76,73 +88,119 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
   __shared__ NdgState st[2];
   __shared__ double wsum[kBisectThreads / 32][2][kBisectVals];
   __shared__ double tot[2][kBisectVals];
+  __shared__ int wcount[kBisectThreads / 32];
+  __shared__ int kept_count[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = gridDim.x;
+  const int64_t chunk = (a.total + nb - 1) / nb;
+  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t own = b0 < a.total ? (a.total - b0 < chunk ? a.total - b0 : chunk) : 0;
   if (tid < 2) {
     st[tid] = *a.ns[tid];
     if (!a.active[tid]) st[tid].done = 1;
+    kept_count[tid] = static_cast<int>(own);
   }
+  double fq[2] = {0.0, 0.0}, fh[2] = {0.0, 0.0}, fs[2] = {0.0, 0.0};
   __syncthreads();
+  bool first = true;
   for (int parity = 0;; parity ^= 1) {
     const bool run[2] = {st[0].done == 0, st[1].done == 0};
     if (!run[0] && !run[1]) break;  // same state in every block
-    double acc[2][kBisectVals];
+    double acc[2][2 * kNuCands];
 #pragma unroll
     for (int s = 0; s < 2; ++s)
 #pragma unroll
-      for (int k = 0; k < kBisectVals; ++k) acc[s][k] = 0.0;
+      for (int k = 0; k < 2 * kNuCands; ++k) acc[s][k] = 0.0;
+    int kept_s[2] = {0, 0};
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       if (!run[s]) continue;
       const double* g = a.g[s];
       const double* lo = a.lo[s];
       const double* hi = a.hi[s];
+      int* list = a.list[s] + b0;
       const double omega = st[s].omega, winv = st[s].winv;
-      for (int64_t i = static_cast<int64_t>(blockIdx.x) * kBisectThreads + tid; i < a.total;
-           i += static_cast<int64_t>(nb) * kBisectThreads) {
-        const double gs = g[i];
-        const bool primal = i < a.n;
-        const double w = primal ? omega : winv;
-        const double los = lo[i];
-        const double his = primal ? hi[i] : INFINITY;
-        const double* rcp = primal ? st[s].rcp_primal : st[s].rcp_dual;
+      const int cnt = kept_count[s];
+      int kept = 0;
+      for (int t0 = 0; t0 < cnt; t0 += kBisectThreads) {
+        const int k = t0 + tid;
+        int i = -1;
+        bool keep = false;
+        if (k < cnt) {
+          i = first ? static_cast<int>(b0 + k) : list[k];
+          const double gs = g[i];
+          if (gs != 0.0) {
+            const bool primal = i < a.n;
+            const double w = primal ? omega : winv;
+            const double los = lo[i];
+            const double his = primal ? hi[i] : INFINITY;
+            const int side = primal ? 0 : 1;
+            const double ulo = gs * st[s].rcp_lo[side];  // |u| largest at nu_lo
+            const double uhi = gs * st[s].rcp_hi[side];
+            const bool clamped_lo = ulo < los || ulo > his;
+            const bool clamped_hi = uhi < los || uhi > his;
+            if (clamped_hi) {  // clamped over the whole bracket
+              const double cv = uhi > his ? his : los;
+              fq[s] += w * cv * cv;
+              fh[s] += gs * cv;
+            } else if (!clamped_lo) {  // free over the whole bracket
+              fs[s] += gs * gs * (primal ? winv : omega);
+            } else {
+              keep = true;
+              const double* rcp = primal ? st[s].rcp_primal : st[s].rcp_dual;
 #pragma unroll
-        for (int p = 0; p < kNuCands; ++p) {
-          const double d = ref_min(ref_max(gs * rcp[p], los), his);
-          acc[s][2 * p] += w * d * d;
-          acc[s][2 * p + 1] += gs * d;
-        }
-        if (gs != 0.0) {
-          const int side = primal ? 0 : 1;
-          const double ulo = gs * st[s].rcp_lo[side];  // |u| largest at nu_lo
-          const double uhi = gs * st[s].rcp_hi[side];
-          const bool clamped_lo = ulo < los || ulo > his;
-          const bool clamped_hi = uhi < los || uhi > his;
-          if (clamped_lo && !clamped_hi) acc[s][2 * kNuCands] += 1.0;
-          if (clamped_hi) {  // clamped over the whole bracket
-            const double cv = uhi > his ? his : los;
-            acc[s][2 * kNuCands + 1] += w * cv * cv;
-            acc[s][2 * kNuCands + 2] += gs * cv;
+              for (int p = 0; p < kNuCands; ++p) {
+                const double d = ref_min(ref_max(gs * rcp[p], los), his);
+                acc[s][2 * p] += w * d * d;
+                acc[s][2 * p + 1] += gs * d;
+              }
+            }
           }
-          if (!clamped_lo) acc[s][2 * kNuCands + 3] += gs * gs * (primal ? winv : omega);
         }
-      }
-    }
+        // in-place, order-preserving compaction of the block's list: every
+        // read of this tile precedes the barrier, every write lands below t0+512
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wcount[warp] = __popc(bal);
+        __syncthreads();
+        int off = kept, tile = 0;
 #pragma unroll
-    for (int s = 0; s < 2; ++s)
+        for (int w = 0; w < kBisectThreads / 32; ++w) {
+          const int c = wcount[w];
+          if (w < warp) off += c;
+          tile += c;
+        }
+        if (keep) list[off + __popc(bal & ((1u << lane) - 1u))] = i;
+        kept += tile;
+        __syncthreads();
+      }
+      kept_s[s] = kept;
+    }
+    __syncthreads();
+    if (tid < 2 && run[tid]) kept_count[tid] = kept_s[tid];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
 #pragma unroll
       for (int k = 0; k < kBisectVals; ++k) {
-        double v = acc[s][k];
+        double v = k < 2 * kNuCands ? acc[s][k]
+                 : k == 2 * kNuCands ? 0.0
+                 : k == 2 * kNuCands + 1 ? fq[s]
+                 : k == 2 * kNuCands + 2 ? fh[s]
+                                         : fs[s];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         if (lane == 0) wsum[warp][s][k] = v;
       }
+    }
     __syncthreads();
     double* part = a.partials + static_cast<size_t>(parity) * 2 * kBisectVals * nb;
     if (tid < 2 * kBisectVals) {
       const int s = tid / kBisectVals, k = tid % kBisectVals;
       double v = 0.0;
-      for (int w = 0; w < kBisectThreads / 32; ++w) v += wsum[w][s][k];
+      if (k == 2 * kNuCands) {
+        v = static_cast<double>(kept_s[s]);
+      } else {
+        for (int w = 0; w < kBisectThreads / 32; ++w) v += wsum[w][s][k];
+      }
       part[static_cast<size_t>(tid) * nb + blockIdx.x] = v;
     }
     grid.sync();
@@ -157,18 +215,19 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
     }
     __syncthreads();
     if (tid < 2 && run[tid]) {
+      const double q = tot[tid][2 * kNuCands + 1], h = tot[tid][2 * kNuCands + 2];
+      const double sf = tot[tid][2 * kNuCands + 3];
       double nsq[kNuCands], gd[kNuCands];
       for (int p = 0; p < kNuCands; ++p) {
-        nsq[p] = tot[tid][2 * p];
-        gd[p] = tot[tid][2 * p + 1];
+        const double nu = st[tid].nu[p];
+        nsq[p] = tot[tid][2 * p] + (q + sf / (nu * nu));
+        gd[p] = tot[tid][2 * p + 1] + (h + sf / nu);
       }
       ndg_replay(&st[tid], nsq, gd, kNuLevels);
       // no breakpoint inside this pass's bracket: none inside the narrower one
-      if (!st[tid].done && tot[tid][2 * kNuCands] == 0.0) {
-        ndg_finish_analytic(&st[tid], tot[tid][2 * kNuCands + 1], tot[tid][2 * kNuCands + 2],
-                            tot[tid][2 * kNuCands + 3]);
-      }
+      if (!st[tid].done && tot[tid][2 * kNuCands] == 0.0) ndg_finish_analytic(&st[tid], q, h, sf);
     }
+    first = false;
     __syncthreads();
   }
   if (blockIdx.x == 0 && tid < 2 && a.active[tid]) *a.ns[tid] = st[tid];
@@ -382,6 +441,8 @@ void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&om
       a.active[s] = want[s] ? 1 : 0;
     }
     a.partials = c->partials;
+    a.list[0] = c->ndg_list;
+    a.list[1] = c->ndg_list + a.total;
     int& grid = c->bisect_grid;
     if (grid == 0) {  // co-resident by construction (cooperative launch)
       int occ = 0;
