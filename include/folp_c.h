@@ -40,7 +40,8 @@ enum {
   FOLP_E_STEP_UNDERFLOW = 15,
   FOLP_E_NONFINITE = 16,
   FOLP_E_INFINITE_PRODUCT = 17,
-  FOLP_E_NO_DEVICE = 18         /* no CUDA device: the engine never falls back */
+  FOLP_E_NO_DEVICE = 18,        /* no CUDA device: the engine never falls back */
+  FOLP_E_IO = 19                /* IoError, MpsParseError ("line N: ...")    */
 };
 
 /* TerminationReason, solver.hpp:72-80 (same order). */
@@ -233,6 +234,29 @@ int folp_malitsky_pock_step(const folp_lp_c* lp, const double* x,
                             double theta_prev, const folp_params_c* params,
                             double* x_next, double* y_next, double* eta_next,
                             double* theta_next, int64_t* trials);
+
+/* ---- MPS and result I/O ---------------------------
+ * parse_mps / parse_mps_file (mps.hpp:50-51), write_mps (:55),
+ * result_to_json / write_result (result_io.hpp:26-31).  A parse error
+ * returns FOLP_E_IO with the reference's "line N: message"; non-finite
+ * matrix values FOLP_E_INVALID_ARGUMENT (SparseMatrix::from_triplets). */
+typedef struct folp_mps folp_mps;
+int folp_mps_parse(const char* text, int64_t length, folp_mps** out);
+int folp_mps_parse_file(const char* path, folp_mps** out);
+/* Views into the parsed instance, valid until folp_mps_destroy. */
+int folp_mps_view(const folp_mps* mps, folp_lp_c* lp, const char** name,
+                  int32_t* was_maximization);
+void folp_mps_destroy(folp_mps* mps);
+/* write_mps / result_to_json into a library-owned buffer (folp_buffer_free);
+ * the result's trace must be complete (trace_capacity >= num_trace). */
+int folp_mps_write(const folp_lp_c* lp, const char* name, char** text,
+                   int64_t* length);
+int folp_result_json(const folp_result_c* result, char** text, int64_t* length);
+/* write_result: summary.json and the three solution files; the vectors have
+ * num_cols / num_rows / num_cols entries. */
+int folp_result_write(const folp_result_c* result, int64_t num_rows,
+                      int64_t num_cols, const char* output_dir);
+void folp_buffer_free(char* buffer);
 
 /* Message of the last failing call on this thread ("" if none). */
 const char* folp_last_error(void);

@@ -14,7 +14,7 @@ from .cabi import LP, Binding, FolpError, SolveResult, params  # noqa: F401
 
 PKG_DIR = Path(__file__).resolve().parent
 LIB_DIR = PKG_DIR / "lib"
-ENGINE_LIB = LIB_DIR / "libfolp_b200.so"
+ENGINE_LIB = Path(os.environ.get("FOLP_ENGINE_LIB", LIB_DIR / "libfolp_b200.so"))  # A/B builds
 GEN_LIB = LIB_DIR / "libfolp_gen.so"
 
 _engine = None

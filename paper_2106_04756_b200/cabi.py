@@ -199,6 +199,35 @@ class SolveResult:
     iterate_trace: list  # (iteration, eta_used, x, y) in the working space
 
 
+def result_to_c(r: SolveResult):
+    """A folp_result_c view of a SolveResult (for the I/O entry points);
+    returns (struct, arrays kept alive)."""
+    x = np.ascontiguousarray(r.primal_solution, dtype=np.float64)
+    y = np.ascontiguousarray(r.dual_solution, dtype=np.float64)
+    z = np.ascontiguousarray(r.reduced_costs, dtype=np.float64)
+    nt = len(r.trace)
+    t_it = np.array([t["iteration"] for t in r.trace] or [0], dtype=np.int64)
+    t_kkt = np.array([t["kkt_passes"] for t in r.trace] or [0.0], dtype=np.float64)
+    t_cur = (InfoC * max(1, nt))()
+    t_avg = (InfoC * max(1, nt))()
+    fields = [f for f, _ in InfoC._fields_]
+    for i, t in enumerate(r.trace):
+        t_cur[i] = InfoC(*[t["current"][f] for f in fields])
+        t_avg[i] = InfoC(*[t["average"][f] for f in fields])
+    rc = ResultC()
+    rc.primal_solution, rc.dual_solution, rc.reduced_costs = _f64(x), _f64(y), _f64(z)
+    rc.trace_capacity = nt
+    rc.num_trace = nt
+    rc.trace_iteration, rc.trace_kkt_passes = _i64(t_it), _f64(t_kkt)
+    rc.trace_current, rc.trace_average = t_cur, t_avg
+    rc.termination_reason = TERMINATION.index(r.termination_reason)
+    rc.final_info = InfoC(*[r.final_info[f] for f in fields])
+    rc.iterations, rc.kkt_passes, rc.wall_seconds = r.iterations, r.kkt_passes, r.wall_seconds
+    rc.restarts, rc.step_trials = r.restarts, r.step_trials
+    rc.step_condition_violations = r.step_condition_violations
+    return rc, (x, y, z, t_it, t_kkt, t_cur, t_avg)
+
+
 class ShardC(C.Structure):
     """include/folp_gpu.h folp_gpu_shard."""
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("backend", C.c_int32),
@@ -248,6 +277,19 @@ class Binding:
             f("session_create_sharded", C.c_int, [C.POINTER(LpC), C.POINTER(ParamsC), _f64p,
                                                    _f64p, C.POINTER(ShardC),
                                                    C.POINTER(C.c_void_p)])
+
+        if hasattr(lib, prefix + "mps_parse"):
+            f("mps_parse", C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)])
+            f("mps_parse_file", C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)])
+            f("mps_view", C.c_int, [C.c_void_p, C.POINTER(LpC), C.POINTER(C.c_char_p),
+                                     C.POINTER(C.c_int32)])
+            f("mps_destroy", None, [C.c_void_p])
+            f("mps_write", C.c_int, [C.POINTER(LpC), C.c_char_p, C.POINTER(C.c_void_p),
+                                      C.POINTER(C.c_int64)])
+            f("result_json", C.c_int, [C.POINTER(ResultC), C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_int64)])
+            f("result_write", C.c_int, [C.POINTER(ResultC), C.c_int64, C.c_int64, C.c_char_p])
+            f("buffer_free", None, [C.c_void_p])
 
     def _fn(self, name, restype, argtypes):
         fn = getattr(self.lib, self.prefix + name)
@@ -323,6 +365,68 @@ class Binding:
             restart_iterations=[int(v) for v in rst[:min(res.num_restart_iterations,
                                                         trace_capacity)]],
             trace=trace, iterate_trace=iters)
+
+    # ---- MPS and result I/O (folp_c.h) ---------------
+    def _mps_lp(self, h) -> tuple:
+        lpc, name, mx = LpC(), C.c_char_p(), C.c_int32()
+        self.check(self.mps_view(h, C.byref(lpc), C.byref(name), C.byref(mx)))
+        m, n, nnz = lpc.num_rows, lpc.num_cols, lpc.nnz
+
+        def arr(ptr, k, dt):
+            return np.ctypeslib.as_array(ptr, shape=(k,)).astype(dt, copy=True) if k else \
+                np.zeros(0, dtype=dt)
+        lp = LP(num_rows=m, num_cols=n, num_inequality_rows=lpc.num_inequality_rows,
+                row_start=arr(lpc.row_start, m + 1, np.int64),
+                row_cols=arr(lpc.row_cols, nnz, np.int64),
+                row_values=arr(lpc.row_values, nnz, np.float64),
+                objective=arr(lpc.objective, n, np.float64),
+                right_hand_side=arr(lpc.right_hand_side, m, np.float64),
+                variable_lower=arr(lpc.variable_lower, n, np.float64),
+                variable_upper=arr(lpc.variable_upper, n, np.float64),
+                objective_constant=lpc.objective_constant, name=name.value.decode())
+        return lp, name.value.decode(), bool(mx.value)
+
+    def parse_mps(self, text) -> tuple:
+        """parse_mps (mps.hpp:50): (LP, name, was_maximization)."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        h = C.c_void_p()
+        self.check(self.mps_parse(data, len(data), C.byref(h)))
+        try:
+            return self._mps_lp(h)
+        finally:
+            self.mps_destroy(h)
+
+    def parse_mps_file(self, path: str) -> tuple:
+        h = C.c_void_p()
+        self.check(self.mps_parse_file(str(path).encode(), C.byref(h)))
+        try:
+            return self._mps_lp(h)
+        finally:
+            self.mps_destroy(h)
+
+    def _take_text(self, call) -> str:
+        buf, length = C.c_void_p(), C.c_int64()
+        self.check(call(C.byref(buf), C.byref(length)))
+        try:
+            return C.string_at(buf, length.value).decode()
+        finally:
+            self.buffer_free(buf)
+
+    def write_mps(self, lp: LP, name: str = "") -> str:
+        """write_mps (mps.hpp:55)."""
+        lpc = lp.to_c()
+        return self._take_text(lambda b, n: self.mps_write(C.byref(lpc), name.encode(), b, n))
+
+    def result_to_json(self, r: SolveResult) -> str:
+        """result_to_json (result_io.hpp:26)."""
+        rc, keep = result_to_c(r)
+        return self._take_text(lambda b, n: self.result_json(C.byref(rc), b, n))
+
+    def write_result(self, r: SolveResult, output_dir: str) -> None:
+        """write_result (result_io.hpp:31)."""
+        rc, keep = result_to_c(r)
+        self.check(self.result_write(C.byref(rc), len(r.dual_solution), len(r.primal_solution),
+                                     str(output_dir).encode()))
 
     def session(self, lp: LP, p: Optional[dict] = None,
                 shard: Optional[ShardC] = None) -> "Session":

@@ -14,6 +14,8 @@
 
 #include "device.hpp"
 #include "folp/lp_model.hpp"
+#include "folp/mps.hpp"
+#include "folp/result_io.hpp"
 #include "folp/scaling.hpp"
 #include "folp/solver.hpp"
 #include "folp/termination.hpp"
@@ -61,6 +63,9 @@ int guarded(F&& f) {
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return FOLP_E_INVALID_ARGUMENT;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return FOLP_E_IO;
   } catch (const DeviceError& e) {
     g_err = e.what();
     return std::strstr(e.what(), "no CUDA device") ? FOLP_E_NO_DEVICE : FOLP_E_CUDA;
@@ -220,7 +225,61 @@ void export_result(const SolveResult& r, folp_result_c* out) {
   }
 }
 
+SolveResult import_result(const folp_result_c* in, int64_t m, int64_t n) {
+  SolveResult r;
+  auto vec = [](const double* p, int64_t k) {
+    return p != nullptr ? std::vector<double>(p, p + k) : std::vector<double>();
+  };
+  r.primal_solution = vec(in->primal_solution, n);
+  r.dual_solution = vec(in->dual_solution, m);
+  r.reduced_costs = vec(in->reduced_costs, n);
+  r.termination_reason = static_cast<TerminationReason>(in->termination_reason);
+  auto info = [](const folp_info_c& i) {
+    ConvergenceInfo o;
+    o.primal_objective = i.primal_objective;
+    o.dual_objective = i.dual_objective;
+    o.gap_abs = i.gap_abs;
+    o.primal_residual_norm = i.primal_residual_norm;
+    o.dual_residual_norm = i.dual_residual_norm;
+    o.norm_q = i.norm_q;
+    o.norm_c = i.norm_c;
+    return o;
+  };
+  r.final_info = info(in->final_info);
+  r.iterations = in->iterations;
+  r.kkt_passes = in->kkt_passes;
+  r.wall_seconds = in->wall_seconds;
+  r.restarts = in->restarts;
+  r.step_trials = in->step_trials;
+  r.step_condition_violations = in->step_condition_violations;
+  if (in->num_trace > in->trace_capacity) {
+    throw std::invalid_argument("result: trace truncated (trace_capacity < num_trace)");
+  }
+  for (int64_t i = 0; i < in->num_trace; ++i) {
+    TraceEntry e;
+    e.iteration = in->trace_iteration[i];
+    e.kkt_passes = in->trace_kkt_passes[i];
+    e.current = info(in->trace_current[i]);
+    e.average = info(in->trace_average[i]);
+    r.trace.push_back(e);
+  }
+  return r;
+}
+
+char* export_text(const std::string& s, int64_t* length) {
+  char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+  if (buf == nullptr) throw std::bad_alloc();
+  std::memcpy(buf, s.data(), s.size());
+  buf[s.size()] = '\0';
+  *length = static_cast<int64_t>(s.size());
+  return buf;
+}
+
 }  // namespace
+
+struct folp_mps {
+  folp::MpsInstance inst;
+};
 
 struct folp_session {
   std::unique_ptr<folp::SolveSession> s;
@@ -430,6 +489,66 @@ int folp_session_result(folp_session* s, folp_result_c* out) {
 }
 
 void folp_session_destroy(folp_session* s) { delete s; }
+
+// ---- MPS and result I/O ----------------------------------------------
+int folp_mps_parse(const char* text, int64_t length, folp_mps** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto m = std::make_unique<folp_mps>();
+    m->inst = parse_mps(std::string_view(text, static_cast<std::size_t>(length)));
+    *out = m.release();
+  });
+}
+
+int folp_mps_parse_file(const char* path, folp_mps** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto m = std::make_unique<folp_mps>();
+    m->inst = parse_mps_file(path);
+    *out = m.release();
+  });
+}
+
+int folp_mps_view(const folp_mps* mps, folp_lp_c* lp, const char** name,
+                  int32_t* was_maximization) {
+  return guarded([&] {
+    const LinearProgram& p = mps->inst.lp;
+    const SparseMatrix& k = p.constraint_matrix;
+    lp->num_rows = p.num_rows();
+    lp->num_cols = p.num_variables();
+    lp->num_inequality_rows = p.num_inequality_rows;
+    lp->nnz = k.nnz();
+    lp->row_start = k.row_start().data();
+    lp->row_cols = k.row_cols().data();
+    lp->row_values = k.row_values().data();
+    lp->objective = p.objective.data();
+    lp->right_hand_side = p.right_hand_side.data();
+    lp->variable_lower = p.variable_lower.data();
+    lp->variable_upper = p.variable_upper.data();
+    lp->objective_constant = p.objective_constant;
+    if (name != nullptr) *name = mps->inst.name.c_str();
+    if (was_maximization != nullptr) *was_maximization = mps->inst.was_maximization ? 1 : 0;
+  });
+}
+
+void folp_mps_destroy(folp_mps* mps) { delete mps; }
+
+int folp_mps_write(const folp_lp_c* lp_in, const char* name, char** text, int64_t* length) {
+  *text = nullptr;
+  return guarded([&] { *text = export_text(write_mps(to_lp(lp_in), name ? name : ""), length); });
+}
+
+int folp_result_json(const folp_result_c* result, char** text, int64_t* length) {
+  *text = nullptr;
+  return guarded([&] { *text = export_text(result_to_json(import_result(result, 0, 0)), length); });
+}
+
+int folp_result_write(const folp_result_c* result, int64_t num_rows, int64_t num_cols,
+                      const char* output_dir) {
+  return guarded([&] { write_result(import_result(result, num_rows, num_cols), output_dir); });
+}
+
+void folp_buffer_free(char* buffer) { std::free(buffer); }
 
 const char* folp_last_error(void) { return g_err.c_str(); }
 

@@ -76,18 +76,48 @@ def test_loopback_shards_first_restart_period(ref, world, partition):
     assert a.kkt_passes == b.kkt_passes
 
 
+def _loopback_launches(eng, lp, p, world, partition):
+    """Kernel launches of a `world`-shard loopback session after two
+    evaluation periods (the per-trial schedules differ: rows = 2 products +
+    primal pass + decide, columns = 2 products + dual pass)."""
+    import threading
+    g = shard.LoopbackGroup(world)
+    out = [None] * world
+
+    def run(r):
+        s = eng.session(lp, p, shard=g.spec(r, partition))
+        try:
+            s.advance(2)
+            out[r] = s.stats()["launches"]
+        finally:
+            s.close()
+
+    try:
+        ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    finally:
+        g.close()
+    assert out[0] == out[1]
+    return out[0]
+
+
 @pytest.mark.parametrize("cfg,scale,want", [(5, 0.005, "cols"), (3, 0.0005, "rows")])
-def test_auto_partition_picks_the_shorter_exchange(cfg, scale, want):
+def test_auto_partition_picks_the_shorter_exchange(eng, cfg, scale, want):
     """AUTO runs columns when m + 2 < n (config 5's shape) and rows otherwise:
-    its results are bit-identical to the explicit partition's (same
-    schedule, same sums) and differ from the other one's."""
+    same results as the explicit partition, and the same launch schedule
+    (which differs between the two partitions)."""
     lp = instances.generate(cfg, 1, scale)
     p = cabi.params(iteration_limit=200)
     auto = shard.solve_loopback(lp, 2, p, partition="auto")
     same = shard.solve_loopback(lp, 2, p, partition=want)
     _same(auto + same)
-    other = shard.solve_loopback(lp, 2, p, partition="cols" if want == "rows" else "rows")
-    assert not np.array_equal(other[0].primal_solution, auto[0].primal_solution)
+    other = "cols" if want == "rows" else "rows"
+    la = _loopback_launches(eng, lp, p, 2, "auto")
+    assert la == _loopback_launches(eng, lp, p, 2, want)
+    assert la != _loopback_launches(eng, lp, p, 2, other)
 
 
 def test_shard_rejects_unsupported_modes():
