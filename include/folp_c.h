@@ -208,6 +208,9 @@ int folp_session_advance(folp_session* s, int64_t evaluations,
  * kernels (profiling is on for sessions); kernel launches so far. */
 int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms,
                        int64_t* loop_slots, int64_t* launches);
+/* The shard partition the session's device context runs (0 rows, 1 columns;
+ * rows for an unsharded one), -1 before a device context exists. */
+int folp_session_partition(folp_session* s, int32_t* partition);
 int folp_session_result(folp_session* s, folp_result_c* out);
 void folp_session_destroy(folp_session* s);
 

@@ -270,6 +270,7 @@ class Binding:
                                             _f64p])
             f("session_stats", C.c_int, [C.c_void_p, _i64p, _f64p, _i64p, _i64p])
             f("session_result", C.c_int, [C.c_void_p, C.POINTER(ResultC)])
+            f("session_partition", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)])
             f("session_destroy", None, [C.c_void_p])
         if hasattr(lib, prefix + "solve_sharded"):
             f("solve_sharded", C.c_int, [C.POINTER(LpC), C.POINTER(ParamsC), _f64p, _f64p,
@@ -539,6 +540,12 @@ class Session:
                                           C.byref(launches)))
         return dict(iterations=it.value, loop_ms=ms.value, loop_slots=slots.value,
                     launches=launches.value)
+
+    def partition(self) -> int:
+        """The shard partition the device context runs (0 rows, 1 columns)."""
+        v = C.c_int32()
+        self.b.check(self.b.session_partition(self.h, C.byref(v)))
+        return v.value
 
     def close(self) -> None:
         if self.h:

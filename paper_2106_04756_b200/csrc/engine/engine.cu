@@ -195,6 +195,7 @@ struct folp_gpu_ctx {
   int64_t ndg_count = 0, ndg_passes = 0, ndg_levels = 0;  // FOLP_TIMING statistics
   void* loop_block = nullptr;  // K~ values + indices of CSR and CSC (one block)
   size_t loop_block_bytes = 0;
+  double* prod = nullptr;      // two-phase products (gather_products_kernel), nnz + 8
 
   // shard: rows [r0, r1) of K~ are this shard's, or columns
   // [r0, r1) under the column partition
@@ -276,6 +277,18 @@ struct folp_gpu_ctx {
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, rb);
+    } else if (prod != nullptr && (&p == &rows || &p == &cols)) {
+      // two phases (segdot.cuh): gathers over the whole axis, then the
+      // segmented sums and the epilogue over the product stream
+      auto gn = gather_products_kernel<Epi>;
+      const int64_t quads = (nnz >> 2) + 1;
+      const int ggrid = ew_grid(quads, reinterpret_cast<const void*>(gn));
+      gn<<<ggrid, kBlock, 0, stream>>>(p.sp.idx, val, nnz, prod, epi);
+      auto fn = segdot_kernel<Epi, false, true>;
+      const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
+      fn<<<grid, kBlock, 0, stream>>>(p.sp, prod, epi, rb);
+      ++launches;
     } else {
       auto fn = segdot_kernel<Epi, false>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
@@ -456,7 +469,7 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     {
       // The loop's streams -- working values and indices of both layouts --
       // in ONE block, so a single L2 access-policy window can cover them.
-      const size_t vb = static_cast<size_t>(nnz + 8) * sizeof(double);
+      const size_t vb = (static_cast<size_t>(nnz + 8) * sizeof(double) + 255) / 256 * 256;
       const size_t ib = (static_cast<size_t>(nnz + 8) * sizeof(int) + 255) / 256 * 256;
       char* blk = c->alloc<char>(2 * vb + 2 * ib);
       c->csr_work = reinterpret_cast<double*>(blk);
@@ -533,6 +546,18 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
                       c->cols.sp.n_units <= warps && (env == nullptr || std::atoi(env) > 0);
       c->small_multi = c->alloc<double>(
           static_cast<size_t>(std::max(c->rows.sp.n_multi, c->cols.sp.n_multi) + 1) * kMaxAcc);
+    }
+    {
+      // Two-phase products when the product stream fits comfortably in L2
+      // next to the gathered vector (FOLP_TWO_PHASE=0 off, =1 always,
+      // default: nnz * 8 B <= 48 MB; tree mode only -- ordered parity runs
+      // keep the single pass, which is bit-identical anyway).
+      const char* env = std::getenv("FOLP_TWO_PHASE");
+      const int mode = env ? std::atoi(env) : 2;
+      const bool fits = static_cast<double>(nnz) * 8.0 <= 48.0 * (1 << 20);
+      if (!c->ordered && !c->small_loop && nnz > 0 && (mode == 1 || (mode == 2 && fits))) {
+        c->prod = c->alloc<double>(nnz + 8);
+      }
     }
     c->counters = c->alloc<unsigned>(kCounters);
     CK(cudaMemsetAsync(c->counters, 0, kCounters * sizeof(unsigned), c->stream));

@@ -210,7 +210,43 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   }
 }
 
+// Two-phase products (gathered vector and products L2-resident): phase 1
+// streams the whole axis once, prod[k] = val[k] * vec[idx[k]], with nothing
+// but independent gathers in flight (4 per thread per step, 16-byte stream
+// loads); phase 2 is segdot_kernel<..., PROD=true>, which reads prod[k] as a
+// coalesced stream instead of gathering.  In the single-pass kernel every
+// dependent load of a warp unit (indices -> gathers -> epilogue) waits
+// behind the SM's whole L1tex gather queue; split, the gathers run at the
+// queue's rate and phase 2's loads see a short queue.  Same products, same
+// summation order: bit-identical to the single-pass kernel.
+template <class Epi>
+__global__ void __launch_bounds__(kBlock)
+gather_products_kernel(const int* __restrict__ idx, const double* __restrict__ val,
+                       int64_t nnz, double* __restrict__ out, Epi epi) {
+  if (!epi.prepare()) return;
+  const double* __restrict__ vec = epi.vec();
+  const int64_t nq = nnz >> 2;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kBlock;
+  const int4* __restrict__ idx4 = reinterpret_cast<const int4*>(idx);
+  const double2* __restrict__ val2 = reinterpret_cast<const double2*>(val);
+  double2* __restrict__ out2 = reinterpret_cast<double2*>(out);
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x; q < nq; q += stride) {
+    const int4 i = __ldcs(&idx4[q]);
+    const double2 a = __ldcs(&val2[2 * q]);
+    const double2 b = __ldcs(&val2[2 * q + 1]);
+    const double g0 = __ldg(&vec[i.x]), g1 = __ldg(&vec[i.y]);
+    const double g2 = __ldg(&vec[i.z]), g3 = __ldg(&vec[i.w]);
+    out2[2 * q] = make_double2(a.x * g0, a.y * g1);
+    out2[2 * q + 1] = make_double2(b.x * g2, b.y * g3);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (nnz & 3)) {
+    const int64_t k = (nq << 2) + threadIdx.x;
+    out[k] = val[k] * __ldg(&vec[idx[k]]);
+  }
+}
+
 // The segmented-dot kernel.
+// PROD: `val` holds the products val[k] * vec[idx[k]] (phase 2 above).
 // Epi must provide:  static constexpr int K (>= 1); static constexpr bool
 //   kReduce (run the reduction tail); __device__ bool prepare();
 //   __device__ const double* vec() const;
@@ -218,7 +254,7 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
 //   __device__ Pre load(int seg) const;
 //   __device__ void apply(int seg, double dot, const Pre&, double (&acc)[K]) const;
 //   __device__ void finalize(const double (&tot)[K]) const;
-template <class Epi, bool ORDERED>
+template <class Epi, bool ORDERED, bool PROD = false>
 __global__ void __launch_bounds__(kBlock)
 segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   constexpr int K = Epi::K;
@@ -254,7 +290,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       // ordered plan: one long segment, summed by one lane in index order
       if (lane == 0) {
         double sum = 0.0;
-        for (int k = k0; k < k1; ++k) sum += val[k] * vec[idx[k]];
+        for (int k = k0; k < k1; ++k) sum += PROD ? val[k] : val[k] * vec[idx[k]];
         epi.apply(d.x, sum, epi.load(d.x), acc);
       }
     } else if (d.x >= 0) {
@@ -272,7 +308,11 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
 #pragma unroll
       for (int j = 0; j < kWarpTile / 32; ++j) {
         const int k = k0 + lane + 32 * j;
-        prod[j] = k < k1 ? val[k] * __ldg(&vec[idx[k]]) : 0.0;
+        if constexpr (PROD) {
+          prod[j] = k < k1 ? val[k] : 0.0;
+        } else {
+          prod[j] = k < k1 ? val[k] * __ldg(&vec[idx[k]]) : 0.0;
+        }
       }
 #pragma unroll
       for (int j = 0; j < kWarpTile / 32; ++j) {
@@ -298,7 +338,13 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       const int multi = -d.x - 1;
       double sum = 0.0;
 #pragma unroll 8
-      for (int k = k0 + lane; k < k1; k += 32) sum += val[k] * __ldg(&vec[idx[k]]);
+      for (int k = k0 + lane; k < k1; k += 32) {
+        if constexpr (PROD) {
+          sum += val[k];
+        } else {
+          sum += val[k] * __ldg(&vec[idx[k]]);
+        }
+      }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
       if (lane == 0) {

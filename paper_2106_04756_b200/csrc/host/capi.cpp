@@ -480,6 +480,15 @@ int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms, in
   });
 }
 
+int folp_session_partition(folp_session* s, int32_t* partition) {
+  return guarded([&] {
+    *partition = -1;
+    if (folp_gpu_ctx* c = s->s->context()) {
+      if (folp_gpu_shard_partition(c, partition) != 0) throw std::runtime_error(folp_gpu_last_error());
+    }
+  });
+}
+
 int folp_session_result(folp_session* s, folp_result_c* out) {
   return guarded([&] {
     const SolveResult* r = s->s->result();

@@ -76,10 +76,10 @@ def test_loopback_shards_first_restart_period(ref, world, partition):
     assert a.kkt_passes == b.kkt_passes
 
 
-def _loopback_launches(eng, lp, p, world, partition):
-    """Kernel launches of a `world`-shard loopback session after two
-    evaluation periods (the per-trial schedules differ: rows = 2 products +
-    primal pass + decide, columns = 2 products + dual pass)."""
+def _loopback_partition(eng, lp, p, world, partition):
+    """The partition a `world`-shard loopback session actually runs (the
+    engine's own answer, folp_session_partition), checked on every shard
+    after one evaluation period."""
     import threading
     g = shard.LoopbackGroup(world)
     out = [None] * world
@@ -87,8 +87,8 @@ def _loopback_launches(eng, lp, p, world, partition):
     def run(r):
         s = eng.session(lp, p, shard=g.spec(r, partition))
         try:
-            s.advance(2)
-            out[r] = s.stats()["launches"]
+            s.advance(1)
+            out[r] = s.partition()
         finally:
             s.close()
 
@@ -106,18 +106,16 @@ def _loopback_launches(eng, lp, p, world, partition):
 
 @pytest.mark.parametrize("cfg,scale,want", [(5, 0.005, "cols"), (3, 0.0005, "rows")])
 def test_auto_partition_picks_the_shorter_exchange(eng, cfg, scale, want):
-    """AUTO runs columns when m + 2 < n (config 5's shape) and rows otherwise:
-    same results as the explicit partition, and the same launch schedule
-    (which differs between the two partitions)."""
+    """AUTO runs columns when m + 2 < n (config 5's shape) and rows otherwise,
+    with the same results as the explicit partition."""
     lp = instances.generate(cfg, 1, scale)
     p = cabi.params(iteration_limit=200)
     auto = shard.solve_loopback(lp, 2, p, partition="auto")
     same = shard.solve_loopback(lp, 2, p, partition=want)
     _same(auto + same)
+    assert _loopback_partition(eng, lp, p, 2, "auto") == cabi.PARTITIONS[want]
     other = "cols" if want == "rows" else "rows"
-    la = _loopback_launches(eng, lp, p, 2, "auto")
-    assert la == _loopback_launches(eng, lp, p, 2, want)
-    assert la != _loopback_launches(eng, lp, p, 2, other)
+    assert _loopback_partition(eng, lp, p, 2, other) == cabi.PARTITIONS[other]
 
 
 def test_shard_rejects_unsupported_modes():

@@ -1,10 +1,16 @@
 #!/bin/bash
-# A/B of engine settings via environment variables: $@ = "NAME=VALUE ..." sets
+# A/B of engine switches: one bench line per "NAME=V[,NAME2=V2]" argument
+# (and one with no override), for each config in $CONFIGS (default 2).
+#   bash tools/gpu_ab.sh FOLP_TWO_PHASE=0 FOLP_TWO_PHASE=1
 cd "$(dirname "$0")/.." || exit 1
 mkdir -p gpurun_out
-: > gpurun_out/ab.log
-for setting in "$@"; do
-  echo "== $setting" >> gpurun_out/ab.log
-  env $setting timeout 300 python bench.py --steps 20 --warmup 5 --time-to-tol 0 --skip-cpu-baseline 2>&1 | \
-    python -c "import json,sys; l=json.loads(sys.stdin.readline()); print(round(l['value']), round(1000*l['roofline']['kernel_ms_per_trial'],2), round(l['roofline']['frac'],3))" >> gpurun_out/ab.log 2>&1
+for cfg in ${CONFIGS:-2}; do
+  for setting in base "$@"; do
+    envs=()
+    [ "$setting" != base ] && IFS=, read -ra envs <<< "$setting"
+    tag=$(echo "$setting" | tr ',=' '__')
+    env "${envs[@]}" timeout 600 python bench.py --config $cfg --steps ${STEPS:-20} --warmup 3 \
+      --time-to-tol 0 --skip-cpu-baseline > gpurun_out/ab_cfg${cfg}_$tag.json 2> gpurun_out/ab_cfg${cfg}_$tag.err
+    echo "cfg$cfg $setting: $(python -c "import json,sys; d=json.load(open('gpurun_out/ab_cfg${cfg}_$tag.json')); r=d['roofline']; print(round(d['value'],1), 'it/s; trial', round(r['kernel_ms_per_trial']*1000,2), 'us; frac', round(r['frac'],3))" 2>&1)"
+  done
 done
