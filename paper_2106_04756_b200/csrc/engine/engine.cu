@@ -219,6 +219,7 @@ struct folp_gpu_ctx {
   cudaGraphExec_t chunk_exec[3] = {nullptr, nullptr, nullptr};  // per step policy
   bool graph_tried[3] = {false, false, false};
   bool graph_ok[3] = {false, false, false};
+  int body_slots[3] = {1, 1, 1};  // trial slots per WHILE-body iteration
   int64_t launches = 0;
   bool profiling = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
@@ -266,6 +267,28 @@ struct folp_gpu_ctx {
   }
   RedBuf red(int counter) { return RedBuf{partials, counters + counter, nullptr, 0}; }
 
+  // Launch of a segdot kernel; with `pdl` (the PDHG loop's products, see
+  // segdot.cuh griddep_wait) as a programmatic dependent launch.
+  bool pdl = false;
+  template <class Epi, bool ORD, bool PR>
+  void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb) {
+    auto fn = segdot_kernel<Epi, ORD, PR>;
+    if (!pdl) {
+      fn<<<grid, kBlock, 0, stream>>>(sp, val, epi, rb);
+      return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, fn, sp, val, epi, rb));
+  }
+
   template <class Epi>
   void seg(const PlanDev& p, const double* val, const Epi& epi, int counter, int region = 1) {
     RedBuf rb = red(counter);
@@ -276,7 +299,7 @@ struct folp_gpu_ctx {
       auto fn = segdot_kernel<Epi, true>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
-      fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, rb);
+      launch_segdot<Epi, true, false>(grid, p.sp, val, epi, rb);
     } else if (prod != nullptr && (&p == &rows || &p == &cols)) {
       // two phases (segdot.cuh): gathers over the whole axis, then the
       // segmented sums and the epilogue over the product stream
@@ -287,13 +310,13 @@ struct folp_gpu_ctx {
       auto fn = segdot_kernel<Epi, false, true>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
-      fn<<<grid, kBlock, 0, stream>>>(p.sp, prod, epi, rb);
+      launch_segdot<Epi, false, true>(grid, p.sp, prod, epi, rb);
       ++launches;
     } else {
       auto fn = segdot_kernel<Epi, false>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
-      fn<<<grid, kBlock, 0, stream>>>(p.sp, val, epi, rb);
+      launch_segdot<Epi, false, false>(grid, p.sp, val, epi, rb);
     }
     ++launches;
     CK(cudaGetLastError());
@@ -548,12 +571,11 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
           static_cast<size_t>(std::max(c->rows.sp.n_multi, c->cols.sp.n_multi) + 1) * kMaxAcc);
     }
     {
-      // Two-phase products when the product stream fits comfortably in L2
-      // next to the gathered vector (FOLP_TWO_PHASE=0 off, =1 always,
-      // default: nnz * 8 B <= 48 MB; tree mode only -- ordered parity runs
-      // keep the single pass, which is bit-identical anyway).
+      // Two-phase products (FOLP_TWO_PHASE=1 always, =2 when the product
+      // stream fits L2 next to the gathered vector; default off: measured
+      // 1.6x slower on config 2 -- profiles/r1_two_phase.md; tree mode only).
       const char* env = std::getenv("FOLP_TWO_PHASE");
-      const int mode = env ? std::atoi(env) : 2;
+      const int mode = env ? std::atoi(env) : 0;
       const bool fits = static_cast<double>(nnz) * 8.0 <= 48.0 * (1 << 20);
       if (!c->ordered && !c->small_loop && nnz > 0 && (mode == 1 || (mode == 2 && fits))) {
         c->prod = c->alloc<double>(nnz + 8);
@@ -1002,7 +1024,9 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     if (c->profiling) CK(cudaEventRecord(c->ev1, c->stream));
     c->pull_state();
     if (!c->sharded() && !(c->small_loop && policy != FOLP_STEP_MALITSKY_POCK)) {
-      c->launches += per_slot * st->slots;
+      // graph: whole body iterations (a stopped slot still launches, and exits)
+      const int64_t bs = c->graph_ok[policy] ? c->body_slots[policy] : 1;
+      c->launches += per_slot * ((st->slots + bs - 1) / bs) * bs;
     }
     if (policy == FOLP_STEP_MALITSKY_POCK) c->kx_valid = false;  // Kx cache not kept
     if (c->profiling) {

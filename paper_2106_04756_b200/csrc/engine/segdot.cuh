@@ -254,10 +254,42 @@ gather_products_kernel(const int* __restrict__ idx, const double* __restrict__ v
 //   __device__ Pre load(int seg) const;
 //   __device__ void apply(int seg, double dot, const Pre&, double (&acc)[K]) const;
 //   __device__ void finalize(const double (&tot)[K]) const;
+// Programmatic dependent launch (the PDHG loop's kernels, FOLP_PDL): a
+// kernel launched with programmatic stream serialization starts while its
+// predecessor drains; griddepcontrol.wait blocks until the predecessor grid
+// has completed and its memory is visible (a no-op without the attribute).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// L2 prefetch of a warp unit's static streams (values, indices, segment
+// bounds): issued before griddep_wait, so the first unit's stream loads
+// overlap the predecessor's tail.
+__device__ __forceinline__ void prefetch_unit(const SegPlan& p, const double* val, int4 d, int lane) {
+  const int k0 = d.z, k1 = d.w;
+  if (k1 <= k0) return;
+  const char* vb = reinterpret_cast<const char*>(val + k0);
+  const char* ib = reinterpret_cast<const char*>(p.idx + k0);
+  const int vlines = ((k1 - k0) * 8 + 127) / 128 + 1;
+  const int ilines = ((k1 - k0) * 4 + 127) / 128 + 1;
+  if (lane < vlines && lane < 20) asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + 128 * lane));
+  if (lane >= 20 && lane - 20 < ilines && lane < 30) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ib + 128 * (lane - 20)));
+  }
+  if (lane == 31 && d.x >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ptr + d.x));
+}
+
 template <class Epi, bool ORDERED, bool PROD = false>
 __global__ void __launch_bounds__(kBlock)
 segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   constexpr int K = Epi::K;
+  {
+    const int u0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (u0 < p.n_units) prefetch_unit(p, val, p.units[u0], threadIdx.x & 31);
+  }
+  griddep_wait();
+  griddep_launch();            // the successor may start filling freed SMs
   if (!epi.prepare()) return;  // loop slot disabled: every CTA agrees
   const double* __restrict__ vec = epi.vec();
   const int* __restrict__ idx = p.idx;

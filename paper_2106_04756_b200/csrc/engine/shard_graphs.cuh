@@ -114,9 +114,28 @@ void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
     c->seg(c->rows, c->csr_work, EpiMpDual{b}, 3, 1);
     c->seg(c->cols, c->csc_work, EpiMpCheck{b}, 6, 0);
   } else {
-    axis_product(c, false, true, EpiPrimal{b}, 2, 0);
-    axis_product(c, true, true, EpiDual{b}, 3, 1);
+    // programmatic dependent launches: each product starts while the
+    // previous one drains (FOLP_PDL=0 disables)
+    const char* env = std::getenv("FOLP_PDL");
+    c->pdl = env == nullptr || std::atoi(env) > 0;
+    try {
+      axis_product(c, false, true, EpiPrimal{b}, 2, 0);
+      axis_product(c, true, true, EpiDual{b}, 3, 1);
+    } catch (...) {
+      c->pdl = false;
+      throw;
+    }
+    c->pdl = false;
   }
+}
+
+// Trial slots per iteration of the chunk graph's WHILE body: a slot whose
+// loop already stopped is a pair of early-exit launches, and within the
+// body the products chain by programmatic dependent launches
+// (FOLP_BODY_SLOTS, default 2).
+int body_slots() {
+  const char* env = std::getenv("FOLP_BODY_SLOTS");
+  return env ? std::max(1, std::atoi(env)) : 2;
 }
 
 // Builds the chunk graph of a policy: WHILE(running) { trial slot }.
@@ -145,7 +164,9 @@ void build_chunk_graph(folp_gpu_ctx* c, int policy) {
       const LoopBufs b = c->loop_bufs(handle, 1);
       const int64_t before = c->launches;
       try {
-        launch_slot(c, policy, b);
+        const int reps = policy == FOLP_STEP_MALITSKY_POCK ? 1 : body_slots();
+        for (int r = 0; r < reps; ++r) launch_slot(c, policy, b);
+        c->body_slots[policy] = reps;
       } catch (...) {
         ok = false;
       }
