@@ -211,6 +211,9 @@ int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms,
 /* The shard partition the session's device context runs (0 rows, 1 columns;
  * rows for an unsharded one), -1 before a device context exists. */
 int folp_session_partition(folp_session* s, int32_t* partition);
+/* The session's device context (include/folp_gpu.h), NULL before one exists
+ * (diagnostics: folp_gpu_debug_warp_times). */
+struct folp_gpu_ctx* folp_session_context(folp_session* s);
 int folp_session_result(folp_session* s, folp_result_c* out);
 void folp_session_destroy(folp_session* s);
 

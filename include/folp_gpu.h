@@ -242,6 +242,10 @@ int32_t folp_gpu_reduction_ordered(const folp_gpu_ctx* ctx);
 
 /* Kernel launches issued by this context so far (for bench accounting). */
 int64_t folp_gpu_launch_count(const folp_gpu_ctx* ctx);
+/* Diagnostic builds only (-DFOLP_WARP_TIMES): per-warp globaltimer stamps
+ * {start, units done, exit} of the most recent kernel A (slot 0) or B
+ * (slot 1) launch, `max_warps` x 3 values; FOLP_E_ARG otherwise. */
+int folp_gpu_debug_warp_times(folp_gpu_ctx* ctx, int32_t slot, uint64_t* out, int32_t max_warps);
 
 /* Device time of the fused step kernels (kernel A + kernel B of every trial
  * slot) summed over all chunks since profiling was (re)enabled, measured

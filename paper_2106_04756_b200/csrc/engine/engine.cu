@@ -1146,6 +1146,21 @@ int folp_gpu_max_abs_entry(folp_gpu_ctx* c, int32_t working, double* out) {
 
 int64_t folp_gpu_launch_count(const folp_gpu_ctx* c) { return c->launches; }
 
+int folp_gpu_debug_warp_times(folp_gpu_ctx* c, int32_t slot, uint64_t* out, int32_t max_warps) {
+  return guarded([&] {
+#ifdef FOLP_WARP_TIMES
+    if (slot < 0 || slot > 1 || max_warps < 0) throw std::invalid_argument("debug_warp_times: slot");
+    const int w = std::min(max_warps, kTraceWarps);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyFromSymbol(out, g_warp_times, static_cast<size_t>(w) * 3 * sizeof(uint64_t),
+                            static_cast<size_t>(slot) * kTraceWarps * 3 * sizeof(uint64_t)));
+#else
+    (void)c; (void)slot; (void)out; (void)max_warps;
+    throw std::invalid_argument("debug_warp_times: build with -DFOLP_WARP_TIMES");
+#endif
+  });
+}
+
 void folp_gpu_set_default_reduction(int32_t ordered) { g_default_ordered = ordered != 0; }
 
 int32_t folp_gpu_reduction_ordered(const folp_gpu_ctx* c) { return c->ordered ? 1 : 0; }

@@ -106,6 +106,7 @@ struct LoopBufs {
 struct EpiPrimal {
   static constexpr int K = 2;
   static constexpr bool kReduce = true;
+  static constexpr int kTrace = 0;  // FOLP_WARP_TIMES slot
   LoopBufs b;
   const double* xc;
   double* xn;
@@ -231,6 +232,7 @@ __device__ __forceinline__ void decide_trial(const LoopBufs& b, double cross, do
 struct EpiDual {
   static constexpr int K = 3;
   static constexpr bool kReduce = true;
+  static constexpr int kTrace = 1;  // FOLP_WARP_TIMES slot
   LoopBufs b;
   const double* yc;
   double* yn;

@@ -280,6 +280,36 @@ __device__ __forceinline__ void prefetch_unit(const SegPlan& p, const double* va
   if (lane == 31 && d.x >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ptr + d.x));
 }
 
+// Per-warp timeline of the loop products (diagnostic build, -DFOLP_WARP_TIMES):
+// globaltimer at warp start, after its last unit, and at kernel exit, for
+// the most recent launch of each traced epilogue (Epi::kTrace = 0 / 1).
+constexpr int kTraceWarps = 16384;
+#ifdef FOLP_WARP_TIMES
+__device__ unsigned long long g_warp_times[2][kTraceWarps][3];
+#endif
+template <class E, class = void>
+struct TraceSlot { static constexpr int v = -1; };
+template <class E>
+struct TraceSlot<E, std::void_t<decltype(E::kTrace)>> { static constexpr int v = E::kTrace; };
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+template <class Epi>
+__device__ __forceinline__ void trace_warp(int which, unsigned long long t) {
+#ifdef FOLP_WARP_TIMES
+  constexpr int slot = TraceSlot<Epi>::v;
+  if constexpr (slot >= 0) {
+    const int w = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0 && w < kTraceWarps) g_warp_times[slot][w][which] = t;
+  }
+#else
+  (void)which;
+  (void)t;
+#endif
+}
+
 template <class Epi, bool ORDERED, bool PROD = false>
 __global__ void __launch_bounds__(kBlock)
 segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
@@ -291,6 +321,9 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   griddep_wait();
   griddep_launch();            // the successor may start filling freed SMs
   if (!epi.prepare()) return;  // loop slot disabled: every CTA agrees
+#ifdef FOLP_WARP_TIMES
+  trace_warp<Epi>(0, global_ns());
+#endif
   const double* __restrict__ vec = epi.vec();
   const int* __restrict__ idx = p.idx;
   const int* __restrict__ ptr = p.ptr;
@@ -402,6 +435,9 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       }
     }
   }
+#ifdef FOLP_WARP_TIMES
+  trace_warp<Epi>(1, global_ns());
+#endif
   if constexpr (Epi::kReduce) {
     if constexpr (ORDERED) {
       ordered_tail(epi, rb);
@@ -409,6 +445,9 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       reduce_tail(epi, acc.v, rb, p.n_multi);
     }
   }
+#ifdef FOLP_WARP_TIMES
+  trace_warp<Epi>(2, global_ns());
+#endif
 }
 
 // A warp's unit of one plan held in registers for a whole chunk (small

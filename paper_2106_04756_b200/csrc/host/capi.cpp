@@ -480,6 +480,8 @@ int folp_session_stats(folp_session* s, int64_t* iterations, double* loop_ms, in
   });
 }
 
+folp_gpu_ctx* folp_session_context(folp_session* s) { return s ? s->s->context() : nullptr; }
+
 int folp_session_partition(folp_session* s, int32_t* partition) {
   return guarded([&] {
     *partition = -1;
