@@ -1154,6 +1154,10 @@ int folp_gpu_debug_warp_times(folp_gpu_ctx* c, int32_t slot, uint64_t* out, int3
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpyFromSymbol(out, g_warp_times, static_cast<size_t>(w) * 3 * sizeof(uint64_t),
                             static_cast<size_t>(slot) * kTraceWarps * 3 * sizeof(uint64_t)));
+    if (max_warps > kTraceWarps) {  // + the last CTA's tail stamps
+      CK(cudaMemcpyFromSymbol(out + 3 * kTraceWarps, g_tail_times, 3 * sizeof(uint64_t),
+                              static_cast<size_t>(slot) * 4 * sizeof(uint64_t)));
+    }
 #else
     (void)c; (void)slot; (void)out; (void)max_warps;
     throw std::invalid_argument("debug_warp_times: build with -DFOLP_WARP_TIMES");

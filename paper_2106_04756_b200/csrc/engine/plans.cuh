@@ -13,7 +13,6 @@ double tile_segs_cutoff() {
 // the longer ones, in index order.
 void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
                 const int* d_ptr, const int* d_idx, PlanDev& out, int64_t s_begin = 0) {
-  (void)nnz;
   const bool ordered = c->ordered;
   // segments per tile: tree mode caps it when segments are very short (a
   // lane then owns several segments, and every extra round waits behind the
@@ -26,6 +25,17 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
     } else if (mean < tile_segs_cutoff()) {
       max_segs = 64;
     }
+  }
+  // tree mode, large axes: segments longer than the serial cap are summed by
+  // a warp (one "single part" unit, epilogue into the warp's accumulators)
+  // instead of by one lane -- a lane walking up to 256 products in sequence
+  // made the slowest warp of a power-law axis 40 % slower than the median
+  // (tools/warp_timeline.py).  FOLP_SERIAL_CAP overrides (256 = off).  Not
+  // for small axes, whose plans may run in k_chunk_cluster.
+  int64_t serial_cap = kWarpTile;
+  if (!ordered && nnz > (int64_t(1) << 20)) {
+    const char* env = std::getenv("FOLP_SERIAL_CAP");
+    serial_cap = std::min<int64_t>(kWarpTile, std::max<int64_t>(1, env ? std::atoi(env) : kSerialCap));
   }
   std::vector<int4> units;
   std::vector<int> multi_seg, multi_parts;
@@ -40,6 +50,12 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   };
   for (int64_t s = s_begin; s < S; ++s) {
     const int64_t len = ptr[s + 1] - ptr[s];
+    if (len > serial_cap && len <= kWarpTile) {
+      close(s);
+      units.push_back(make_int4(-1, -static_cast<int>(s) - 2, static_cast<int>(ptr[s]),
+                                static_cast<int>(ptr[s + 1])));
+      continue;
+    }
     if (len <= kWarpTile) {
       if (seg0 >= 0 && (tile_nnz + len > kWarpTile || s - seg0 >= max_segs)) close(s);
       if (seg0 < 0) seg0 = s;

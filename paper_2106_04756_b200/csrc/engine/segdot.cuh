@@ -23,6 +23,9 @@
 //          reference's own order (sparse_matrix.cpp:112-118), so these dots
 //          are bit-identical -- and runs the epilogue with operands it loaded
 //          before the gathers.
+//   single part {-1, -(seg+2), k0, k1}: tree mode, a segment longer than
+//          the serial cap (plans.cuh), reduced by the warp; its epilogue
+//          feeds the warp's own accumulators (no slot, no arrival).
 //   part : a fixed chunk (kWarpTile entries; kGiantPart for giant segments)
 //          of a longer segment, reduced by the warp.  The last part of a
 //          segment to arrive sums the part sums in part order and runs the
@@ -47,6 +50,7 @@ constexpr int kWarpTile = 256;        // nonzeros per tile / part (8 per lane)
 constexpr int kGiantMin = 65536;      // segments above this use kGiantPart parts
 constexpr int kGiantPart = 2048;      // nnz per part of a giant segment
 constexpr int kMaxAcc = 30;           // widest reduction (bisection pass)
+constexpr int kSerialCap = 256;       // tree mode: longest segment one lane sums
 
 // std::max / std::min semantics (NaN in `a` propagates), which the
 // reference's projections rely on for its NonFiniteIterate detection.
@@ -176,6 +180,48 @@ __device__ __forceinline__ void ordered_tail(const Epi& epi, RedBuf rb) {
   }
 }
 
+// Per-warp timeline of the loop products (diagnostic build, -DFOLP_WARP_TIMES):
+// globaltimer at warp start, after its last unit, and at kernel exit, for
+// the most recent launch of each traced epilogue (Epi::kTrace = 0 / 1).
+constexpr int kTraceWarps = 16384;
+#ifdef FOLP_WARP_TIMES
+__device__ unsigned long long g_warp_times[2][kTraceWarps][3];
+__device__ unsigned long long g_tail_times[2][4];  // last CTA: ticket, sums, finalize, end
+#endif
+template <class E, class = void>
+struct TraceSlot { static constexpr int v = -1; };
+template <class E>
+struct TraceSlot<E, std::void_t<decltype(E::kTrace)>> { static constexpr int v = E::kTrace; };
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+template <class Epi>
+__device__ __forceinline__ void trace_tail(int which) {
+#ifdef FOLP_WARP_TIMES
+  constexpr int slot = TraceSlot<Epi>::v;
+  if constexpr (slot >= 0) {
+    if (threadIdx.x == 0) g_tail_times[slot][which] = global_ns();
+  }
+#else
+  (void)which;
+#endif
+}
+template <class Epi>
+__device__ __forceinline__ void trace_warp(int which, unsigned long long t) {
+#ifdef FOLP_WARP_TIMES
+  constexpr int slot = TraceSlot<Epi>::v;
+  if constexpr (slot >= 0) {
+    const int w = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0 && w < kTraceWarps) g_warp_times[slot][w][which] = t;
+  }
+#else
+  (void)which;
+  (void)t;
+#endif
+}
+
 // Per-block partial + last-block-done final reduction, then epi.finalize().
 template <class Epi>
 __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K], RedBuf rb,
@@ -194,6 +240,7 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   }
   __syncthreads();
   if (!s_last) return;
+  trace_tail<Epi>(0);
   __threadfence();
   const int np = static_cast<int>(gridDim.x) + n_extra;
   double part[K];
@@ -204,8 +251,10 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
     for (int k = 0; k < K; ++k) part[k] += ld_cg(&rb.partials[i * K + k]);
   }
   block_sum_vec<K>(part, s_vec, tot);
+  trace_tail<Epi>(1);
   if (threadIdx.x == 0) {
     epi.finalize(tot);
+    trace_tail<Epi>(2);
     *rb.counter = 0u;
   }
 }
@@ -278,36 +327,6 @@ __device__ __forceinline__ void prefetch_unit(const SegPlan& p, const double* va
     asm volatile("prefetch.global.L2 [%0];" ::"l"(ib + 128 * (lane - 20)));
   }
   if (lane == 31 && d.x >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ptr + d.x));
-}
-
-// Per-warp timeline of the loop products (diagnostic build, -DFOLP_WARP_TIMES):
-// globaltimer at warp start, after its last unit, and at kernel exit, for
-// the most recent launch of each traced epilogue (Epi::kTrace = 0 / 1).
-constexpr int kTraceWarps = 16384;
-#ifdef FOLP_WARP_TIMES
-__device__ unsigned long long g_warp_times[2][kTraceWarps][3];
-#endif
-template <class E, class = void>
-struct TraceSlot { static constexpr int v = -1; };
-template <class E>
-struct TraceSlot<E, std::void_t<decltype(E::kTrace)>> { static constexpr int v = E::kTrace; };
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-template <class Epi>
-__device__ __forceinline__ void trace_warp(int which, unsigned long long t) {
-#ifdef FOLP_WARP_TIMES
-  constexpr int slot = TraceSlot<Epi>::v;
-  if constexpr (slot >= 0) {
-    const int w = blockIdx.x * kWarps + (threadIdx.x >> 5);
-    if ((threadIdx.x & 31) == 0 && w < kTraceWarps) g_warp_times[slot][w][which] = t;
-  }
-#else
-  (void)which;
-  (void)t;
-#endif
 }
 
 template <class Epi, bool ORDERED, bool PROD = false>
@@ -401,6 +420,9 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
     } else if constexpr (!ORDERED) {
       // ---------------- part of a long segment ----------------
       const int multi = -d.x - 1;
+      const bool single = d.y < 0;
+      typename Epi::Pre pre_single{};
+      if (single && lane == 0) pre_single = epi.load(-d.y - 2);  // in flight with the gathers
       double sum = 0.0;
 #pragma unroll 8
       for (int k = k0 + lane; k < k1; k += 32) {
@@ -412,7 +434,9 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
-      if (lane == 0) {
+      if (single) {
+        if (lane == 0) epi.apply(-d.y - 2, sum, pre_single, acc);
+      } else if (lane == 0) {
         p.part_sums[u] = sum;
         __threadfence();
         const int np = p.multi_parts[multi];

@@ -32,8 +32,11 @@ def main():
     ctx = lib.folp_session_context(s.h)
     W = 16384
     for slot, name in [(0, "A (K'y, primal)"), (1, "B (K x', dual)")]:
-        buf = np.zeros(W * 3, dtype=np.uint64)
-        rc = lib.folp_gpu_debug_warp_times(ctx, slot, buf.ctypes.data_as(C.POINTER(C.c_uint64)), W)
+        buf = np.zeros(W * 3 + 3, dtype=np.uint64)
+        rc = lib.folp_gpu_debug_warp_times(ctx, slot, buf.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                           W + 1)
+        tail = buf[3 * W:].astype(np.int64)
+        buf = buf[:3 * W]
         if rc != 0:
             print("debug_warp_times failed", rc)
             return
@@ -48,6 +51,8 @@ def main():
                        ("tail wait", ex - ud)]:
             print(f"  {lab:10s} " + "  ".join(f"p{p}={np.percentile(v, p):7.2f}" for p in q))
         busy = (ud - st).sum() / (len(st) * ex.max())
+        tl = (tail - t0) / 1e3
+        print(f"  last CTA: ticket {tl[0]:.2f}  sums {tl[1]:.2f}  finalize {tl[2]:.2f} us")
         print(f"  warp-busy fraction of (warps x span): {busy:.3f}")
     s.close()
 
