@@ -33,7 +33,7 @@ constexpr int kUnderflow = 4;
 constexpr double kStepSizeFloor = 1e-300;  // solver.cpp:31
 
 // Device-resident loop state.  Host mirrors it at chunk boundaries.
-struct DevState {
+struct alignas(8) DevState {
   int32_t running;   // slot kernels work only while 1
   int32_t status;
   int32_t cur;       // parity of the CURRENT buffers
@@ -67,6 +67,8 @@ struct DevState {
   double mp_dy_sq;   // ||dy||^2 of the current trial
   double mp_break, mp_down, mp_interp;
 };
+
+static_assert(sizeof(DevState) % 8 == 0, "DevState is copied as 8-byte words");
 
 // a[i] for i in {0, 1} without dynamic indexing (which would force the
 // parameter struct into local memory).
@@ -163,9 +165,10 @@ struct EpiPrimal {
 
 // The adaptive step-size rule (adaptive_step, solver.cpp:173-199) and the
 // loop bookkeeping, run by one thread once a trial's sums are known.
-__device__ __forceinline__ void decide_trial(const LoopBufs& b, double cross, double movement,
-                                             bool bad) {
-  DevState* st = b.st;
+// `st` is the device state or the last CTA's shared copy of it; `rg`, when
+// given, holds this trial's red / grow factors (loaded in parallel).
+__device__ __forceinline__ void decide_trial_on(const LoopBufs& b, DevState* st, double cross,
+                                                double movement, bool bad, const double* rg) {
   st->slots += 1;
   st->pending = 0.0;  // consumed by kernels A and B of this slot
   const double eta = st->eta;
@@ -181,8 +184,8 @@ __device__ __forceinline__ void decide_trial(const LoopBufs& b, double cross, do
     if (st->policy == 0) {
       const int64_t ki = st->k_total - st->k_chunk0;
       const double eta_bar = cross > 0.0 ? movement / (2.0 * cross) : INFINITY;
-      const double a = b.red[ki] * eta_bar;
-      const double g = b.grow[ki] * eta;
+      const double a = (rg ? rg[0] : b.red[ki]) * eta_bar;
+      const double g = (rg ? rg[1] : b.grow[ki]) * eta;
       eta_next = (g < a) ? g : a;  // std::min(a, g)
       accept = eta <= eta_bar;
     }
@@ -222,6 +225,10 @@ __device__ __forceinline__ void decide_trial(const LoopBufs& b, double cross, do
     }
   }
   if (b.use_cond) cudaGraphSetConditional(b.cond, st->running ? 1u : 0u);
+}
+__device__ __forceinline__ void decide_trial(const LoopBufs& b, double cross, double movement,
+                                             bool bad) {
+  decide_trial_on(b, b.st, cross, movement, bad, nullptr);
 }
 
 // Kernel B: K x' of the trial primal, fused dual projected step with the
@@ -286,6 +293,30 @@ struct EpiDual {
     double movement = tot[1] / st->omega;  // solver.cpp:83
     movement = movement + st->sx;
     decide_trial(b, tot[0], movement, st->bad_a != 0.0 || tot[2] != 0.0);
+  }
+  // the decision on the last CTA's shared copy of the state (segdot.cuh StateTail)
+  static constexpr int kStateWords = sizeof(DevState) / 8;
+  __device__ unsigned long long* state_words() const {
+    return reinterpret_cast<unsigned long long*>(b.st);
+  }
+  __device__ void tail_aux(double* rg) const {  // this trial's step factors
+    const DevState* st = b.st;
+    if (__ldcg(&st->policy) == 0) {
+      const int64_t ki = __ldcg(&st->k_total) - __ldcg(&st->k_chunk0);
+      rg[0] = b.red[ki];
+      rg[1] = b.grow[ki];
+    }
+  }
+  __device__ void finalize_state(const double (&tot)[K], unsigned long long* words,
+                                 const double* rg) const {
+    if (shard_out != nullptr) {
+      for (int k = 0; k < K; ++k) shard_out[k] = tot[k];
+      return;
+    }
+    DevState* st = reinterpret_cast<DevState*>(words);
+    double movement = tot[1] / st->omega;  // solver.cpp:83
+    movement = movement + st->sx;
+    decide_trial_on(b, st, tot[0], movement, st->bad_a != 0.0 || tot[2] != 0.0, rg);
   }
   __device__ void finalize_ordered(const double* t, int64_t m) const {
     const DevState* st = b.st;

@@ -222,6 +222,18 @@ __device__ __forceinline__ void trace_warp(int which, unsigned long long t) {
 #endif
 }
 
+// Epilogues whose finalize runs the loop's step decision on the device
+// state (EpiDual) expose it as kStateWords 8-byte words: the last CTA loads
+// them into shared memory with all its threads while it sums the partials,
+// decides on the shared copy and writes it back -- a dozen dependent global
+// round trips of one thread cost ~2.4 us per trial (tools/warp_timeline.py).
+template <class E, class = void>
+struct StateTail { static constexpr int words = 0; };
+template <class E>
+struct StateTail<E, std::void_t<decltype(E::kStateWords)>> {
+  static constexpr int words = E::kStateWords;
+};
+
 // Per-block partial + last-block-done final reduction, then epi.finalize().
 template <class Epi>
 __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K], RedBuf rb,
@@ -242,20 +254,49 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   if (!s_last) return;
   trace_tail<Epi>(0);
   __threadfence();
+  constexpr int SW = StateTail<Epi>::words;
+  __shared__ unsigned long long s_state[SW > 0 ? SW : 1];
+  __shared__ double s_rg[2];
+  if constexpr (SW > 0) {
+    if (threadIdx.x < SW) s_state[threadIdx.x] = __ldcg(epi.state_words() + threadIdx.x);
+    if (threadIdx.x == kBlock - 1) epi.tail_aux(s_rg);
+  }
   const int np = static_cast<int>(gridDim.x) + n_extra;
   double part[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) part[k] = 0.0;
-  for (int i = threadIdx.x; i < np; i += kBlock) {
+  // all of a thread's loads in flight at once (same per-thread order)
+  constexpr int R = K <= 2 ? 4 : 2;
+  for (int base = threadIdx.x; base < np; base += kBlock * R) {
+    double v[R][K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) part[k] += ld_cg(&rb.partials[i * K + k]);
+    for (int r = 0; r < R; ++r) {
+      const int i = base + r * kBlock;
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[r][k] = i < np ? ld_cg(&rb.partials[i * K + k]) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (base + r * kBlock < np) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) part[k] += v[r][k];
+      }
+    }
   }
   block_sum_vec<K>(part, s_vec, tot);
   trace_tail<Epi>(1);
   if (threadIdx.x == 0) {
-    epi.finalize(tot);
+    if constexpr (SW > 0) {
+      epi.finalize_state(tot, s_state, s_rg);
+    } else {
+      epi.finalize(tot);
+    }
     trace_tail<Epi>(2);
     *rb.counter = 0u;
+  }
+  if constexpr (SW > 0) {
+    __syncthreads();
+    if (threadIdx.x < SW) epi.state_words()[threadIdx.x] = s_state[threadIdx.x];
   }
 }
 
