@@ -59,6 +59,11 @@ __device__ __forceinline__ double ref_min(double a, double b) { return (b < a) ?
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+// Release / acquire fence at GPU scope for the last-arrival patterns (store;
+// fence; atomic ticket -- ticket; fence; loads).  __threadfence() is
+// fence.sc.gpu, a sequentially consistent fence the patterns do not need.
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // One warp unit: a tile {seg0, seg1, k0, k1} (seg0 >= 0) or a part
 // {-(multi+1), first_unit_of_segment, k0, k1} of multi-part segment `multi`.
 struct SegPlan {
@@ -246,14 +251,14 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) rb.partials[blockIdx.x * K + k] = tot[k];
-    __threadfence();
+    fence_acq_rel();
     const unsigned ticket = atomicAdd(rb.counter, 1u);
     s_last = (ticket == gridDim.x - 1) ? 1 : 0;
+    if (s_last) fence_acq_rel();  // acquire; the barrier below extends it to the CTA
   }
   __syncthreads();
   if (!s_last) return;
   trace_tail<Epi>(0);
-  __threadfence();
   constexpr int SW = StateTail<Epi>::words;
   __shared__ unsigned long long s_state[SW > 0 ? SW : 1];
   __shared__ double s_rg[2];
@@ -479,11 +484,11 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         if (lane == 0) epi.apply(-d.y - 2, sum, pre_single, acc);
       } else if (lane == 0) {
         p.part_sums[u] = sum;
-        __threadfence();
+        fence_acq_rel();
         const int np = p.multi_parts[multi];
         const unsigned arrived = atomicAdd(&p.arrivals[multi], 1u);
         if (arrived == static_cast<unsigned>(np - 1)) {
-          __threadfence();
+          fence_acq_rel();
           const int first = d.y;
           double total = 0.0;
           for (int q = 0; q < np; ++q) total += ld_cg(&p.part_sums[first + q]);
