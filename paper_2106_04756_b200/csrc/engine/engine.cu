@@ -1152,10 +1152,10 @@ int folp_gpu_debug_warp_times(folp_gpu_ctx* c, int32_t slot, uint64_t* out, int3
     if (slot < 0 || slot > 1 || max_warps < 0) throw std::invalid_argument("debug_warp_times: slot");
     const int w = std::min(max_warps, kTraceWarps);
     CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpyFromSymbol(out, g_warp_times, static_cast<size_t>(w) * 3 * sizeof(uint64_t),
-                            static_cast<size_t>(slot) * kTraceWarps * 3 * sizeof(uint64_t)));
+    CK(cudaMemcpyFromSymbol(out, g_warp_times, static_cast<size_t>(w) * 4 * sizeof(uint64_t),
+                            static_cast<size_t>(slot) * kTraceWarps * 4 * sizeof(uint64_t)));
     if (max_warps > kTraceWarps) {  // + the last CTA's tail stamps
-      CK(cudaMemcpyFromSymbol(out + 3 * kTraceWarps, g_tail_times, 3 * sizeof(uint64_t),
+      CK(cudaMemcpyFromSymbol(out + 4 * kTraceWarps, g_tail_times, 3 * sizeof(uint64_t),
                               static_cast<size_t>(slot) * 4 * sizeof(uint64_t)));
     }
 #else

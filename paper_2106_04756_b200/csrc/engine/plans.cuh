@@ -38,47 +38,121 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
     serial_cap = std::min<int64_t>(kWarpTile, std::max<int64_t>(1, env ? std::atoi(env) : kSerialCap));
   }
   std::vector<int4> units;
-  std::vector<int> multi_seg, multi_parts;
-  int64_t seg0 = -1, tile_nnz = 0;
-  auto close = [&](int64_t seg_end) {
-    if (seg0 >= 0 && seg_end > seg0) {
-      units.push_back(make_int4(static_cast<int>(seg0), static_cast<int>(seg_end),
-                                static_cast<int>(ptr[seg0]), static_cast<int>(ptr[seg_end])));
-    }
-    seg0 = -1;
-    tile_nnz = 0;
-  };
-  for (int64_t s = s_begin; s < S; ++s) {
-    const int64_t len = ptr[s + 1] - ptr[s];
-    if (len > serial_cap && len <= kWarpTile) {
+  std::vector<int> multi_seg, multi_parts, multi_first;
+  // One pass over the segments with tiles of at most `target` nonzeros.
+  auto build = [&](int64_t target) {
+    units.clear();
+    multi_seg.clear();
+    multi_parts.clear();
+    multi_first.clear();
+    int64_t seg0 = -1, tile_nnz = 0;
+    auto close = [&](int64_t seg_end) {
+      if (seg0 >= 0 && seg_end > seg0) {
+        units.push_back(make_int4(static_cast<int>(seg0), static_cast<int>(seg_end),
+                                  static_cast<int>(ptr[seg0]), static_cast<int>(ptr[seg_end])));
+      }
+      seg0 = -1;
+      tile_nnz = 0;
+    };
+    for (int64_t s = s_begin; s < S; ++s) {
+      const int64_t len = ptr[s + 1] - ptr[s];
+      if (len > serial_cap && len <= kWarpTile) {
+        close(s);
+        units.push_back(make_int4(-1, -static_cast<int>(s) - 2, static_cast<int>(ptr[s]),
+                                  static_cast<int>(ptr[s + 1])));
+        continue;
+      }
+      if (len <= kWarpTile) {
+        if (seg0 >= 0 && (tile_nnz + len > target || s - seg0 >= max_segs)) close(s);
+        if (seg0 < 0) seg0 = s;
+        tile_nnz += len;
+        continue;
+      }
       close(s);
-      units.push_back(make_int4(-1, -static_cast<int>(s) - 2, static_cast<int>(ptr[s]),
-                                static_cast<int>(ptr[s + 1])));
-      continue;
+      if (ordered) {  // one lane sums the whole segment in index order
+        units.push_back(make_int4(static_cast<int>(s), static_cast<int>(s + 1),
+                                  static_cast<int>(ptr[s]), static_cast<int>(ptr[s + 1])));
+        continue;
+      }
+      // parts: d.y = the part's own slot (its index in this original order)
+      const int multi = static_cast<int>(multi_seg.size());
+      const int64_t part = len > kGiantMin ? kGiantPart : kWarpTile;
+      multi_first.push_back(static_cast<int>(units.size()));
+      for (int64_t b = ptr[s]; b < ptr[s + 1]; b += part) {
+        units.push_back(make_int4(-(multi + 1), static_cast<int>(units.size()), static_cast<int>(b),
+                                  static_cast<int>(std::min<int64_t>(b + part, ptr[s + 1]))));
+      }
+      multi_seg.push_back(static_cast<int>(s));
+      multi_parts.push_back(static_cast<int>(units.size()) - multi_first.back());
     }
-    if (len <= kWarpTile) {
-      if (seg0 >= 0 && (tile_nnz + len > kWarpTile || s - seg0 >= max_segs)) close(s);
-      if (seg0 < 0) seg0 = s;
-      tile_nnz += len;
-      continue;
+    close(S);
+  };
+  build(kWarpTile);
+  // Tree mode, large axes: balance the persistent grid's warps.  A warp's
+  // units run back to back behind its SM's gather queue, so a kernel ends
+  // with its most loaded SM (tools/warp_timeline.py: per-warp work spread
+  // 1.7x on config 2's power-law columns).  (1) Tile size retargeted so the
+  // unit count is a whole number of rounds of the grid's warps; (2) per
+  // round, the round's units (contiguous in memory) go to the warps with the
+  // least work so far, largest first (LPT).  FOLP_BALANCE=0 disables.
+  const char* benv = std::getenv("FOLP_BALANCE");
+  const int nw = c->sms * kPlanCtasPerSm * kWarps;
+  if (!ordered && nnz > (int64_t(1) << 20) && (benv == nullptr || std::atoi(benv) > 0) &&
+      static_cast<int64_t>(units.size()) > nw) {
+    int64_t tile_units = 0, tile_nnz_total = 0;
+    for (const int4& d : units) {
+      if (d.x >= 0) {
+        ++tile_units;
+        tile_nnz_total += d.w - d.z;
+      }
     }
-    close(s);
-    if (ordered) {  // one lane sums the whole segment in index order
-      units.push_back(make_int4(static_cast<int>(s), static_cast<int>(s + 1),
-                                static_cast<int>(ptr[s]), static_cast<int>(ptr[s + 1])));
-      continue;
+    const int64_t other = static_cast<int64_t>(units.size()) - tile_units;
+    const int64_t rounds = (static_cast<int64_t>(units.size()) + nw - 1) / nw;
+    const int64_t want_tiles = rounds * nw - other;
+    if (want_tiles > tile_units && tile_units > 0) {
+      const int64_t target = std::max<int64_t>(32, (tile_nnz_total + want_tiles - 1) / want_tiles);
+      if (target < kWarpTile) build(target);
     }
-    const int multi = static_cast<int>(multi_seg.size());
-    const int64_t part = len > kGiantMin ? kGiantPart : kWarpTile;
-    const int first = static_cast<int>(units.size());
-    for (int64_t b = ptr[s]; b < ptr[s + 1]; b += part) {
-      units.push_back(make_int4(-(multi + 1), first, static_cast<int>(b),
-                                static_cast<int>(std::min<int64_t>(b + part, ptr[s + 1]))));
+    auto cost = [](const int4& d) -> int64_t {
+      const int64_t segs = d.x >= 0 ? d.y - d.x : 1;
+      return (d.w - d.z) + 2 * segs + 24;
+    };
+    // assign[r * nw + w] = unit of warp w in round r; warps are relabelled at
+    // the end so a short last round lands on the least loaded warps
+    const int64_t nu = static_cast<int64_t>(units.size());
+    const int64_t full = nu / nw;
+    std::vector<int> assign(static_cast<size_t>(full) * nw);
+    std::vector<int64_t> load(nw, 0);
+    std::vector<int> wo(nw), uo(nw);
+    for (int64_t r = 0; r < full; ++r) {
+      for (int i = 0; i < nw; ++i) uo[i] = static_cast<int>(r * nw) + i;
+      std::stable_sort(uo.begin(), uo.end(),
+                       [&](int a, int b) { return cost(units[a]) > cost(units[b]); });
+      for (int w = 0; w < nw; ++w) wo[w] = w;
+      std::stable_sort(wo.begin(), wo.end(), [&](int a, int b) { return load[a] < load[b]; });
+      for (int i = 0; i < nw; ++i) {
+        assign[r * nw + wo[i]] = uo[i];
+        load[wo[i]] += cost(units[uo[i]]);
+      }
     }
-    multi_seg.push_back(static_cast<int>(s));
-    multi_parts.push_back(static_cast<int>(units.size()) - first);
+    const int rest = static_cast<int>(nu - full * nw);
+    for (int w = 0; w < nw; ++w) wo[w] = w;
+    std::stable_sort(wo.begin(), wo.end(), [&](int a, int b) { return load[a] < load[b]; });
+    std::vector<int> label(nw);  // label[w]: warp index in the launched grid
+    for (int i = 0; i < nw; ++i) label[wo[i]] = i;  // least loaded -> lowest labels
+    std::vector<int4> perm(units.size());
+    for (int64_t r = 0; r < full; ++r) {
+      for (int w = 0; w < nw; ++w) perm[r * nw + label[w]] = units[assign[r * nw + w]];
+    }
+    if (rest > 0) {  // labels 0..rest-1 are the least loaded: largest units first
+      uo.resize(rest);
+      for (int i = 0; i < rest; ++i) uo[i] = static_cast<int>(full * nw) + i;
+      std::stable_sort(uo.begin(), uo.end(),
+                       [&](int a, int b) { return cost(units[a]) > cost(units[b]); });
+      for (int i = 0; i < rest; ++i) perm[full * nw + i] = units[uo[i]];
+    }
+    units.swap(perm);
   }
-  close(S);
   auto up = [&](const auto& v) {
     using T = typename std::decay_t<decltype(v)>::value_type;
     T* d = dalloc<T>(v.size());
@@ -102,6 +176,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   p.n_units = static_cast<int>(units.size());
   p.multi_seg = up(multi_seg);
   p.multi_parts = up(multi_parts);
+  p.multi_first = up(multi_first);
   p.n_multi = static_cast<int>(multi_seg.size());
   p.part_sums = dalloc<double>(units.size());
   out.owned.push_back(p.part_sums);

@@ -12,8 +12,9 @@
 // proj/tests/acceptance_main.cpp:653-682).
 //
 // Work units (built once on the host, SegPlan) -- all warp-sized, one
-// balanced stream distributed round-robin over the warps of a grid of a few
-// CTAs per SM:
+// stream distributed round-robin over the warps of a persistent grid of a
+// few CTAs per SM (unit u runs on warp u mod warps; plans.cuh orders the
+// units so every warp gets the same work):
 //   tile : consecutive segments with len <= kWarpTile packed into <=
 //          kWarpTile nonzeros (CSR-stream per warp).  Lane l loads entries
 //          l, l+32, ... of the tile's contiguous value/index range
@@ -26,7 +27,8 @@
 //   single part {-1, -(seg+2), k0, k1}: tree mode, a segment longer than
 //          the serial cap (plans.cuh), reduced by the warp; its epilogue
 //          feeds the warp's own accumulators (no slot, no arrival).
-//   part : a fixed chunk (kWarpTile entries; kGiantPart for giant segments)
+//   part {-(multi+1), slot, k0, k1}: a fixed chunk (kWarpTile entries;
+//          kGiantPart for giant segments)
 //          of a longer segment, reduced by the warp.  The last part of a
 //          segment to arrive sums the part sums in part order and runs the
 //          epilogue; its reduction contribution goes to a per-segment slot so
@@ -51,6 +53,7 @@ constexpr int kGiantMin = 65536;      // segments above this use kGiantPart part
 constexpr int kGiantPart = 2048;      // nnz per part of a giant segment
 constexpr int kMaxAcc = 30;           // widest reduction (bisection pass)
 constexpr int kSerialCap = 256;       // tree mode: longest segment one lane sums
+constexpr int kPlanCtasPerSm = 4;     // the loop products' residency (64 registers)
 
 // std::max / std::min semantics (NaN in `a` propagates), which the
 // reference's projections rely on for its NonFiniteIterate detection.
@@ -74,6 +77,7 @@ struct SegPlan {
   int n_units;
   const int* multi_seg;   // [n_multi] segment id of each multi-part segment
   const int* multi_parts; // [n_multi] number of parts
+  const int* multi_first; // [n_multi] slot of the first part (parts' slots are consecutive)
   int n_multi;
   double* part_sums;      // [n_units] (only part slots used)
   unsigned* arrivals;     // [n_multi], zero between launches
@@ -190,7 +194,7 @@ __device__ __forceinline__ void ordered_tail(const Epi& epi, RedBuf rb) {
 // the most recent launch of each traced epilogue (Epi::kTrace = 0 / 1).
 constexpr int kTraceWarps = 16384;
 #ifdef FOLP_WARP_TIMES
-__device__ unsigned long long g_warp_times[2][kTraceWarps][3];
+__device__ unsigned long long g_warp_times[2][kTraceWarps][4];  // + work word
 __device__ unsigned long long g_tail_times[2][4];  // last CTA: ticket, sums, finalize, end
 #endif
 template <class E, class = void>
@@ -412,10 +416,17 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   // data-pipe wavefronts and measured slower: profiles/r1_segpipe_experiments.md.)
   int u = blockIdx.x * kWarps + warp;
   int4 d_next = u < p.n_units ? p.units[u] : make_int4(0, 0, 0, 0);
+#ifdef FOLP_WARP_TIMES
+  unsigned long long work = 0;  // nnz | parts << 24 | tile segments << 36 | smid << 52
+#endif
   for (; u < p.n_units; u += nw) {
     const int4 d = d_next;
     if (u + nw < p.n_units) d_next = p.units[u + nw];
     const int k0 = d.z, k1 = d.w;
+#ifdef FOLP_WARP_TIMES
+    work += static_cast<unsigned long long>(k1 - k0) +
+            (d.x < 0 ? (1ull << 24) : (static_cast<unsigned long long>(d.y - d.x) << 36));
+#endif
     if (d.x >= 0 && k1 - k0 > kWarpTile) {
       // ordered plan: one long segment, summed by one lane in index order
       if (lane == 0) {
@@ -483,13 +494,13 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       if (single) {
         if (lane == 0) epi.apply(-d.y - 2, sum, pre_single, acc);
       } else if (lane == 0) {
-        p.part_sums[u] = sum;
+        p.part_sums[d.y] = sum;
         fence_acq_rel();
         const int np = p.multi_parts[multi];
         const unsigned arrived = atomicAdd(&p.arrivals[multi], 1u);
         if (arrived == static_cast<unsigned>(np - 1)) {
           fence_acq_rel();
-          const int first = d.y;
+          const int first = p.multi_first[multi];
           double total = 0.0;
           for (int q = 0; q < np; ++q) total += ld_cg(&p.part_sums[first + q]);
           const int seg = p.multi_seg[multi];
@@ -507,6 +518,11 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   }
 #ifdef FOLP_WARP_TIMES
   trace_warp<Epi>(1, global_ns());
+  {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    trace_warp<Epi>(3, work | (static_cast<unsigned long long>(smid) << 52));
+  }
 #endif
   if constexpr (Epi::kReduce) {
     if constexpr (ORDERED) {
@@ -606,7 +622,7 @@ __device__ void cluster_product(const SegPlan& p, const ResidentUnit& r, int u, 
     const int np = p.multi_parts[multi];
     unsigned last = 0;
     if (lane == 0) {
-      p.part_sums[u] = sum;
+      p.part_sums[d.y] = sum;
       __threadfence();
       last = atomicAdd(&p.arrivals[multi], 1u) == static_cast<unsigned>(np - 1) ? 1u : 0u;
     }
@@ -614,7 +630,8 @@ __device__ void cluster_product(const SegPlan& p, const ResidentUnit& r, int u, 
     if (last) {
       __threadfence();
       double total = 0.0;
-      for (int q = lane; q < np; q += 32) total += ld_cg(&p.part_sums[d.y + q]);
+      const int first = p.multi_first[multi];
+      for (int q = lane; q < np; q += 32) total += ld_cg(&p.part_sums[first + q]);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) total += __shfl_down_sync(0xffffffffu, total, off);
       if (lane == 0) {
