@@ -110,47 +110,87 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
     const int64_t rounds = (static_cast<int64_t>(units.size()) + nw - 1) / nw;
     const int64_t want_tiles = rounds * nw - other;
     if (want_tiles > tile_units && tile_units > 0) {
-      const int64_t target = std::max<int64_t>(32, (tile_nnz_total + want_tiles - 1) / want_tiles);
-      if (target < kWarpTile) build(target);
+      // the smallest tile target whose plan still fits the rounds (greedy
+      // packing leaves gaps, so search rather than divide)
+      const int64_t cap_units = rounds * nw;
+      int64_t lo = std::max<int64_t>(32, tile_nnz_total / want_tiles), hi = kWarpTile;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        build(mid);
+        if (static_cast<int64_t>(units.size()) <= cap_units) hi = mid; else lo = mid + 1;
+      }
+      build(lo);
     }
     auto cost = [](const int4& d) -> int64_t {
       const int64_t segs = d.x >= 0 ? d.y - d.x : 1;
       return (d.w - d.z) + 2 * segs + 24;
     };
-    // assign[r * nw + w] = unit of warp w in round r; warps are relabelled at
-    // the end so a short last round lands on the least loaded warps
+    // Balanced at CTA granularity: the 8 consecutive units a CTA's warps
+    // take in one round stay together and in order (neighbouring segments
+    // share gathered lines in L1); per round, the round's chunks go to the
+    // CTAs with the least work so far, largest first.  A short last round
+    // lands on the least loaded CTAs (CTA indices relabelled).
     const int64_t nu = static_cast<int64_t>(units.size());
-    const int64_t full = nu / nw;
-    std::vector<int> assign(static_cast<size_t>(full) * nw);
-    std::vector<int64_t> load(nw, 0);
-    std::vector<int> wo(nw), uo(nw);
+    const int nc = nw / kWarps;                      // CTAs of the persistent grid
+    const int64_t nchunks = (nu + kWarps - 1) / kWarps;
+    auto chunk_cost = [&](int64_t ch) {
+      int64_t t = 0;
+      for (int64_t u = ch * kWarps; u < std::min<int64_t>(nu, (ch + 1) * kWarps); ++u) t += cost(units[u]);
+      return t;
+    };
+    const int64_t full = nchunks / nc;
+    std::vector<int64_t> assign(static_cast<size_t>(full) * nc);
+    std::vector<int64_t> load(nc, 0);
+    std::vector<int> co(nc);
+    std::vector<int64_t> ko(nc);
     for (int64_t r = 0; r < full; ++r) {
-      for (int i = 0; i < nw; ++i) uo[i] = static_cast<int>(r * nw) + i;
-      std::stable_sort(uo.begin(), uo.end(),
-                       [&](int a, int b) { return cost(units[a]) > cost(units[b]); });
-      for (int w = 0; w < nw; ++w) wo[w] = w;
-      std::stable_sort(wo.begin(), wo.end(), [&](int a, int b) { return load[a] < load[b]; });
-      for (int i = 0; i < nw; ++i) {
-        assign[r * nw + wo[i]] = uo[i];
-        load[wo[i]] += cost(units[uo[i]]);
+      for (int i = 0; i < nc; ++i) ko[i] = r * nc + i;
+      std::stable_sort(ko.begin(), ko.end(),
+                       [&](int64_t a, int64_t b) { return chunk_cost(a) > chunk_cost(b); });
+      for (int b = 0; b < nc; ++b) co[b] = b;
+      std::stable_sort(co.begin(), co.end(), [&](int a, int b) { return load[a] < load[b]; });
+      for (int i = 0; i < nc; ++i) {
+        assign[r * nc + co[i]] = ko[i];
+        load[co[i]] += chunk_cost(ko[i]);
       }
     }
-    const int rest = static_cast<int>(nu - full * nw);
-    for (int w = 0; w < nw; ++w) wo[w] = w;
-    std::stable_sort(wo.begin(), wo.end(), [&](int a, int b) { return load[a] < load[b]; });
-    std::vector<int> label(nw);  // label[w]: warp index in the launched grid
-    for (int i = 0; i < nw; ++i) label[wo[i]] = i;  // least loaded -> lowest labels
-    std::vector<int4> perm(units.size());
+    for (int b = 0; b < nc; ++b) co[b] = b;
+    std::stable_sort(co.begin(), co.end(), [&](int a, int b) { return load[a] < load[b]; });
+    std::vector<int> label(nc);
+    for (int i = 0; i < nc; ++i) label[co[i]] = i;
+    // unit u runs on warp u mod nw = CTA (u mod nw) / 8; round r of CTA b is
+    // units r * nw + 8 b .. + 7
+    // slots the balanced order leaves empty (a partial chunk not in the
+    // last position) hold empty tiles {0, 0, 0, 0}: no segment, no entry
+    const int64_t rest_chunks = nchunks - full * nc;
+    std::vector<int4> perm(static_cast<size_t>(full * nw + rest_chunks * kWarps), make_int4(0, 0, 0, 0));
+    auto put_chunk = [&](int64_t r, int b, int64_t ch) {
+      for (int j = 0; j < kWarps; ++j) {
+        const int64_t src = ch * kWarps + j, dst = r * nw + static_cast<int64_t>(b) * kWarps + j;
+        if (src < nu) perm[dst] = units[src];
+      }
+    };
     for (int64_t r = 0; r < full; ++r) {
-      for (int w = 0; w < nw; ++w) perm[r * nw + label[w]] = units[assign[r * nw + w]];
+      for (int b = 0; b < nc; ++b) put_chunk(r, label[b], assign[r * nc + b]);
     }
-    if (rest > 0) {  // labels 0..rest-1 are the least loaded: largest units first
-      uo.resize(rest);
-      for (int i = 0; i < rest; ++i) uo[i] = static_cast<int>(full * nw) + i;
-      std::stable_sort(uo.begin(), uo.end(),
-                       [&](int a, int b) { return cost(units[a]) > cost(units[b]); });
-      for (int i = 0; i < rest; ++i) perm[full * nw + i] = units[uo[i]];
+    const int64_t rest = nchunks - full * nc;
+    if (rest > 0) {  // CTAs 0..rest-1 are the least loaded: largest chunks first
+      std::vector<int64_t> ro(rest);
+      for (int64_t i = 0; i < rest; ++i) ro[i] = full * nc + i;
+      std::stable_sort(ro.begin(), ro.end(),
+                       [&](int64_t a, int64_t b) { return chunk_cost(a) > chunk_cost(b); });
+      // the last round's slots are the first nu - full * nw; a partial chunk
+      // must take the highest slots so no slot inside the range stays empty
+      const int64_t last = nchunks - 1;
+      const bool partial = nu % kWarps != 0;
+      int64_t slot = 0;
+      for (int64_t i = 0; i < rest; ++i) {
+        if (partial && ro[i] == last) continue;
+        put_chunk(full, static_cast<int>(slot++), ro[i]);
+      }
+      if (partial) put_chunk(full, static_cast<int>(slot), last);
     }
+    while (!perm.empty() && perm.back().x == 0 && perm.back().y == 0 && perm.back().w == 0) perm.pop_back();
     units.swap(perm);
   }
   auto up = [&](const auto& v) {

@@ -26,7 +26,12 @@ def _sum_abs_terms(lp, vec, transpose):
     return out
 
 
-@pytest.mark.parametrize("cfg,scale", FAMILIES)
+# above 2^20 nonzeros the tree-mode plans are balanced (plans.cuh: retargeted
+# tiles, chunk-level LPT order, single parts, padding slots)
+LARGE = [(2, 0.4), (3, 0.06), (5, 0.04)]
+
+
+@pytest.mark.parametrize("cfg,scale", FAMILIES + LARGE)
 def test_products_match_reference(eng, ref, cfg, scale):
     lp = _lp(cfg, scale)
     rng = np.random.default_rng(cfg)

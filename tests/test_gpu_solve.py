@@ -121,6 +121,21 @@ def test_tree_mode_first_100_iterates(eng, ref):
     assert a.kkt_passes == b.kkt_passes
 
 
+@pytest.mark.parametrize("cfg,scale", [(2, 0.4), (3, 0.06)])
+def test_tree_mode_balanced_plans_first_restart_period(eng, ref, cfg, scale):
+    """Instances above 2^20 nonzeros run the balanced unit plans (plans.cuh):
+    the first restart period stays within 1e-9 of the reference, restarts and
+    the ledger agree over 120 iterations."""
+    lp = instances.generate(cfg, 1, scale)
+    assert lp.nnz > (1 << 20)
+    p = cabi.params(record_iterate_trace=True, iteration_limit=120)
+    a = eng.solve_lp(lp, p, iterate_capacity=120)
+    b = ref.solve_lp(lp, p, iterate_capacity=120)
+    assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-9
+    assert a.restart_iterations == b.restart_iterations
+    assert a.kkt_passes == b.kkt_passes
+
+
 @pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 0.01), (5, 0.01)])
 def test_tree_mode_solve_to_1e8(eng, ref, cfg, scale):
     """Production reductions to 1e-8.  The adaptive step amplifies last-bit
