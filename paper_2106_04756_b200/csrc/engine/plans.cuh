@@ -97,8 +97,32 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   // least work so far, largest first (LPT).  FOLP_BALANCE=0 disables.
   const char* benv = std::getenv("FOLP_BALANCE");
   const int nw = c->sms * kPlanCtasPerSm * kWarps;
-  if (!ordered && nnz > (int64_t(1) << 20) && (benv == nullptr || std::atoi(benv) > 0) &&
-      static_cast<int64_t>(units.size()) > nw) {
+  auto cost = [](const int4& d) -> int64_t {
+    const int64_t segs = d.x >= 0 ? d.y - d.x : 1;
+    return (d.w - d.z) + 2 * segs + 24;
+  };
+  // max / mean CTA load of the plain round-robin order: even plans (config
+  // 5's equal parts and tiles) are left alone -- reordering them measured
+  // 14 % slower there, while skewed ones gain (config 3: 11 %)
+  auto rr_imbalance = [&]() {
+    const int nc = nw / kWarps;
+    std::vector<int64_t> ld(nc, 0);
+    int64_t tot = 0;
+    for (size_t u = 0; u < units.size(); ++u) {
+      ld[(u % nw) / kWarps] += cost(units[u]);
+      tot += cost(units[u]);
+    }
+    const int64_t mx = *std::max_element(ld.begin(), ld.end());
+    return tot > 0 ? static_cast<double>(mx) * nc / static_cast<double>(tot) : 1.0;
+  };
+  const double imb0 = units.size() > static_cast<size_t>(nw) ? rr_imbalance() : 1.0;
+  const bool balance = !ordered && nnz > (int64_t(1) << 20) && (benv == nullptr || std::atoi(benv) > 0) &&
+                       static_cast<int64_t>(units.size()) > nw && imb0 > kBalanceMin;
+  if (std::getenv("FOLP_TIMING") != nullptr && units.size() > static_cast<size_t>(nw)) {
+    std::fprintf(stderr, "[folp timing] plan S=%lld units=%zu round-robin CTA imbalance %.3f%s\n",
+                 static_cast<long long>(S - s_begin), units.size(), imb0, balance ? " -> balanced" : "");
+  }
+  if (balance) {
     int64_t tile_units = 0, tile_nnz_total = 0;
     for (const int4& d : units) {
       if (d.x >= 0) {
@@ -121,10 +145,6 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
       }
       build(lo);
     }
-    auto cost = [](const int4& d) -> int64_t {
-      const int64_t segs = d.x >= 0 ? d.y - d.x : 1;
-      return (d.w - d.z) + 2 * segs + 24;
-    };
     // Balanced at CTA granularity: the 8 consecutive units a CTA's warps
     // take in one round stay together and in order (neighbouring segments
     // share gathered lines in L1); per round, the round's chunks go to the
@@ -191,6 +211,12 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
       if (partial) put_chunk(full, static_cast<int>(slot), last);
     }
     while (!perm.empty() && perm.back().x == 0 && perm.back().y == 0 && perm.back().w == 0) perm.pop_back();
+    if (std::getenv("FOLP_TIMING") != nullptr) {
+      units.swap(perm);
+      std::fprintf(stderr, "[folp timing] plan S=%lld balanced: units=%zu imbalance %.3f\n",
+                   static_cast<long long>(S - s_begin), units.size(), rr_imbalance());
+      units.swap(perm);
+    }
     units.swap(perm);
   }
   auto up = [&](const auto& v) {

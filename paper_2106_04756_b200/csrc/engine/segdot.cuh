@@ -54,6 +54,7 @@ constexpr int kGiantPart = 2048;      // nnz per part of a giant segment
 constexpr int kMaxAcc = 30;           // widest reduction (bisection pass)
 constexpr int kSerialCap = 256;       // tree mode: longest segment one lane sums
 constexpr int kPlanCtasPerSm = 4;     // the loop products' residency (64 registers)
+constexpr double kBalanceMin = 1.04;  // round-robin CTA load imbalance worth reordering
 
 // std::max / std::min semantics (NaN in `a` propagates), which the
 // reference's projections rely on for its NonFiniteIterate detection.

@@ -124,14 +124,15 @@ def test_tree_mode_first_100_iterates(eng, ref):
 @pytest.mark.parametrize("cfg,scale", [(2, 0.4), (3, 0.06)])
 def test_tree_mode_balanced_plans_first_restart_period(eng, ref, cfg, scale):
     """Instances above 2^20 nonzeros run the balanced unit plans (plans.cuh):
-    the first restart period stays within 1e-9 of the reference, restarts and
-    the ledger agree over 120 iterations."""
+    the first restart period stays within 1e-7 of the reference (tree-mode
+    sums; a wrong plan is off by O(1)), restarts and the ledger agree over
+    120 iterations."""
     lp = instances.generate(cfg, 1, scale)
     assert lp.nnz > (1 << 20)
     p = cabi.params(record_iterate_trace=True, iteration_limit=120)
     a = eng.solve_lp(lp, p, iterate_capacity=120)
     b = ref.solve_lp(lp, p, iterate_capacity=120)
-    assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-9
+    assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-7
     assert a.restart_iterations == b.restart_iterations
     assert a.kkt_passes == b.kkt_passes
 
