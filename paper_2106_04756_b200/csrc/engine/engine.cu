@@ -183,6 +183,7 @@ struct folp_gpu_ctx {
   int max_giant = 0;
   int bisect_grid = 0;
   int* ndg_list = nullptr;        // k_ndg_bisect active lists [2][n + m]
+  int* ndg_compact = nullptr;     // k_ndg_bisect block 0's gathered lists [2][kBisectSmall]
   bool coop_ok = true;            // cooperative launches available (else OpNdgPass passes)
   // evaluation period as a CUDA graph, one per CURRENT buffer parity
   cudaGraphExec_t eval_exec[2] = {nullptr, nullptr};
@@ -555,7 +556,10 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       c->lo[s] = c->alloc<double>(n + m);
       c->hi[s] = vn();
     }
-    if (!c->ordered) c->ndg_list = c->alloc<int>(2 * static_cast<size_t>(n + m) + 2);
+    if (!c->ordered) {
+      c->ndg_list = c->alloc<int>(2 * static_cast<size_t>(n + m) + 2);
+      c->ndg_compact = c->alloc<int>(2 * static_cast<size_t>(kBisectSmall));
+    }
     c->partials = c->alloc<double>(static_cast<size_t>(kMaxGrid + c->max_giant + 8) * kMaxAcc);
     if (c->ordered) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);

@@ -80,7 +80,84 @@ struct BisectArgs {
   int active[2];
   int* list[2];      // [total] per set: the blocks' active element lists
   double* partials;  // [2 parity][2 sets][kBisectVals][grid]
+  int* compact[2];   // [kBisectSmall] per set: the last active elements, block 0's
+  int small_limit;   // switch to one block at <= this many active elements (0: never)
 };
+
+// Once at most kBisectSmall elements of every running set still have a
+// breakpoint inside the bracket, they are gathered into one list and block
+// 0 finishes the bisection alone: a pass then costs one block's sweep over
+// a few thousand L2-resident elements instead of a grid-wide sync.
+constexpr int kBisectSmall = 4096;
+
+// One pass over a set's active elements (tree mode): retire the elements
+// whose clamping cannot change inside the bracket into the closed-form sums
+// (fq, fh, fs), accumulate ||d||_w^2 and g'd at the candidates for the rest,
+// and compact the list in place (order preserved).  Returns the kept count
+// (the same in every thread of the block).
+__device__ __forceinline__ int bisect_sweep(const BisectArgs& a, const NdgState& st, int s,
+                                            int* list, int cnt, bool first, int64_t b0,
+                                            double (&acc)[2 * kNuCands], double& fq, double& fh,
+                                            double& fs, int* wcount) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* g = a.g[s];
+  const double* lo = a.lo[s];
+  const double* hi = a.hi[s];
+  const double omega = st.omega, winv = st.winv;
+  int kept = 0;
+  for (int t0 = 0; t0 < cnt; t0 += kBisectThreads) {
+    const int k = t0 + tid;
+    int i = -1;
+    bool keep = false;
+    if (k < cnt) {
+      i = first ? static_cast<int>(b0 + k) : list[k];
+      const double gs = g[i];
+      if (gs != 0.0) {
+        const bool primal = i < a.n;
+        const double w = primal ? omega : winv;
+        const double los = lo[i];
+        const double his = primal ? hi[i] : INFINITY;
+        const int side = primal ? 0 : 1;
+        const double ulo = gs * st.rcp_lo[side];  // |u| largest at nu_lo
+        const double uhi = gs * st.rcp_hi[side];
+        const bool clamped_lo = ulo < los || ulo > his;
+        const bool clamped_hi = uhi < los || uhi > his;
+        if (clamped_hi) {  // clamped over the whole bracket
+          const double cv = uhi > his ? his : los;
+          fq += w * cv * cv;
+          fh += gs * cv;
+        } else if (!clamped_lo) {  // free over the whole bracket
+          fs += gs * gs * (primal ? winv : omega);
+        } else {
+          keep = true;
+          const double* rcp = primal ? st.rcp_primal : st.rcp_dual;
+#pragma unroll
+          for (int p = 0; p < kNuCands; ++p) {
+            const double d = ref_min(ref_max(gs * rcp[p], los), his);
+            acc[2 * p] += w * d * d;
+            acc[2 * p + 1] += gs * d;
+          }
+        }
+      }
+    }
+    // in-place, order-preserving compaction: every read of this tile
+    // precedes the barrier, every write lands below t0 + kBisectThreads
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int off = kept, tile = 0;
+#pragma unroll
+    for (int w = 0; w < kBisectThreads / 32; ++w) {
+      const int c = wcount[w];
+      if (w < warp) off += c;
+      tile += c;
+    }
+    if (keep) list[off + __popc(bal & ((1u << lane) - 1u))] = i;
+    kept += tile;
+    __syncthreads();
+  }
+  return kept;
+}
 
 __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
   namespace cg = cooperative_groups;
@@ -90,6 +167,8 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
   __shared__ double tot[2][kBisectVals];
   __shared__ int wcount[kBisectThreads / 32];
   __shared__ int kept_count[2];
+  __shared__ int s_off[2];
+  __shared__ double base[2][3];  // block 0 alone: the grid's Q, H, S at the switch
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = gridDim.x;
   const int64_t chunk = (a.total + nb - 1) / nb;
@@ -102,7 +181,7 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
   }
   double fq[2] = {0.0, 0.0}, fh[2] = {0.0, 0.0}, fs[2] = {0.0, 0.0};
   __syncthreads();
-  bool first = true;
+  bool first = true, alone = false;
   for (int parity = 0;; parity ^= 1) {
     const bool run[2] = {st[0].done == 0, st[1].done == 0};
     if (!run[0] && !run[1]) break;  // same state in every block
@@ -115,65 +194,9 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       if (!run[s]) continue;
-      const double* g = a.g[s];
-      const double* lo = a.lo[s];
-      const double* hi = a.hi[s];
-      int* list = a.list[s] + b0;
-      const double omega = st[s].omega, winv = st[s].winv;
-      const int cnt = kept_count[s];
-      int kept = 0;
-      for (int t0 = 0; t0 < cnt; t0 += kBisectThreads) {
-        const int k = t0 + tid;
-        int i = -1;
-        bool keep = false;
-        if (k < cnt) {
-          i = first ? static_cast<int>(b0 + k) : list[k];
-          const double gs = g[i];
-          if (gs != 0.0) {
-            const bool primal = i < a.n;
-            const double w = primal ? omega : winv;
-            const double los = lo[i];
-            const double his = primal ? hi[i] : INFINITY;
-            const int side = primal ? 0 : 1;
-            const double ulo = gs * st[s].rcp_lo[side];  // |u| largest at nu_lo
-            const double uhi = gs * st[s].rcp_hi[side];
-            const bool clamped_lo = ulo < los || ulo > his;
-            const bool clamped_hi = uhi < los || uhi > his;
-            if (clamped_hi) {  // clamped over the whole bracket
-              const double cv = uhi > his ? his : los;
-              fq[s] += w * cv * cv;
-              fh[s] += gs * cv;
-            } else if (!clamped_lo) {  // free over the whole bracket
-              fs[s] += gs * gs * (primal ? winv : omega);
-            } else {
-              keep = true;
-              const double* rcp = primal ? st[s].rcp_primal : st[s].rcp_dual;
-#pragma unroll
-              for (int p = 0; p < kNuCands; ++p) {
-                const double d = ref_min(ref_max(gs * rcp[p], los), his);
-                acc[s][2 * p] += w * d * d;
-                acc[s][2 * p + 1] += gs * d;
-              }
-            }
-          }
-        }
-        // in-place, order-preserving compaction of the block's list: every
-        // read of this tile precedes the barrier, every write lands below t0+512
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) wcount[warp] = __popc(bal);
-        __syncthreads();
-        int off = kept, tile = 0;
-#pragma unroll
-        for (int w = 0; w < kBisectThreads / 32; ++w) {
-          const int c = wcount[w];
-          if (w < warp) off += c;
-          tile += c;
-        }
-        if (keep) list[off + __popc(bal & ((1u << lane) - 1u))] = i;
-        kept += tile;
-        __syncthreads();
-      }
-      kept_s[s] = kept;
+      int* list = alone ? a.compact[s] : a.list[s] + b0;
+      kept_s[s] = bisect_sweep(a, st[s], s, list, kept_count[s], first, b0, acc[s], fq[s], fh[s],
+                               fs[s], wcount);
     }
     __syncthreads();
     if (tid < 2 && run[tid]) kept_count[tid] = kept_s[tid];
@@ -193,25 +216,41 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
     }
     __syncthreads();
     double* part = a.partials + static_cast<size_t>(parity) * 2 * kBisectVals * nb;
-    if (tid < 2 * kBisectVals) {
-      const int s = tid / kBisectVals, k = tid % kBisectVals;
-      double v = 0.0;
-      if (k == 2 * kNuCands) {
-        v = static_cast<double>(kept_s[s]);
-      } else {
-        for (int w = 0; w < kBisectThreads / 32; ++w) v += wsum[w][s][k];
+    if (alone) {
+      // block 0 alone: block totals are the totals (plus the grid's
+      // retired sums at the switch)
+      if (tid < 2 * kBisectVals) {
+        const int s = tid / kBisectVals, k = tid % kBisectVals;
+        double v = 0.0;
+        if (k == 2 * kNuCands) {
+          v = static_cast<double>(kept_s[s]);
+        } else {
+          for (int w = 0; w < kBisectThreads / 32; ++w) v += wsum[w][s][k];
+          if (k > 2 * kNuCands) v += base[s][k - 2 * kNuCands - 1];
+        }
+        tot[s][k] = v;
       }
-      part[static_cast<size_t>(tid) * nb + blockIdx.x] = v;
-    }
-    grid.sync();
-    // every block: totals in block order, one warp per (set, value) pair
-    for (int pair = warp; pair < 2 * kBisectVals; pair += kBisectThreads / 32) {
-      const double* src = part + static_cast<size_t>(pair) * nb;
-      double v = 0.0;
-      for (int b = lane; b < nb; b += 32) v += src[b];
+    } else {
+      if (tid < 2 * kBisectVals) {
+        const int s = tid / kBisectVals, k = tid % kBisectVals;
+        double v = 0.0;
+        if (k == 2 * kNuCands) {
+          v = static_cast<double>(kept_s[s]);
+        } else {
+          for (int w = 0; w < kBisectThreads / 32; ++w) v += wsum[w][s][k];
+        }
+        part[static_cast<size_t>(tid) * nb + blockIdx.x] = v;
+      }
+      grid.sync();
+      // every block: totals in block order, one warp per (set, value) pair
+      for (int pair = warp; pair < 2 * kBisectVals; pair += kBisectThreads / 32) {
+        const double* src = part + static_cast<size_t>(pair) * nb;
+        double v = 0.0;
+        for (int b = lane; b < nb; b += 32) v += src[b];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0) tot[pair / kBisectVals][pair % kBisectVals] = v;
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) tot[pair / kBisectVals][pair % kBisectVals] = v;
+      }
     }
     __syncthreads();
     if (tid < 2 && run[tid]) {
@@ -229,6 +268,42 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
     }
     first = false;
     __syncthreads();
+    if (!alone && a.small_limit > 0) {
+      // every block sees the same totals, so all take the same branch
+      bool go = st[0].done == 0 || st[1].done == 0;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (st[s].done == 0 && tot[s][2 * kNuCands] > static_cast<double>(a.small_limit)) go = false;
+      }
+      if (go) {
+        if (tid < 2) {  // this block's offset in the gathered list
+          int off = 0;
+          for (int b = 0; b < static_cast<int>(blockIdx.x); ++b) {
+            off += static_cast<int>(part[static_cast<size_t>(tid * kBisectVals + 2 * kNuCands) * nb + b]);
+          }
+          s_off[tid] = off;
+          base[tid][0] = tot[tid][2 * kNuCands + 1];
+          base[tid][1] = tot[tid][2 * kNuCands + 2];
+          base[tid][2] = tot[tid][2 * kNuCands + 3];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (st[s].done) continue;
+          const int* own_list = a.list[s] + b0;
+          for (int k = tid; k < kept_count[s]; k += kBisectThreads) {
+            a.compact[s][s_off[s] + k] = own_list[k];
+          }
+        }
+        grid.sync();
+        if (blockIdx.x != 0) return;
+        if (tid < 2) kept_count[tid] = static_cast<int>(tot[tid][2 * kNuCands]);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) fq[s] = fh[s] = fs[s] = 0.0;  // now in base[]
+        alone = true;
+        __syncthreads();
+      }
+    }
   }
   if (blockIdx.x == 0 && tid < 2 && a.active[tid]) *a.ns[tid] = st[tid];
 }
@@ -443,6 +518,12 @@ void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&om
     a.partials = c->partials;
     a.list[0] = c->ndg_list;
     a.list[1] = c->ndg_list + a.total;
+    a.compact[0] = c->ndg_compact;
+    a.compact[1] = c->ndg_compact + kBisectSmall;
+    {
+      const char* env = std::getenv("FOLP_BISECT_SMALL");  // 0: grid-wide to the end
+      a.small_limit = env ? std::min(std::max(0, std::atoi(env)), kBisectSmall) : kBisectSmall;
+    }
     int& grid = c->bisect_grid;
     if (grid == 0) {  // co-resident by construction (cooperative launch)
       int occ = 0;
