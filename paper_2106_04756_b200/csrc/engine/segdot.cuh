@@ -381,7 +381,12 @@ __device__ __forceinline__ void prefetch_unit(const SegPlan& p, const double* va
 }
 
 template <class Epi, bool ORDERED, bool PROD = false>
-__global__ void __launch_bounds__(kBlock)
+#ifdef FOLP_WARP_TIMES
+#define FOLP_SEGDOT_BOUNDS __launch_bounds__(kBlock, kPlanCtasPerSm)  // same residency as the product build
+#else
+#define FOLP_SEGDOT_BOUNDS __launch_bounds__(kBlock)
+#endif
+__global__ void FOLP_SEGDOT_BOUNDS
 segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   constexpr int K = Epi::K;
   {
