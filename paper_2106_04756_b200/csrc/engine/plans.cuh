@@ -33,9 +33,16 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   // (tools/warp_timeline.py).  FOLP_SERIAL_CAP overrides (256 = off).  Not
   // for small axes, whose plans may run in k_chunk_cluster.
   int64_t serial_cap = kWarpTile;
+  // ... and segments up to single_max entries are one warp unit each (no
+  // parts: no arrival atomics, fences or slots; the balanced order below
+  // spreads their cost).  FOLP_SINGLE_MAX overrides.
+  int64_t single_max = kWarpTile;
   if (!ordered && nnz > (int64_t(1) << 20)) {
     const char* env = std::getenv("FOLP_SERIAL_CAP");
     serial_cap = std::min<int64_t>(kWarpTile, std::max<int64_t>(1, env ? std::atoi(env) : kSerialCap));
+    const char* smax = std::getenv("FOLP_SINGLE_MAX");
+    single_max = std::max<int64_t>(kWarpTile, smax ? std::atoll(smax) : kSingleMax);
+    if (single_max > kWarpTile) serial_cap = std::min<int64_t>(serial_cap, kWarpTile);
   }
   std::vector<int4> units;
   std::vector<int> multi_seg, multi_parts, multi_first;
@@ -56,7 +63,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
     };
     for (int64_t s = s_begin; s < S; ++s) {
       const int64_t len = ptr[s + 1] - ptr[s];
-      if (len > serial_cap && len <= kWarpTile) {
+      if (len > serial_cap && (len <= kWarpTile || len <= single_max)) {
         close(s);
         units.push_back(make_int4(-1, -static_cast<int>(s) - 2, static_cast<int>(ptr[s]),
                                   static_cast<int>(ptr[s + 1])));

@@ -29,7 +29,10 @@ __global__ void k_axis_absmax(const int* __restrict__ ptr, const double* __restr
 // atomicMax on the bit pattern (non-negative doubles order like their bits),
 // so the result is the exact maximum in any order.
 __device__ __forceinline__ int long_unit_segment(const SegPlan& p, const int4& d) {
-  if (d.x < 0) return d.y < 0 ? -1 : p.multi_seg[-d.x - 1];  // single parts are short
+  if (d.x < 0) {  // single units: the long ones are this axis' long segments too
+    if (d.y < 0) return d.w - d.z > kWarpTile ? -d.y - 2 : -1;
+    return p.multi_seg[-d.x - 1];
+  }
   return d.w - d.z > kWarpTile ? d.x : -1;
 }
 
