@@ -53,7 +53,7 @@ constexpr int kGiantMin = 65536;      // segments above this use kGiantPart part
 constexpr int kGiantPart = 2048;      // nnz per part of a giant segment
 constexpr int kMaxAcc = 30;           // widest reduction (bisection pass)
 constexpr int kSerialCap = 256;       // tree mode: longest segment one lane sums
-constexpr int kSingleMax = 256;       // tree mode, large axes: longest one-warp segment
+constexpr int kSingleMax = 1024;      // tree mode, large axes: longest one-warp segment
 constexpr int kPlanCtasPerSm = 4;     // the loop products' residency (64 registers)
 constexpr double kBalanceMin = 1.04;  // round-robin CTA load imbalance worth reordering
 
