@@ -257,28 +257,6 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   out.owned.push_back(p.arrivals);
   CK(cudaMemset(p.arrivals, 0, std::max<size_t>(1, multi_seg.size()) * sizeof(unsigned)));
   c->max_giant = std::max(c->max_giant, p.n_multi);
-  // Dynamic tail (tree mode, large axes): the last FOLP_DYN_FRAC (default
-  // kDynFrac) of the units are claimed by whichever warps finish their static
-  // share first -- SMs drain their gather queues at rates ~10 % apart, which
-  // no static order can know (tools/warp_timeline.py).
-  p.n_static = p.n_units;
-  p.claim = nullptr;
-  p.dyn_slots = nullptr;
-  {
-    const char* env = std::getenv("FOLP_DYN_FRAC");
-    const double frac = env ? std::atof(env) : kDynFrac;
-    if (!ordered && nnz > (int64_t(1) << 20) && frac > 0.0 && p.n_units > nw) {
-      const int n_dyn = static_cast<int>(std::min<double>(p.n_units - nw, frac * p.n_units));
-      if (n_dyn > 0) {
-        p.n_static = p.n_units - n_dyn;
-        p.claim = dalloc<unsigned>(1);
-        out.owned.push_back(p.claim);
-        CK(cudaMemset(p.claim, 0, sizeof(unsigned)));
-        p.dyn_slots = dalloc<double>(static_cast<size_t>(n_dyn) * kMaxAcc);
-        out.owned.push_back(p.dyn_slots);
-      }
-    }
-  }
 }
 
 void upload_index(folp_gpu_ctx* c, const int64_t* src, int* dst, int64_t count, int64_t* stage,

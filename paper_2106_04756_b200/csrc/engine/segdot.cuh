@@ -56,7 +56,6 @@ constexpr int kSerialCap = 256;       // tree mode: longest segment one lane sum
 constexpr int kSingleMax = 1024;      // tree mode, large axes: longest one-warp segment
 constexpr int kPlanCtasPerSm = 4;     // the loop products' residency (64 registers)
 constexpr double kBalanceMin = 1.04;  // round-robin CTA load imbalance worth reordering
-constexpr double kDynFrac = 0.2;      // share of the units claimed dynamically (tree mode)
 
 // std::max / std::min semantics (NaN in `a` propagates), which the
 // reference's projections rely on for its NonFiniteIterate detection.
@@ -84,12 +83,6 @@ struct SegPlan {
   int n_multi;
   double* part_sums;      // [n_units] (only part slots used)
   unsigned* arrivals;     // [n_multi], zero between launches
-  // tree mode, large axes: units [n_static, n_units) are claimed by the warps
-  // that finish their static share first; each such unit's reduction terms go
-  // to its own slot, so the sums never depend on which warp ran it
-  int n_static;           // == n_units: no dynamic tail
-  unsigned* claim;        // dynamic claims, zero between launches
-  double* dyn_slots;      // [(n_units - n_static) * kMaxAcc]
 };
 
 struct RedBuf {
@@ -178,20 +171,6 @@ __device__ __forceinline__ void block_sum_vec(double (&acc)[K], double (*scratch
   __syncthreads();
 }
 
-// The warp's per-lane terms reduced into dst[0..K) by lane 0 (block_sum_vec's
-// shuffle tree), the accumulators zeroed.
-template <int K>
-__device__ __forceinline__ void warp_flush(double (&acc)[K], double* dst, int lane) {
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double v = acc[k];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if (lane == 0) dst[k] = v;
-    acc[k] = 0.0;
-  }
-}
-
 // Ordered mode: after every CTA stored its terms, the last CTA's thread 0
 // folds them (epi.finalize_ordered).
 template <class Epi>
@@ -254,21 +233,6 @@ __device__ __forceinline__ void trace_warp(int which, unsigned long long t) {
 #endif
 }
 
-template <class Epi>
-__device__ __forceinline__ void reduce_tail_tot(const Epi& epi, double (&tot)[Epi::K], RedBuf rb,
-                                                int n_extra, const double* dyn, int n_dyn,
-                                                unsigned* claim);
-// The CTA's totals from per-thread accumulators, then the tail above.
-template <class Epi>
-__device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K], RedBuf rb,
-                                            int n_extra) {
-  constexpr int K = Epi::K;
-  __shared__ double s_acc[kWarps][K];
-  double tot[K];
-  block_sum_vec<K>(acc, s_acc, tot);
-  reduce_tail_tot(epi, tot, rb, n_extra, nullptr, 0, nullptr);
-}
-
 // Epilogues whose finalize runs the loop's step decision on the device
 // state (EpiDual) expose it as kStateWords 8-byte words: the last CTA loads
 // them into shared memory with all its threads while it sums the partials,
@@ -282,16 +246,14 @@ struct StateTail<E, std::void_t<decltype(E::kStateWords)>> {
 };
 
 // Per-block partial + last-block-done final reduction, then epi.finalize().
-// `tot` (thread 0): the CTA's totals; the last CTA adds, in index order, the
-// per-CTA partials, the n_extra multi-part slots and the n_dyn dynamic-unit
-// slots (p.dyn_slots, stride K), then resets `claim`.
 template <class Epi>
-__device__ __forceinline__ void reduce_tail_tot(const Epi& epi, double (&tot)[Epi::K], RedBuf rb,
-                                                int n_extra, const double* dyn, int n_dyn,
-                                                unsigned* claim) {
+__device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K], RedBuf rb,
+                                            int n_extra) {
   constexpr int K = Epi::K;
   __shared__ double s_vec[kWarps][K];
   __shared__ int s_last;
+  double tot[K];
+  block_sum_vec<K>(acc, s_vec, tot);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) rb.partials[blockIdx.x * K + k] = tot[k];
@@ -332,23 +294,6 @@ __device__ __forceinline__ void reduce_tail_tot(const Epi& epi, double (&tot)[Ep
       }
     }
   }
-  for (int base = threadIdx.x; base < n_dyn; base += kBlock * R) {
-    double v[R][K];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = base + r * kBlock;
-#pragma unroll
-      for (int k = 0; k < K; ++k) v[r][k] = i < n_dyn ? ld_cg(&dyn[i * K + k]) : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (base + r * kBlock < n_dyn) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) part[k] += v[r][k];
-      }
-    }
-  }
-  if (claim != nullptr && threadIdx.x == 0) *claim = 0u;
   block_sum_vec<K>(part, s_vec, tot);
   trace_tail<Epi>(1);
   if (threadIdx.x == 0) {
@@ -476,37 +421,14 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   // indices -> gathers chain is cut to indices -> gathers.  (Prefetching the
   // index stream too -- in registers or by cp.async -- costs occupancy or
   // data-pipe wavefronts and measured slower: profiles/r1_segpipe_experiments.md.)
-  // Static units u = warp, warp + nw, ... below n_static; then units claimed
-  // one ahead from p.claim (tree mode).  A warp's static terms are reduced
-  // into s_static before its first dynamic unit, each dynamic unit's terms
-  // into its own slot.
-  constexpr bool kDyn = !ORDERED && Epi::kReduce;
-  const int n_static = kDyn ? p.n_static : p.n_units;
-  __shared__ double s_static[kWarps][K];
-  bool flushed = false;
-  auto claim = [&]() -> int {
-    int c = 0;
-    if (lane == 0) c = static_cast<int>(atomicAdd(p.claim, 1u));
-    return n_static + __shfl_sync(0xffffffffu, c, 0);
-  };
   int u = blockIdx.x * kWarps + warp;
-  if (u >= n_static) u = n_static < p.n_units ? claim() : p.n_units;
   int4 d_next = u < p.n_units ? p.units[u] : make_int4(0, 0, 0, 0);
 #ifdef FOLP_WARP_TIMES
   unsigned long long work = 0;  // nnz | parts << 24 | tile segments << 36 | smid << 52
 #endif
-  while (u < p.n_units) {
+  for (; u < p.n_units; u += nw) {
     const int4 d = d_next;
-    int u_next = u + nw;
-    if (u < n_static && u_next >= n_static) u_next = n_static < p.n_units ? claim() : p.n_units;
-    if (u >= n_static) u_next = claim();
-    if (u_next < p.n_units) d_next = p.units[u_next];
-    if constexpr (kDyn) {
-      if (u >= n_static && !flushed) {  // the static share's terms
-        warp_flush<K>(acc.v, s_static[warp], lane);
-        flushed = true;
-      }
-    }
+    if (u + nw < p.n_units) d_next = p.units[u + nw];
     const int k0 = d.z, k1 = d.w;
 #ifdef FOLP_WARP_TIMES
     work += static_cast<unsigned long long>(k1 - k0) +
@@ -600,10 +522,6 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         }
       }
     }
-    if constexpr (kDyn) {
-      if (u >= n_static) warp_flush<K>(acc.v, p.dyn_slots + static_cast<size_t>(u - n_static) * K, lane);
-    }
-    u = u_next;
   }
 #ifdef FOLP_WARP_TIMES
   trace_warp<Epi>(1, global_ns());
@@ -617,20 +535,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
     if constexpr (ORDERED) {
       ordered_tail(epi, rb);
     } else {
-      if (!flushed) warp_flush<K>(acc.v, s_static[warp], lane);
-      __syncthreads();
-      double tot[K];
-      if (threadIdx.x == 0) {  // warps in order: block_sum_vec's association
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          double t = 0.0;
-#pragma unroll
-          for (int w = 0; w < kWarps; ++w) t += s_static[w][k];
-          tot[k] = t;
-        }
-      }
-      reduce_tail_tot(epi, tot, rb, p.n_multi, p.dyn_slots, p.n_units - n_static,
-                      n_static < p.n_units ? p.claim : nullptr);
+      reduce_tail(epi, acc.v, rb, p.n_multi);
     }
   }
 #ifdef FOLP_WARP_TIMES
