@@ -193,7 +193,7 @@ struct folp_gpu_ctx {
   double* eval_omega_d = nullptr;
   bool small_loop = false;        // k_chunk_cluster (tree mode, <= one unit per warp)
   double* small_multi = nullptr;  // its multi-part epilogue slots
-  int64_t ndg_count = 0, ndg_passes = 0, ndg_levels = 0;  // FOLP_TIMING statistics
+  int64_t ndg_count = 0, ndg_passes = 0, ndg_levels = 0, ndg_grid_passes = 0;  // FOLP_TIMING statistics
   void* loop_block = nullptr;  // K~ values + indices of CSR and CSC (one block)
   size_t loop_block_bytes = 0;
   double* prod = nullptr;      // two-phase products (gather_products_kernel), nnz + 8
@@ -381,9 +381,20 @@ struct folp_gpu_ctx {
 
   ~folp_gpu_ctx() {
     if (ndg_count > 0 && std::getenv("FOLP_TIMING") != nullptr) {
-      std::fprintf(stderr, "[folp timing] duality gaps %lld: %.1f passes, %.1f bisection levels each\n",
+      std::fprintf(stderr,
+                   "[folp timing] duality gaps %lld: %.1f passes (%.1f grid-wide), %.1f bisection levels each\n",
                    static_cast<long long>(ndg_count), static_cast<double>(ndg_passes) / ndg_count,
+                   static_cast<double>(ndg_grid_passes) / ndg_count,
                    static_cast<double>(ndg_levels) / ndg_count);
+#ifdef FOLP_BISECT_TIMES
+      unsigned long long bt[kBisectTimeSlots][3];
+      if (cudaMemcpyFromSymbol(bt, g_bisect_times, sizeof bt) == cudaSuccess) {
+        for (int k = 0; k < kBisectTimeSlots && bt[k][1] > 0; ++k) {
+          std::fprintf(stderr, "[folp timing] bisection pass %d: %.2f us avg over %llu launches (%llu alone)\n", k,
+                       1e-3 * static_cast<double>(bt[k][0]) / static_cast<double>(bt[k][1]), bt[k][1], bt[k][2]);
+        }
+      }
+#endif
     }
     if (device >= 0) cudaSetDevice(device);
     for (auto& e : chunk_exec)
@@ -878,6 +889,7 @@ int folp_gpu_evaluation_period(folp_gpu_ctx* c, double omega, int32_t want_gaps,
       out->gap[s] = c->ndg_h[s].result;
       c->ndg_count += 1;
       c->ndg_passes += c->ndg_h[s].passes;
+      c->ndg_grid_passes += c->ndg_h[s].grid_passes;
       c->ndg_levels += c->ndg_h[s].it;
     }
     out->gaps_valid = 1;

@@ -67,6 +67,7 @@ __global__ void k_ndg_init(NdgState* st, const double* sums, const double* dist,
 // once no block has any left, ndg_finish_analytic ends the bisection from
 // Q, H, S.
 constexpr int kBisectThreads = 512;
+constexpr int kBisectBatch = 4;  // tiles per super-tile in bisect_sweep
 // per set: ||d||_w^2 and g'd per midpoint over the active elements, the
 // number of active elements kept, and the running Q, H, S of the retired ones
 constexpr int kBisectVals = 2 * kNuCands + 4;
@@ -100,23 +101,50 @@ __device__ __forceinline__ int bisect_sweep(const BisectArgs& a, const NdgState&
                                             double (&acc)[2 * kNuCands], double& fq, double& fh,
                                             double& fs, int* wcount) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int R = kBisectBatch;
+  constexpr int W = kBisectThreads / 32;
   const double* g = a.g[s];
   const double* lo = a.lo[s];
   const double* hi = a.hi[s];
   const double omega = st.omega, winv = st.winv;
   int kept = 0;
-  for (int t0 = 0; t0 < cnt; t0 += kBisectThreads) {
-    const int k = t0 + tid;
-    int i = -1;
-    bool keep = false;
-    if (k < cnt) {
-      i = first ? static_cast<int>(b0 + k) : list[k];
-      const double gs = g[i];
-      if (gs != 0.0) {
+  // Super-tiles of R x kBisectThreads elements: every index, then every
+  // element load of the super-tile is issued before any is used (a pass over
+  // a few thousand elements is a chain of dependent L2 round trips
+  // otherwise), one barrier publishes the R tiles' keep counts, one more
+  // closes the compaction.  Thread tid still visits k = tid, tid + T, ... in
+  // order, so the sums and the kept list are those of a tile-by-tile sweep.
+  for (int t0 = 0; t0 < cnt; t0 += R * kBisectThreads) {
+    int iv[R];
+    double gv[R], lov[R], hiv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int k = t0 + r * kBisectThreads + tid;
+      iv[r] = k < cnt ? (first ? static_cast<int>(b0 + k) : list[k]) : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = iv[r];
+      gv[r] = 0.0;
+      lov[r] = 0.0;
+      hiv[r] = INFINITY;
+      if (i >= 0) {
+        gv[r] = g[i];
+        lov[r] = lo[i];
+        if (i < a.n) hiv[r] = hi[i];
+      }
+    }
+    unsigned keepmask = 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = iv[r];
+      const double gs = gv[r];
+      bool keep = false;
+      if (i >= 0 && gs != 0.0) {
         const bool primal = i < a.n;
         const double w = primal ? omega : winv;
-        const double los = lo[i];
-        const double his = primal ? hi[i] : INFINITY;
+        const double los = lov[r];
+        const double his = hiv[r];
         const int side = primal ? 0 : 1;
         const double ulo = gs * st.rcp_lo[side];  // |u| largest at nu_lo
         const double uhi = gs * st.rcp_hi[side];
@@ -139,21 +167,28 @@ __device__ __forceinline__ int bisect_sweep(const BisectArgs& a, const NdgState&
           }
         }
       }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) wcount[r * W + warp] = __popc(bal);
+      if (keep) keepmask |= 1u << r;
     }
-    // in-place, order-preserving compaction: every read of this tile
-    // precedes the barrier, every write lands below t0 + kBisectThreads
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) wcount[warp] = __popc(bal);
+    // in-place, order-preserving compaction: every read of this super-tile
+    // precedes the barrier, every write lands below t0 + R * kBisectThreads
     __syncthreads();
-    int off = kept, tile = 0;
+    int off = kept;
 #pragma unroll
-    for (int w = 0; w < kBisectThreads / 32; ++w) {
-      const int c = wcount[w];
-      if (w < warp) off += c;
-      tile += c;
+    for (int r = 0; r < R; ++r) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (keepmask >> r) & 1u);
+      int before = 0, tile = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int c = wcount[r * W + w];
+        if (w < warp) before += c;
+        tile += c;
+      }
+      if ((keepmask >> r) & 1u) list[off + before + __popc(bal & ((1u << lane) - 1u))] = iv[r];
+      off += tile;
     }
-    if (keep) list[off + __popc(bal & ((1u << lane) - 1u))] = i;
-    kept += tile;
+    kept = off;
     __syncthreads();
   }
   return kept;
@@ -165,7 +200,7 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
   __shared__ NdgState st[2];
   __shared__ double wsum[kBisectThreads / 32][2][kBisectVals];
   __shared__ double tot[2][kBisectVals];
-  __shared__ int wcount[kBisectThreads / 32];
+  __shared__ int wcount[kBisectBatch * kBisectThreads / 32];
   __shared__ int kept_count[2];
   __shared__ int s_off[2];
   __shared__ double base[2][3];  // block 0 alone: the grid's Q, H, S at the switch
@@ -182,6 +217,10 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
   double fq[2] = {0.0, 0.0}, fh[2] = {0.0, 0.0}, fs[2] = {0.0, 0.0};
   __syncthreads();
   bool first = true, alone = false;
+#ifdef FOLP_BISECT_TIMES
+  unsigned long long t_prev = global_ns();
+  int pass_no = 0;
+#endif
   for (int parity = 0;; parity ^= 1) {
     const bool run[2] = {st[0].done == 0, st[1].done == 0};
     if (!run[0] && !run[1]) break;  // same state in every block
@@ -262,12 +301,28 @@ __global__ void __launch_bounds__(kBisectThreads) k_ndg_bisect(BisectArgs a) {
         nsq[p] = tot[tid][2 * p] + (q + sf / (nu * nu));
         gd[p] = tot[tid][2 * p + 1] + (h + sf / nu);
       }
-      ndg_replay(&st[tid], nsq, gd, kNuLevels);
+      if (!alone) st[tid].grid_passes += 1;
+      ndg_replay(&st[tid], nsq, gd, kNuLevels, false);
       // no breakpoint inside this pass's bracket: none inside the narrower one
       if (!st[tid].done && tot[tid][2 * kNuCands] == 0.0) ndg_finish_analytic(&st[tid], q, h, sf);
     }
     first = false;
     __syncthreads();
+    // the next candidates' reciprocals, one division per thread
+    if (tid < 2 * kNdgRcp && run[tid / kNdgRcp] && !st[tid / kNdgRcp].done) {
+      ndg_reciprocal(&st[tid / kNdgRcp], tid % kNdgRcp);
+    }
+    __syncthreads();
+#ifdef FOLP_BISECT_TIMES
+    if (blockIdx.x == 0 && tid == 0 && pass_no < kBisectTimeSlots) {
+      const unsigned long long t = global_ns();
+      g_bisect_times[pass_no][0] += t - t_prev;
+      g_bisect_times[pass_no][1] += 1;
+      g_bisect_times[pass_no][2] += alone ? 1 : 0;
+      t_prev = t;
+    }
+    ++pass_no;
+#endif
     if (!alone && a.small_limit > 0) {
       // every block sees the same totals, so all take the same branch
       bool go = st[0].done == 0 || st[1].done == 0;
@@ -534,6 +589,9 @@ void enqueue_ndg_solve(folp_gpu_ctx* c, const bool (&want)[2], const double (&om
       // small programs would otherwise serialize on the whole GPU
       const int64_t want = (c->n + c->m + int64_t(kBisectThreads) * 4 - 1) / (int64_t(kBisectThreads) * 4);
       grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, want)));
+      if (const char* env = std::getenv("FOLP_BISECT_GRID")) {  // experiments
+        grid = std::max(1, std::min(grid, std::atoi(env)));
+      }
     }
     void* args[] = {&a};
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ndg_bisect),

@@ -1062,8 +1062,16 @@ struct NdgState {
   int32_t it;      // bisection iterations consumed (<= 200)
   int32_t done;
   int32_t passes;
-  int32_t pad;
+  int32_t grid_passes;  // tree-mode cooperative passes that synchronized the grid
 };
+
+#ifdef FOLP_BISECT_TIMES
+// Diagnostic build: block 0's %globaltimer at the start and after each pass,
+// summed per pass index over launches ([k][0] ns, [k][1] launches, [k][2]
+// launches in which block 0 ran pass k alone); read by the context's timing print.
+constexpr int kBisectTimeSlots = 32;
+__device__ unsigned long long g_bisect_times[kBisectTimeSlots][3];
+#endif
 
 // Heap-ordered tree of the next kNuLevels bisection midpoints below
 // [lo, hi]: node i covers [a_i, b_i] with nu_i = 0.5 * (a_i + b_i)
@@ -1126,7 +1134,7 @@ __device__ inline void ndg_finish_analytic(NdgState* st, double q, double h, dou
 // Replays `levels` levels of the reference bisection (solver.cpp:356-368)
 // from per-node sums (heap order) and leaves the next bracket.
 __device__ inline void ndg_replay(NdgState* st, const double* norm_sq, const double* gd,
-                                  int levels) {
+                                  int levels, bool reciprocals = true) {
   const double r = st->radius;
   const double r2 = r * r;
   double lo_ = st->nu_lo, hi_ = st->nu_hi;
@@ -1156,7 +1164,22 @@ __device__ inline void ndg_replay(NdgState* st, const double* norm_sq, const dou
   st->nu_lo = lo_;
   st->nu_hi = hi_;
   ndg_candidates(lo_, hi_, st->nu);
-  ndg_reciprocals(st);
+  if (reciprocals) ndg_reciprocals(st);
+}
+
+// ndg_reciprocals' value j (0..kNdgRcp-1) alone -- the same IEEE operations,
+// so threads can share the work.
+constexpr int kNdgRcp = 2 * kNuCands + 4;
+__device__ inline void ndg_reciprocal(NdgState* st, int j) {
+  if (j < kNuCands) {
+    st->rcp_primal[j] = 1.0 / (st->nu[j] * st->omega);
+  } else if (j < 2 * kNuCands) {
+    st->rcp_dual[j - kNuCands] = 1.0 / (st->nu[j - kNuCands] * st->winv);
+  } else if (j < 2 * kNuCands + 2) {
+    st->rcp_lo[j - 2 * kNuCands] = 1.0 / (st->nu_lo * (j == 2 * kNuCands ? st->omega : st->winv));
+  } else {
+    st->rcp_hi[j - 2 * kNuCands - 2] = 1.0 / (st->nu_hi * (j == 2 * kNuCands + 2 ? st->omega : st->winv));
+  }
 }
 
 // One bisection pass.  Tree mode: ||d(nu)||_w^2 and g'd(nu) for the 7 nodes
