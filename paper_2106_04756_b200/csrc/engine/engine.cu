@@ -162,6 +162,11 @@ struct folp_gpu_ctx {
   double *mp_ext, *mp_dy;  // Malitsky-Pock scratch
   double *kx_avg;   // K~ x of AVERAGE (filled by the duality gap)
   double *kx_aux;
+  double* kty_raw[2] = {nullptr, nullptr};  // tree mode: K'y of CURRENT / AVERAGE in a period
+  // the evaluation period's K'y cache for set s (tree mode, unsharded; else null)
+  double* kty_cache(int s) const {
+    return (!ordered && !sharded() && std::getenv("FOLP_NDG_RAW") == nullptr) ? kty_raw[s] : nullptr;
+  }
   double *xr, *yr;  // reduced point scratch
   double *g[2], *lo[2], *hi[2];  // duality-gap scratch per candidate (CURRENT, AVERAGE)
   double *partials;
@@ -568,6 +573,8 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       c->hi[s] = vn();
     }
     if (!c->ordered) {
+      c->kty_raw[0] = vn();
+      c->kty_raw[1] = vn();
       c->ndg_list = c->alloc<int>(2 * static_cast<size_t>(n + m) + 2);
       c->ndg_compact = c->alloc<int>(2 * static_cast<size_t>(kBisectSmall));
     }
@@ -860,11 +867,13 @@ int folp_gpu_evaluation_period(folp_gpu_ctx* c, double omega, int32_t want_gaps,
       CK(cudaStreamSynchronize(c->stream));
     } else {
       enqueue_average(c);
-      for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s]);
+      for (int s = 0; s < 2; ++s) {
+        enqueue_evaluate(c, slots[s], 0, kResEval[s], want_gaps ? c->kty_cache(s) : nullptr);
+      }
       if (want_gaps) {
         for (int s = 0; s < 2; ++s) {
           enqueue_distance(c, slots[s], FOLP_PT_LAST, kResDist[s]);
-          enqueue_ndg_setup(c, slots[s], s, omega);
+          enqueue_ndg_setup(c, slots[s], s, omega, c->kty_cache(s));
           enqueue_ndg_init(c, s, kResDist[s], 0.0, omega);
         }
         enqueue_ndg_solve(c, {true, true}, {omega, omega});

@@ -397,7 +397,8 @@ void enqueue_average(folp_gpu_ctx* c) {
 }
 
 // convergence_info reductions of a slot into the block at res[base].
-void enqueue_evaluate(folp_gpu_ctx* c, int which, int raw, int base) {
+// kty_out (tree mode): keep K'y of the presolved point for enqueue_ndg_setup.
+void enqueue_evaluate(folp_gpu_ctx* c, int which, int raw, int base, double* kty_out = nullptr) {
   OpEvalPoint op{};
   op.raw = raw != 0 ? 1 : 0;
   op.n = c->n;
@@ -419,6 +420,7 @@ void enqueue_evaluate(folp_gpu_ctx* c, int which, int raw, int base) {
   dres.q_dot_y = c->res + base + 1;
   dres.constant = c->objective_constant;
   dres.dual_objective = c->res + base + 10;
+  dres.kty_out = raw == 0 ? kty_out : nullptr;
   axis_product(c, false, false, dres, 9);
   if (!c->norms_ready) {
     c->ew(c->m, OpNormSq{c->q0, c->res + kResNorms}, 10);
@@ -456,14 +458,21 @@ void enqueue_distance(folp_gpu_ctx* c, int a, int b, int base) {
 // g, lo, hi of a slot into scratch set s with the setup sums
 // (solver.cpp:300-342); Kx of the point is cached for CURRENT and kept for
 // AVERAGE (a restart to it reuses it).
-void enqueue_ndg_setup(folp_gpu_ctx* c, int which, int s, double omega) {
+// kty_raw: K'y of the same point from enqueue_evaluate (tree mode), so the
+// working-space K~'y~ is D2 (K'y) elementwise instead of a column product.
+void enqueue_ndg_setup(folp_gpu_ctx* c, int which, int s, double omega,
+                       const double* kty_raw = nullptr) {
   const int64_t n = c->n, m = c->m;
   double* px = c->slot_x(which);
   double* py = c->slot_y(which);
   double* sums = c->res + kResNdg[s];
   EpiNdgPrimal ep{py, px, c->cw, c->lw, c->uw, omega, c->g[s], c->lo[s], c->hi[s], sums};
   if (c->capturing_eval) ep.omega_dev = c->eval_omega_d;
-  axis_product(c, false, true, ep, 13, 0);
+  if (kty_raw != nullptr) {
+    c->ew(n, OpNdgPrimalRaw{kty_raw, c->d2, ep}, 13, 0);
+  } else {
+    axis_product(c, false, true, ep, 13, 0);
+  }
   EpiNdgDual ed{};
   ed.x = px;
   ed.y = py;

@@ -855,6 +855,7 @@ struct EpiDualResidual {
   const double* q_dot_y;   // ordered mode: q'y from step 1
   double constant;         // ordered mode: objective constant
   double* dual_objective;  // ordered mode: q'y + const + sum bound*lambda
+  double* kty_out = nullptr;  // tree mode: K'y of the presolved point, kept for the gap setup
   __device__ bool prepare() { return true; }
   __device__ const double* vec() const { return yr; }
   struct Pre {
@@ -863,6 +864,7 @@ struct EpiDualResidual {
   __device__ Pre load(int j) const { return Pre{c[j], l[j], u[j]}; }
   template <class Acc>
   __device__ void apply(int j, double kty, const Pre& o, Acc& acc) const {
+    if (kty_out != nullptr) kty_out[j] = kty;
     const double r = o.c - kty;
     const double lj = o.l, uj = o.u;
     const bool has_lower = lj > -INFINITY;
@@ -1044,6 +1046,27 @@ struct OpNdgDualCached {
   __device__ void finalize_ordered(const double* t, int64_t m) const {
     e.finalize_ordered(t, m);
   }
+};
+
+// EpiNdgPrimal without touching K (tree mode): the working-space K~'y~ of
+// the point is D2 (K' y) with y = D1 y~ the presolved dual that
+// convergence_info has just multiplied (EpiDualResidual::kty_out) -- the
+// same product up to rounding, one elementwise pass instead of a column
+// product.
+struct OpNdgPrimalRaw {
+  static constexpr int K = 5;
+  static constexpr bool kReduce = true;
+  const double* kty_raw;
+  const double* d2;
+  EpiNdgPrimal e;
+  __device__ bool prepare() { return e.prepare(); }
+  template <class Acc>
+  __device__ void apply(int64_t j, Acc& acc) const {
+    const int jj = static_cast<int>(j);
+    e.apply(jj, d2[j] * kty_raw[j], e.load(jj), acc);
+  }
+  __device__ void finalize(const double (&tot)[K]) const { e.finalize(tot); }
+  __device__ void finalize_ordered(const double*, int64_t) const {}
 };
 
 // Bisection state of one normalized_duality_gap evaluation.

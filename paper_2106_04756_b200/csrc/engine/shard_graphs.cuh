@@ -208,10 +208,10 @@ void build_eval_graph(folp_gpu_ctx* c, int cur) {
     CK(cudaMemcpyAsync(c->eval_omega_d, c->eval_omega_h, sizeof(double), cudaMemcpyHostToDevice,
                        c->stream));
     enqueue_average(c);
-    for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s]);
+    for (int s = 0; s < 2; ++s) enqueue_evaluate(c, slots[s], 0, kResEval[s], c->kty_cache(s));
     for (int s = 0; s < 2; ++s) {
       enqueue_distance(c, slots[s], FOLP_PT_LAST, kResDist[s]);
-      enqueue_ndg_setup(c, slots[s], s, 1.0);
+      enqueue_ndg_setup(c, slots[s], s, 1.0, c->kty_cache(s));
       enqueue_ndg_init(c, s, kResDist[s], 0.0, 1.0);
     }
     enqueue_ndg_solve(c, {true, true}, {1.0, 1.0});
