@@ -19,6 +19,35 @@ struct ShardComm {
   virtual double max_scalar(double v, cudaStream_t s) = 0;
   // in-place: rows [bounds[r], bounds[r+1]) of buf from shard r, for every r
   virtual void gather_rows(double* buf, const std::vector<int64_t>& bounds, cudaStream_t s) = 0;
+
+  // Peer exchange -- the all-reduce of a trial's partial product fused into
+  // the product's epilogue: rank p's producer stores its partial straight
+  // into slot p of every rank's receive area (NVLink P2P stores on a
+  // multi-GPU node), peer_fence() waits until every rank's stores have
+  // landed, and each rank sums its W slots in rank order (so every rank
+  // holds bit-identical sums without a collective on the data).  Receive
+  // areas are double-buffered by exchange parity: a rank can run at most one
+  // exchange ahead of another (each fence waits for all producers).
+  bool peer = false;        // exchange through peer slots (peer_setup done)
+  int64_t peer_cap = 0;     // doubles per slot
+  double** peer_dst_d = nullptr;  // [2][W] device: slot `rank` of every rank's area
+  double** peer_src_d = nullptr;  // [2][W] device: this rank's W slots
+  virtual void peer_setup(int64_t count) { (void)count; }
+  virtual void peer_fence(cudaStream_t s) { (void)s; }
+  double* const* peer_dst(int parity) const { return peer_dst_d + parity * world; }
+  const double* const* peer_src(int parity) const { return peer_src_d + parity * world; }
+  // device pointer tables from host vectors ([2][W] each)
+  void upload_tables(const std::vector<double*>& dst, const std::vector<double*>& src) {
+    CK(cudaMalloc(&peer_dst_d, 2 * world * sizeof(double*)));
+    CK(cudaMalloc(&peer_src_d, 2 * world * sizeof(double*)));
+    CK(cudaMemcpy(peer_dst_d, dst.data(), 2 * world * sizeof(double*), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(peer_src_d, src.data(), 2 * world * sizeof(double*), cudaMemcpyHostToDevice));
+  }
+  void free_tables() {
+    if (peer_dst_d) cudaFree(peer_dst_d);
+    if (peer_src_d) cudaFree(peer_src_d);
+    peer_dst_d = peer_src_d = nullptr;
+  }
 };
 
 // NCCL, loaded at run time: the single-GPU path has no NCCL dependency, and
@@ -29,6 +58,7 @@ struct NcclApi {
   decltype(&ncclCommInitRank) comm_init_rank = nullptr;
   decltype(&ncclAllReduce) all_reduce = nullptr;
   decltype(&ncclBroadcast) bcast = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclCommDestroy) comm_destroy = nullptr;
@@ -46,6 +76,7 @@ const NcclApi& nccl_api() {
     api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
     api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
     api.bcast = reinterpret_cast<decltype(api.bcast)>(dlsym(h, "ncclBroadcast"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
     api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
     api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
@@ -79,9 +110,59 @@ struct NcclComm final : ShardComm {
     NCK(api.comm_init_rank(&comm, w, id, r));
     CK(cudaMalloc(&scratch, sizeof(double)));
   }
+  double* area = nullptr;             // own receive area [2][W][cap]
+  std::vector<double*> peer_areas;    // mapped areas of the other ranks (IPC)
   ~NcclComm() override {
+    for (size_t r = 0; r < peer_areas.size(); ++r) {
+      if (peer_areas[r] && static_cast<int>(r) != rank) cudaIpcCloseMemHandle(peer_areas[r]);
+    }
+    free_tables();
+    if (area) cudaFree(area);
     if (scratch) cudaFree(scratch);
     if (comm) nccl_api().comm_destroy(comm);
+  }
+  // Receive areas: allocated here, exported as CUDA IPC handles, the handles
+  // all-gathered through NCCL, the peers' areas opened with peer access.
+  void peer_setup(int64_t count) override {
+    const NcclApi& api = nccl_api();
+    if (api.all_gather == nullptr) throw EngineError(FOLP_E_RUNTIME, "ncclAllGather missing");
+    peer_cap = std::max<int64_t>(count, 1);
+    CK(cudaMalloc(&area, 2 * world * peer_cap * sizeof(double)));
+    cudaIpcMemHandle_t mine;
+    CK(cudaIpcGetMemHandle(&mine, area));
+    std::vector<cudaIpcMemHandle_t> all(world);
+    char* dev = nullptr;
+    CK(cudaMalloc(&dev, world * sizeof(cudaIpcMemHandle_t)));
+    CK(cudaMemcpy(dev + rank * sizeof(cudaIpcMemHandle_t), &mine, sizeof(mine), cudaMemcpyHostToDevice));
+    NCK(api.all_gather(dev + rank * sizeof(cudaIpcMemHandle_t), dev, sizeof(cudaIpcMemHandle_t),
+                       ncclUint8, comm, nullptr));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(all.data(), dev, world * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    peer_areas.assign(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) {
+        peer_areas[r] = area;
+      } else {
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess));
+        peer_areas[r] = static_cast<double*>(ptr);
+      }
+    }
+    std::vector<double*> dst(2 * world), src(2 * world);
+    for (int par = 0; par < 2; ++par) {
+      for (int r = 0; r < world; ++r) {
+        dst[par * world + r] = peer_areas[r] + (par * world + rank) * peer_cap;
+        src[par * world + r] = area + (par * world + r) * peer_cap;
+      }
+    }
+    upload_tables(dst, src);
+    peer = true;
+  }
+  // Every rank's producer has completed (and its P2P stores with it) once
+  // this one-element all-reduce completes on the stream.
+  void peer_fence(cudaStream_t s) override {
+    if (world > 1) NCK(nccl_api().all_reduce(scratch, scratch, 1, ncclFloat64, ncclSum, comm, s));
   }
   void allreduce_sum(double* buf, int64_t count, cudaStream_t s) override {
     if (count > 0) NCK(nccl_api().all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm, s));
@@ -162,12 +243,39 @@ struct LoopbackComm final : ShardComm {
     rank = r;
     world = group->world;
   }
+  double* area = nullptr;  // own receive area [2][W][cap]
   ~LoopbackComm() override {
     // a shard that leaves releases anyone still waiting (after the last
     // collective nobody waits; before it, waiting would never end)
     g->poison();
+    free_tables();
+    if (area) cudaFree(area);
     if (d_ptrs) cudaFree(d_ptrs);
     if (d_sum) cudaFree(d_sum);
+  }
+  // Same layout as the NCCL/IPC areas; on one GPU the peers' areas are
+  // plain device pointers published through the group.
+  void peer_setup(int64_t count) override {
+    peer_cap = std::max<int64_t>(count, 1);
+    CK(cudaMalloc(&area, 2 * world * peer_cap * sizeof(double)));
+    g->ptrs[rank] = area;
+    g->barrier();
+    std::vector<double*> dst(2 * world), src(2 * world);
+    for (int par = 0; par < 2; ++par) {
+      for (int r = 0; r < world; ++r) {
+        dst[par * world + r] = g->ptrs[r] + (par * world + rank) * peer_cap;
+        src[par * world + r] = area + (par * world + r) * peer_cap;
+      }
+    }
+    g->barrier();
+    upload_tables(dst, src);
+    peer = true;
+  }
+  // The producers of every shard have finished: no kernel ever waits on
+  // another shard's kernel (they share one GPU).
+  void peer_fence(cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));
+    g->barrier();
   }
   void allreduce_sum(double* buf, int64_t count, cudaStream_t s) override {
     CK(cudaStreamSynchronize(s));

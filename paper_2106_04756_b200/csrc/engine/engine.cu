@@ -217,6 +217,7 @@ struct folp_gpu_ctx {
   int* lcsc_pos = nullptr;            // local CSC entry -> full CSC position
   double* lcsc_val = nullptr;
   double* kty_part = nullptr;
+  int peer_parity = 0;  // receive-area parity of the next peer exchange
   double* shard_sums = nullptr;
   bool shard_values_ready = false;
   bool rows_dirty = false;            // partitioned vectors outside [r0, r1) stale
@@ -1366,6 +1367,16 @@ int folp_gpu_shard_attach(folp_gpu_ctx* c, const folp_gpu_shard* spec, const int
                c->col_part ? c->lrows : c->lcols);
     // row partition: partial K'y [n]; column partition: partial Kx' [m] + sx, bad
     c->kty_part = c->alloc<double>(std::max<int64_t>(c->col_part ? m + 2 : n, 1));
+    // FOLP_SHARD_EXCHANGE=peer|collective; default peer on the loopback
+    // group, collective (NCCL all-reduce) on NCCL until the P2P path has run
+    // on a multi-GPU node
+    {
+      const char* env = std::getenv("FOLP_SHARD_EXCHANGE");
+      bool peer = spec->backend == FOLP_SHARD_LOOPBACK;
+      if (env != nullptr && std::strcmp(env, "peer") == 0) peer = true;
+      if (env != nullptr && std::strcmp(env, "collective") == 0) peer = false;
+      if (peer) c->comm->peer_setup(c->col_part ? m + 2 : n);
+    }
     c->shard_sums = c->alloc<double>(4);
     c->shard_values_ready = false;
     c->rows_dirty = false;

@@ -350,6 +350,13 @@ struct EpiShardPart {
   double* out;
   const double* v;
   bool trial_x;
+  // peer exchange (ShardComm::peer): the partial goes straight to slot
+  // `rank` of all `world` receive areas; segment 0's unit also forwards the
+  // two primal sums kernel A left at extra[0..1] (column partition)
+  double* const* outs = nullptr;
+  int world = 0;
+  const double* extra = nullptr;
+  int64_t extra_at = 0;
   __device__ bool prepare() {
     if (!b.st->running) return false;
     v = trial_x ? pick(b.x, b.st->cur ^ 1) : pick(b.y, b.st->cur);
@@ -360,22 +367,42 @@ struct EpiShardPart {
   __device__ Pre load(int) const { return Pre{}; }
   template <class Acc>
   __device__ void apply(int j, double dot, const Pre&, Acc&) const {
-    out[j] = dot;
+    if (outs == nullptr) {
+      out[j] = dot;
+      return;
+    }
+    for (int r = 0; r < world; ++r) outs[r][j] = dot;
+    if (j == 0 && extra != nullptr) {
+      const double e0 = extra[0], e1 = extra[1];
+      for (int r = 0; r < world; ++r) {
+        outs[r][extra_at] = e0;
+        outs[r][extra_at + 1] = e1;
+      }
+    }
   }
   __device__ void finalize(const double (&)[K]) const {}
   __device__ void finalize_ordered(const double*, int64_t) const {}
 };
+
+// Sum of the `world` peer slots at i, in rank order (every rank the same).
+__device__ __forceinline__ double sum_slots(const double* const* src, int world, int64_t i) {
+  double v = src[0][i];
+  for (int r = 1; r < world; ++r) v += src[r][i];
+  return v;
+}
 
 struct OpShardPrimal {
   static constexpr int K = 2;
   static constexpr bool kReduce = true;
   EpiPrimal e;
   const double* kty;
+  const double* const* src = nullptr;  // peer exchange: the partials' slots
+  int world = 0;
   __device__ bool prepare() { return e.prepare(); }
   template <class Acc>
   __device__ void apply(int64_t j, Acc& acc) const {
     const int jj = static_cast<int>(j);
-    e.apply(jj, kty[jj], e.load(jj), acc);
+    e.apply(jj, src != nullptr ? sum_slots(src, world, j) : kty[jj], e.load(jj), acc);
   }
   __device__ void finalize(const double (&tot)[K]) const { e.finalize(tot); }
   __device__ void finalize_ordered(const double*, int64_t) const {}
@@ -404,17 +431,22 @@ struct OpShardDual {
   EpiDual e;
   const double* kx;
   const double* a_sums;  // global sx, bad of kernel A
+  const double* const* src = nullptr;  // peer exchange: slots [0, m) Kx', [m, m+2) sx, bad
+  int world = 0;
+  int64_t m = 0;
   __device__ bool prepare() { return e.prepare(); }
   template <class Acc>
   __device__ void apply(int64_t i, Acc& acc) const {
     const int ii = static_cast<int>(i);
-    e.apply(ii, kx[ii], e.load(ii), acc);
+    e.apply(ii, src != nullptr ? sum_slots(src, world, i) : kx[ii], e.load(ii), acc);
   }
   __device__ void finalize(const double (&tot)[K]) const {
     const DevState* st = e.b.st;
+    const double sx = src != nullptr ? sum_slots(src, world, m) : a_sums[0];
+    const double bad = src != nullptr ? sum_slots(src, world, m + 1) : a_sums[1];
     double movement = tot[1] / st->omega;  // solver.cpp:83, on the global sums
-    movement = movement + a_sums[0];
-    decide_trial(e.b, tot[0], movement, a_sums[1] != 0.0 || tot[2] != 0.0);
+    movement = movement + sx;
+    decide_trial(e.b, tot[0], movement, bad != 0.0 || tot[2] != 0.0);
   }
   __device__ void finalize_ordered(const double*, int64_t) const {}
 };

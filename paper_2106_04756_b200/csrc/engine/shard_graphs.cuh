@@ -84,6 +84,46 @@ void prep(folp_gpu_ctx* c) {
 // One sharded trial slot (see ops.cuh, "Row-sharded trial" and
 // "Column-sharded trial").
 void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
+  ShardComm& comm = *c->comm;
+  if (comm.peer) {  // the exchange fused into the partial product's epilogue
+    const int par = c->peer_parity;
+    c->peer_parity ^= 1;
+    if (c->col_part) {
+      EpiPrimal ep{b};
+      ep.shard_out = c->kty_part + c->m;  // partial sx, bad: forwarded by the producer
+      c->seg(c->lcols, c->csc_work, ep, 2);
+      EpiShardPart sp{b, c->kty_part, nullptr, true};
+      sp.outs = comm.peer_dst(par);
+      sp.world = comm.world;
+      sp.extra = c->kty_part + c->m;
+      sp.extra_at = c->m;
+      c->seg(c->lrows, c->lcsc_val, sp, 1);
+      comm.peer_fence(c->stream);
+      OpShardDual od{EpiDual{b}, nullptr, nullptr};
+      od.src = comm.peer_src(par);
+      od.world = comm.world;
+      od.m = c->m;
+      c->ew(c->m, od, 3);
+      return;
+    }
+    EpiShardPart sp{b, c->kty_part, nullptr, false};
+    sp.outs = comm.peer_dst(par);
+    sp.world = comm.world;
+    c->seg(c->lcols, c->lcsc_val, sp, 1);
+    comm.peer_fence(c->stream);
+    OpShardPrimal op{EpiPrimal{b}, nullptr};
+    op.src = comm.peer_src(par);
+    op.world = comm.world;
+    c->ew(c->n, op, 2);
+    EpiDual ed{b};
+    ed.shard_out = c->shard_sums;
+    c->seg(c->lrows, c->csr_work, ed, 3);
+    comm.allreduce_sum(c->shard_sums, 3, c->stream);
+    k_shard_decide<<<1, 1, 0, c->stream>>>(b, c->shard_sums);
+    ++c->launches;
+    CK(cudaGetLastError());
+    return;
+  }
   if (c->col_part) {
     EpiPrimal ep{b};
     ep.shard_out = c->kty_part + c->m;  // partial sx, bad ride with the partial Kx'

@@ -148,3 +148,48 @@ def test_nccl_world1_matches_single_gpu(eng):
         for u, v in ((xa, xb), (ya, yb)):
             worst = max(worst, float(np.max(np.abs(u - v) / np.maximum(1.0, np.abs(v)))))
     assert worst <= 1e-12
+
+
+@pytest.mark.parametrize("partition", ["rows", "cols"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_exchange_matches_collective(monkeypatch, world, partition):
+    """The exchange fused into the partial product's epilogue (each shard
+    stores its partial into slot `rank` of every shard's receive area, sums
+    in rank order) gives bit-identical solves to the loopback all-reduce
+    (which also sums in rank order) -- iterates, restarts and solutions."""
+    lp = instances.generate(5, 1, 0.01)
+    p = cabi.params(iteration_limit=600, record_iterate_trace=True)
+    monkeypatch.setenv("FOLP_SHARD_EXCHANGE", "peer")
+    peer = shard.solve_loopback(lp, world, p, partition=partition, iterate_capacity=50)
+    monkeypatch.setenv("FOLP_SHARD_EXCHANGE", "collective")
+    coll = shard.solve_loopback(lp, world, p, partition=partition, iterate_capacity=50)
+    _same(peer + coll)
+    for (ia, ea, xa, ya), (ib, eb, xb, yb) in zip(peer[0].iterate_trace, coll[0].iterate_trace):
+        assert ia == ib and ea == eb
+        assert np.array_equal(xa, xb) and np.array_equal(ya, yb)
+
+
+@pytest.mark.parametrize("partition", ["rows", "cols"])
+def test_nccl_world1_peer_exchange(eng, monkeypatch, partition):
+    """NCCL backend with FOLP_SHARD_EXCHANGE=peer at world size 1: the
+    receive area is exported as a CUDA IPC handle, all-gathered through
+    NCCL and the fence is the one-element all-reduce -- the multi-GPU code
+    path with a single peer (itself)."""
+    import torch.distributed as dist
+    monkeypatch.setenv("FOLP_SHARD_EXCHANGE", "peer")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        lp = instances.generate(1, 1, 1.0)
+        p = cabi.params(record_iterate_trace=True, iteration_limit=120)
+        a = shard.solve(lp, p, partition=partition, iterate_capacity=120)
+    finally:
+        dist.destroy_process_group()
+    b = eng.solve_lp(lp, p, iterate_capacity=120)
+    assert a.iterations == b.iterations == 120
+    assert a.restart_iterations == b.restart_iterations
+    worst = 0.0
+    for (ia, ea, xa, ya), (ib, eb, xb, yb) in zip(a.iterate_trace[:40], b.iterate_trace[:40]):
+        for u, v in ((xa, xb), (ya, yb)):
+            worst = max(worst, float(np.max(np.abs(u - v) / np.maximum(1.0, np.abs(v)))))
+    assert worst <= 1e-12

@@ -131,6 +131,18 @@ def _rank_main(rank, world, port, out):
         rows = np.repeat(np.arange(lp.num_rows), np.diff(lptr))
         kxp = np.zeros(lp.num_rows)
         np.add.at(kxp, rows, c.data[pos] * x[cols])
+        # peer exchange (FOLP_SHARD_EXCHANGE=peer): the partial lands in slot
+        # `rank` of every rank's receive area, each rank sums its slots in
+        # rank order -- identical sums everywhere without a data collective
+        area = [torch.zeros(lp.num_rows, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(area, torch.from_numpy(kxp.copy()))
+        peer = area[0].clone()
+        for r in range(1, world):
+            peer += area[r]
+        everyone = [torch.zeros(lp.num_rows, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(everyone, peer)
+        peer_ok = all(torch.equal(e, everyone[0]) for e in everyone)
+        peer_ok = peer_ok and float(np.max(np.abs(peer.numpy() - a @ x))) <= 1e-12 * (1 + np.max(np.abs(a @ x)))
         t = torch.from_numpy(kxp)
         dist.all_reduce(t)
         kx_ref = a @ x
@@ -144,7 +156,7 @@ def _rank_main(rank, world, port, out):
             dist.broadcast(seg, src=src)
             fx[int(bc[src]):int(bc[src + 1])] = seg
         x_exact = bool(np.array_equal(fx.numpy(), x))
-        out.put((rank, kty_err, kx_exact and x_exact and kx_err <= 1e-12, same, r1 - r0))
+        out.put((rank, kty_err, kx_exact and x_exact and kx_err <= 1e-12 and peer_ok, same, r1 - r0))
     finally:
         dist.destroy_process_group()
 
