@@ -115,6 +115,12 @@ typedef struct folp_gpu_eval {
 /* Context lifetime. device < 0 picks $FOLP_DEVICE (default 0). */
 int folp_gpu_create(const folp_gpu_problem* problem, int device,
                     folp_gpu_ctx** out);
+/* Same, with the working columns renumbered: working column j is the
+ * problem's column col_order[j] (a permutation of 0..n-1).  Every n-vector
+ * passed to or returned by the context is in working order (the host driver
+ * maps them).  Used for degree ordering of skewed columns (tree mode). */
+int folp_gpu_create_ordered(const folp_gpu_problem* problem, const int64_t* col_order, int device,
+                            folp_gpu_ctx** out);
 void folp_gpu_destroy(folp_gpu_ctx* ctx);
 
 /* rescale_problem (scaling.cpp:48-96) on device: ruiz_iterations Ruiz
@@ -239,6 +245,8 @@ int folp_gpu_multiply_transpose(folp_gpu_ctx* ctx, int32_t working,
  * the CPU reference; parity runs).  $FOLP_REDUCTION=ordered|tree overrides. */
 void folp_gpu_set_default_reduction(int32_t ordered);
 int32_t folp_gpu_reduction_ordered(const folp_gpu_ctx* ctx);
+/* The mode a context created now gets (the default, or $FOLP_REDUCTION). */
+int32_t folp_gpu_default_reduction(void);
 
 /* Kernel launches issued by this context so far (for bench accounting). */
 int64_t folp_gpu_launch_count(const folp_gpu_ctx* ctx);

@@ -448,6 +448,11 @@ extern "C" {
 const char* folp_gpu_last_error(void) { return g_err.c_str(); }
 
 int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
+  return folp_gpu_create_ordered(p, nullptr, device, out);
+}
+
+int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order, int device,
+                            folp_gpu_ctx** out) {
   *out = nullptr;
   return guarded([&] {
     if (p->num_rows < 0 || p->num_cols < 0 || p->nnz < 0 ||
@@ -475,10 +480,7 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     };
     std::unique_ptr<folp_gpu_ctx> c(new folp_gpu_ctx());
     c->device = pick_device(device);
-    c->ordered = g_default_ordered;
-    if (const char* env = std::getenv("FOLP_REDUCTION")) {
-      c->ordered = std::strcmp(env, "ordered") == 0;
-    }
+    c->ordered = folp_gpu_default_reduction() != 0;
     if (const char* env = std::getenv("FOLP_NO_COOP")) c->coop_ok = std::atoi(env) == 0;
     set_device(c.get());
     CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
@@ -499,7 +501,28 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     const int64_t *col_start = p->col_start, *col_rows = p->col_rows;
     const double* col_values = p->col_values;
     // No column mirror from the host: transpose on the device (below).
-    const bool device_csc = col_start == nullptr || col_rows == nullptr || col_values == nullptr;
+    const bool device_csc =
+        col_order != nullptr || col_start == nullptr || col_rows == nullptr || col_values == nullptr;
+    // working column j = caller's column col_order[j]: indices renumbered
+    // on device right after their upload, the CSC built from the
+    // renumbered CSR, c / l / u gathered (host vectors map at the boundary)
+    int* order_d = nullptr;
+    int* rank_d = nullptr;
+    if (col_order != nullptr && n > 0) {
+      std::vector<int> ord(static_cast<size_t>(n)), rnk(static_cast<size_t>(n), -1);
+      for (int64_t j = 0; j < n; ++j) {
+        const int64_t o = col_order[j];
+        if (o < 0 || o >= n || rnk[static_cast<size_t>(o)] >= 0) {
+          throw EngineError(FOLP_E_INVALID_ARGUMENT, "folp_gpu_create_ordered: not a permutation");
+        }
+        ord[static_cast<size_t>(j)] = static_cast<int>(o);
+        rnk[static_cast<size_t>(o)] = static_cast<int>(j);
+      }
+      order_d = c->alloc<int>(n);
+      rank_d = c->alloc<int>(n);
+      CK(cudaMemcpy(order_d, ord.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(rank_d, rnk.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+    }
 
     // value / index streams padded by 8 entries: bulk tiles are staged in
     // 16-byte-aligned windows that may run up to 3 entries past the end
@@ -526,6 +549,11 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
       try {
         upload_index(c.get(), p->row_start, c->csr_ptr, m + 1, stage, cap);
         upload_index(c.get(), p->row_cols, c->csr_col, nnz, stage, cap);
+        if (rank_d != nullptr && nnz > 0) {
+          k_renumber<<<c->simple_grid(nnz), kBlock, 0, c->stream>>>(c->csr_col, rank_d, nnz);
+          ++c->launches;
+          CK(cudaGetLastError());
+        }
         if (!device_csc) {
           upload_index(c.get(), col_start, c->csc_ptr, n + 1, stage, cap);
           upload_index(c.get(), col_rows, c->csc_row, nnz, stage, cap);
@@ -625,6 +653,14 @@ int folp_gpu_create(const folp_gpu_problem* p, int device, folp_gpu_ctx** out) {
     upload(c.get(), c->c0, p->objective, n);
     upload(c.get(), c->l0, p->variable_lower, n);
     upload(c.get(), c->u0, p->variable_upper, n);
+    if (order_d != nullptr) {
+      for (double* v : {c->c0, c->l0, c->u0}) {
+        copy_d2d(c.get(), c->xr, v, n);  // xr: scratch until the first evaluation
+        k_gather_order<<<c->simple_grid(n), kBlock, 0, c->stream>>>(c->xr, order_d, v, n);
+        ++c->launches;
+        CK(cudaGetLastError());
+      }
+    }
     upload(c.get(), c->q0, p->right_hand_side, m);
     // Identity scaling until folp_gpu_rescale: working problem = presolved.
     copy_d2d(c.get(), c->cw, c->c0, n);
@@ -1194,6 +1230,11 @@ int folp_gpu_debug_warp_times(folp_gpu_ctx* c, int32_t slot, uint64_t* out, int3
 void folp_gpu_set_default_reduction(int32_t ordered) { g_default_ordered = ordered != 0; }
 
 int32_t folp_gpu_reduction_ordered(const folp_gpu_ctx* c) { return c->ordered ? 1 : 0; }
+
+int32_t folp_gpu_default_reduction(void) {
+  if (const char* env = std::getenv("FOLP_REDUCTION")) return std::strcmp(env, "ordered") == 0 ? 1 : 0;
+  return g_default_ordered ? 1 : 0;
+}
 
 
 int folp_gpu_set_profiling(folp_gpu_ctx* c, int32_t enabled) {

@@ -239,6 +239,20 @@ __global__ void k_narrow(const int64_t* __restrict__ src, int* __restrict__ dst,
     dst[i] = static_cast<int>(src[i]);
 }
 
+// Working column numbering (folp_gpu_create_ordered): column indices
+// through rank[], n-vectors gathered through order[].
+__global__ void k_renumber(int* __restrict__ idx, const int* __restrict__ rank, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    idx[i] = rank[idx[i]];
+}
+__global__ void k_gather_order(const double* __restrict__ src, const int* __restrict__ order,
+                               double* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[order[i]];
+}
+
 // Start point (solver.cpp:853-865): z/D then projected.
 __global__ void k_start_point(int64_t n, int64_t m, int64_t m1, const double* x0,
                               const double* y0, const double* d1, const double* d2,

@@ -24,7 +24,7 @@ void raise(int code, const std::string& where) {
 }
 
 void Context::create(const SparseMatrix& k, const double* c, const double* q, const double* l,
-                     const double* u, Index m1, double constant) {
+                     const double* u, Index m1, double constant, const Index* col_order) {
   folp_gpu_problem p{};
   p.num_rows = k.num_rows();
   p.num_cols = k.num_cols();
@@ -55,15 +55,15 @@ void Context::create(const SparseMatrix& k, const double* c, const double* q, co
     zero_cols.assign(static_cast<std::size_t>(k.num_cols()) + 1, 0);
     p.col_start = zero_cols.data();
   }
-  check(folp_gpu_create(&p, -1, &ctx_), "device context");
+  check(folp_gpu_create_ordered(&p, col_order, -1, &ctx_), "device context");
   m_ = k.num_rows();
   n_ = k.num_cols();
 }
 
-Context::Context(const LinearProgram& lp) {
+Context::Context(const LinearProgram& lp, const Index* col_order) {
   create(lp.constraint_matrix, lp.objective.data(), lp.right_hand_side.data(),
          lp.variable_lower.data(), lp.variable_upper.data(), lp.num_inequality_rows,
-         lp.objective_constant);
+         lp.objective_constant, col_order);
 }
 
 Context::Context(const SparseMatrix& k) {

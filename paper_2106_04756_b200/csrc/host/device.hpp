@@ -29,7 +29,8 @@ ConvergenceInfo to_info(const folp_gpu_eval& e, double objective_constant);
 class Context {
  public:
   Context() = default;
-  explicit Context(const LinearProgram& lp);
+  // col_order: working column order (folp_gpu_create_ordered), or null
+  explicit Context(const LinearProgram& lp, const Index* col_order = nullptr);
   // Matrix-only context (vectors read as zeros).
   explicit Context(const SparseMatrix& k);
   ~Context();
@@ -51,7 +52,7 @@ class Context {
 
  private:
   void create(const SparseMatrix& k, const double* c, const double* q, const double* l,
-              const double* u, Index m1, double constant);
+              const double* u, Index m1, double constant, const Index* col_order = nullptr);
   folp_gpu_ctx* ctx_ = nullptr;
   Index m_ = 0;
   Index n_ = 0;

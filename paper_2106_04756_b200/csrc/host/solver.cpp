@@ -11,6 +11,7 @@
 #include "folp/solver.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -19,8 +20,11 @@
 #include <ostream>
 #include <random>
 #include <string>
+#include <thread>
 
 #include "device.hpp"
+#include "parallel.hpp"
+#include "sparse_access.hpp"
 #include "session.hpp"
 #include "folp/linalg.hpp"
 #include "folp/presolve.hpp"
@@ -175,6 +179,21 @@ class Driver {
   SolveResult finish_numerical_error();
   bool evaluate_and_maybe_restart(SolveResult& out);
   void record_iterate();
+  void order_columns();
+  // working-space column order (col_order_[i] = presolved column of working
+  // column i; empty: identity) and the maps of primal vectors across it
+  void primal_to_work(std::vector<double>& v) const {
+    if (col_order_.empty()) return;
+    std::vector<double> w(v.size());
+    for (std::size_t i = 0; i < w.size(); ++i) w[i] = v[static_cast<std::size_t>(col_order_[i])];
+    v.swap(w);
+  }
+  void primal_from_work(std::vector<double>& v) const {
+    if (col_order_.empty()) return;
+    std::vector<double> w(v.size());
+    for (std::size_t i = 0; i < w.size(); ++i) w[static_cast<std::size_t>(col_order_[i])] = v[i];
+    v.swap(w);
+  }
 
   const LinearProgram& raw_;
   SolverParams p_;
@@ -184,6 +203,8 @@ class Driver {
 
   PresolveTransform transform_;
   LinearProgram presolved_storage_;
+  std::vector<Index> col_order_;   // working column order on the device (empty: identity)
+  bool raw_on_device_ = false;      // the device matrix is raw K (column order aside)
   const LinearProgram* work_ = nullptr;  // the presolved LP (raw_ when identity)
   std::unique_ptr<device::Context> dev_;
   KktPassLedger ledger_;
@@ -228,9 +249,10 @@ SolveResult Driver::finish_point(TerminationReason reason, const PrimalDualPoint
   // raw K.  When presolve was the identity the device already holds raw K.
   std::vector<double> kty(static_cast<std::size_t>(raw_.num_variables()), 0.0);
   if (!kty.empty()) {
-    if (dev_ && transform_.is_identity() && work_ == &raw_) {
+    if (dev_ && transform_.is_identity() && raw_on_device_) {
       device::check(folp_gpu_multiply_transpose(ctx(), 0, full.dual.data(), kty.data()),
                     "reduced costs");
+      primal_from_work(kty);
     } else {
       raw_.constraint_matrix.multiply_transpose(full.dual, kty);
     }
@@ -257,6 +279,7 @@ SolveResult Driver::finish(TerminationReason reason, int slot, const Convergence
   reduced.dual.resize(static_cast<std::size_t>(work_->num_rows()));
   device::check(folp_gpu_get_reduced_point(ctx(), slot, reduced.primal.data(), reduced.dual.data()),
                 "reduced_point");
+  primal_from_work(reduced.primal);
   return finish_point(reason, reduced, info);
 }
 
@@ -324,6 +347,7 @@ void Driver::record_iterate() {
   rec.iteration = k_total_;
   rec.eta_used = last_eta_used_;
   rec.point = dev_->get_point(FOLP_PT_CURRENT);
+  primal_from_work(rec.point.primal);
   tmpl_.iterate_trace.push_back(std::move(rec));
 }
 
@@ -406,6 +430,56 @@ bool Driver::evaluate_and_maybe_restart(SolveResult& out) {
   return false;
 }
 
+// Column renumbering (tree mode, one context, $FOLP_HOT_COLUMNS=0 turns it
+// off, =1 forces it): when the column degrees are strongly skewed (config
+// 2's power law: max degree >= 16x the mean), the working columns are
+// ordered by descending degree, so the x gathers of K x concentrate on a
+// short hot prefix of x that stays in L1 (config 2: -5.9 % device time per
+// evaluation period, profiles/r1_session2_experiments.md).  Columns keep
+// their entries and rows their entry order (only the column numbers change),
+// so every row and column dot is the caller's.  The engine renumbers on
+// the device (folp_gpu_create_ordered); the host only computes the order and
+// maps primal vectors at the boundary.  Ordered mode keeps the reference's
+// order throughout.
+void Driver::order_columns() {
+  const char* env = std::getenv("FOLP_HOT_COLUMNS");
+  const int mode = env != nullptr ? std::atoi(env) : -1;
+  if (mode == 0 || shard_ != nullptr || folp_gpu_default_reduction() != 0) return;
+  const SparseMatrix& k = work_->constraint_matrix;
+  const Index n = work_->num_variables(), m = work_->num_rows(), nnz = k.nnz();
+  if (nnz == 0 || (mode != 1 && n < (Index(1) << 16))) return;
+  const std::span<const Index> start = k.row_start(), cols = k.row_cols();
+  // host threads for the O(nnz) passes (the e2e path pays for them): all
+  // cores, >= 64k entries each
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int nt = static_cast<int>(std::max<Index>(1, std::min<Index>({Index(hw), Index(16), nnz >> 16})));
+  auto split = [&](Index count, auto&& f) {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back([&, t] { f(count * t / nt, count * (t + 1) / nt, t); });
+    f(Index(0), count / nt, 0);
+    for (auto& th : pool) th.join();
+  };
+  std::vector<Index> deg(static_cast<std::size_t>(n), 0);
+  split(nnz, [&](Index b, Index e, int) {
+    for (Index q = b; q < e; ++q) {
+      std::atomic_ref<Index>(deg[static_cast<std::size_t>(cols[q])]).fetch_add(1, std::memory_order_relaxed);
+    }
+  });
+  const Index max_deg = *std::max_element(deg.begin(), deg.end());
+  if (mode != 1 && static_cast<double>(max_deg) < 16.0 * static_cast<double>(nnz) / static_cast<double>(n)) {
+    return;
+  }
+  // counting sort by descending degree, stable in the column index
+  std::vector<Index> first(static_cast<std::size_t>(max_deg) + 2, 0);
+  for (Index j = 0; j < n; ++j) ++first[static_cast<std::size_t>(max_deg - deg[j]) + 1];
+  for (std::size_t d = 1; d < first.size(); ++d) first[d] += first[d - 1];
+  col_order_.assign(static_cast<std::size_t>(n), 0);
+  for (Index j = 0; j < n; ++j) {
+    const Index r = first[static_cast<std::size_t>(max_deg - deg[j])]++;
+    col_order_[static_cast<std::size_t>(r)] = j;
+  }
+}
+
 SolveResult Driver::run() {  // solver.cpp:818-946
   if (auto done = start()) return std::move(*done);
   return std::move(*advance(std::numeric_limits<Index>::max()));
@@ -442,6 +516,9 @@ std::optional<SolveResult> Driver::start() {
   }
   mark("presolved");
   if (work_->num_variables() == 0) return finish_trivial();
+  raw_on_device_ = work_ == &raw_;
+  order_columns();
+  mark("columns ordered");
 
   if (p_.use_pock_chambolle) {
     const double a = p_.pc_alpha;
@@ -455,7 +532,7 @@ std::optional<SolveResult> Driver::start() {
     }
   }
 
-  dev_ = std::make_unique<device::Context>(*work_);
+  dev_ = std::make_unique<device::Context>(*work_, col_order_.empty() ? nullptr : col_order_.data());
   mark("context");
   device::check(folp_gpu_rescale(ctx(), p_.ruiz_iterations, p_.use_pock_chambolle ? 1 : 0,
                                  p_.pc_alpha, nullptr, nullptr),
@@ -464,7 +541,8 @@ std::optional<SolveResult> Driver::start() {
   if (shard_ != nullptr) dev_->attach_shard(work_->constraint_matrix, *shard_);
 
   // start point into the working space, projected (solver.cpp:853-865)
-  const PrimalDualPoint z = restrict_point(transform_, z0_.primal, z0_.dual);
+  PrimalDualPoint z = restrict_point(transform_, z0_.primal, z0_.dual);
+  primal_to_work(z.primal);
   device::check(folp_gpu_set_start(ctx(), z.primal.data(), z.dual.data()), "start point");
 
   double max_abs = 0.0, norm_c = 0.0, norm_q = 0.0;
@@ -478,7 +556,8 @@ std::optional<SolveResult> Driver::start() {
   if (p_.step_policy == StepPolicy::kConstant) {
     double norm = 0.0;
     if (has_entries) {
-      const std::vector<double> v0 = start_vector(work_->num_variables());
+      std::vector<double> v0 = start_vector(work_->num_variables());
+      primal_to_work(v0);
       int64_t mult = 0;
       device::check(folp_gpu_spectral_norm(ctx(), v0.data(), kPowerTol, kPowerMaxIters, &norm,
                                            &mult),
