@@ -446,25 +446,11 @@ void Driver::order_columns() {
   const int mode = env != nullptr ? std::atoi(env) : -1;
   if (mode == 0 || shard_ != nullptr || folp_gpu_default_reduction() != 0) return;
   const SparseMatrix& k = work_->constraint_matrix;
-  const Index n = work_->num_variables(), m = work_->num_rows(), nnz = k.nnz();
+  const Index n = work_->num_variables(), nnz = k.nnz();
   if (nnz == 0 || (mode != 1 && n < (Index(1) << 16))) return;
-  const std::span<const Index> start = k.row_start(), cols = k.row_cols();
-  // host threads for the O(nnz) passes (the e2e path pays for them): all
-  // cores, >= 64k entries each
-  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  const int nt = static_cast<int>(std::max<Index>(1, std::min<Index>({Index(hw), Index(16), nnz >> 16})));
-  auto split = [&](Index count, auto&& f) {
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back([&, t] { f(count * t / nt, count * (t + 1) / nt, t); });
-    f(Index(0), count / nt, 0);
-    for (auto& th : pool) th.join();
-  };
+  const std::span<const Index> cols = k.row_cols();
   std::vector<Index> deg(static_cast<std::size_t>(n), 0);
-  split(nnz, [&](Index b, Index e, int) {
-    for (Index q = b; q < e; ++q) {
-      std::atomic_ref<Index>(deg[static_cast<std::size_t>(cols[q])]).fetch_add(1, std::memory_order_relaxed);
-    }
-  });
+  host::parallel_histogram(cols.data(), nnz, n, deg.data());
   const Index max_deg = *std::max_element(deg.begin(), deg.end());
   if (mode != 1 && static_cast<double>(max_deg) < 16.0 * static_cast<double>(nnz) / static_cast<double>(n)) {
     return;
