@@ -280,6 +280,21 @@ struct folp_gpu_ctx {
   template <class Epi, bool ORD, bool PR>
   void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb) {
     auto fn = segdot_kernel<Epi, ORD, PR>;
+    // L1 / shared split: the smallest shared carveout that still holds
+    // kPlanCtasPerSm CTAs leaves the most L1 to the gathers (config 2
+    // 59.7 -> 57.6 us per trial, config 3 -1.7 %, config 5 +1.3 %; 25 % and
+    // below cost residency).  FOLP_CARVEOUT=% overrides, -1 = driver default.
+    static const bool carved = [&] {
+      const char* env = std::getenv("FOLP_CARVEOUT");
+      const int pct = env != nullptr ? std::atoi(env) : kSegdotCarveout;
+      if (pct >= 0) {
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                             cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        cudaGetLastError();
+      }
+      return true;
+    }();
+    (void)carved;
     if (!pdl) {
       fn<<<grid, kBlock, 0, stream>>>(sp, val, epi, rb);
       return;

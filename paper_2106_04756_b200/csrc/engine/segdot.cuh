@@ -56,6 +56,7 @@ constexpr int kSerialCap = 256;       // tree mode: longest segment one lane sum
 constexpr int kSingleMax = 1024;      // tree mode, large axes: longest one-warp segment
 constexpr int kPlanCtasPerSm = 4;     // the loop products' residency (64 registers)
 constexpr double kBalanceMin = 1.04;  // round-robin CTA load imbalance worth reordering
+constexpr int kSegdotCarveout = 36;   // % of the unified L1 as shared memory (engine.cu)
 
 // std::max / std::min semantics (NaN in `a` propagates), which the
 // reference's projections rely on for its NonFiniteIterate detection.
