@@ -218,6 +218,7 @@ struct folp_gpu_ctx {
   double* lcsc_val = nullptr;
   double* kty_part = nullptr;
   int peer_parity = 0;  // receive-area parity of the next peer exchange
+  bool hot_columns = false;  // created with a degree order (folp_gpu_create_ordered)
   double* shard_sums = nullptr;
   bool shard_values_ready = false;
   bool rows_dirty = false;            // partitioned vectors outside [r0, r1) stale
@@ -280,21 +281,25 @@ struct folp_gpu_ctx {
   template <class Epi, bool ORD, bool PR>
   void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb) {
     auto fn = segdot_kernel<Epi, ORD, PR>;
-    // L1 / shared split: the smallest shared carveout that still holds
-    // kPlanCtasPerSm CTAs leaves the most L1 to the gathers (config 2
-    // 59.7 -> 57.6 us per trial, config 3 -1.7 %, config 5 +1.3 %; 25 % and
-    // below cost residency).  FOLP_CARVEOUT=% overrides, -1 = driver default.
-    static const bool carved = [&] {
+    // L1 / shared split: for degree-ordered columns (a hot prefix of the
+    // gathered vector), the smallest shared carveout that still holds
+    // kPlanCtasPerSm CTAs leaves the most L1 to the gathers (config 2 59.7
+    // -> 57.6 us per trial); other layouts keep the driver's choice (config
+    // 4's window-blocked products lose 25 % with it, config 5 3 %).
+    // FOLP_CARVEOUT=% forces one split everywhere, -1 = driver default.
+    // (A function attribute: contexts of both kinds in one process only
+    // trade performance, never results.)
+    {
+      static int applied = -2;
       const char* env = std::getenv("FOLP_CARVEOUT");
-      const int pct = env != nullptr ? std::atoi(env) : kSegdotCarveout;
-      if (pct >= 0) {
+      const int want = env != nullptr ? std::atoi(env) : (hot_columns ? kSegdotCarveout : -1);
+      if (want != applied) {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                             cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+                             cudaFuncAttributePreferredSharedMemoryCarveout, want);
         cudaGetLastError();
+        applied = want;
       }
-      return true;
-    }();
-    (void)carved;
+    }
     if (!pdl) {
       fn<<<grid, kBlock, 0, stream>>>(sp, val, epi, rb);
       return;
@@ -535,6 +540,7 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
       }
       order_d = c->alloc<int>(n);
       rank_d = c->alloc<int>(n);
+      c->hot_columns = true;
       CK(cudaMemcpy(order_d, ord.data(), n * sizeof(int), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(rank_d, rnk.data(), n * sizeof(int), cudaMemcpyHostToDevice));
     }
