@@ -30,7 +30,8 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   // a warp (one "single part" unit, epilogue into the warp's accumulators)
   // instead of by one lane -- a lane walking up to 256 products in sequence
   // made the slowest warp of a power-law axis 40 % slower than the median
-  // (tools/warp_timeline.py).  FOLP_SERIAL_CAP overrides (256 = off).  Not
+  // (tools/warp_timeline.py).  FOLP_SERIAL_CAP overrides (256 = off; default
+  // kSerialCap).  Not
   // for small axes, whose plans may run in k_chunk_cluster.
   int64_t serial_cap = kWarpTile;
   // ... and segments up to single_max entries are one warp unit each (no
