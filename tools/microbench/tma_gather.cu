@@ -14,6 +14,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -254,7 +255,36 @@ int main(int argc, char** argv) {
     verify([&] { k_lsu<<<sms * 8, 256>>>(di, dx, nnz, dout); }, "lsu");
     for (int n_tma : {64, 256}) verify([&] { k_tma<<<sms * 8, kChunk>>>(map, di, dx, nnz, n_tma, dout); }, "tma");
     report("lsu", timeit([&] { k_lsu<<<sms * 8, 256>>>(di, dx, nnz, dout); }));
-    for (double f : {0.0, 0.1, 0.2, 0.3, 0.4}) {
+    {
+      // hot-first renumbering: vector entries ordered by how often they are
+      // gathered (descending), indices remapped -- the locality a degree
+      // ordering of the gathered axis would give
+      std::vector<int64_t> cnt(Xp, 0);
+      for (int64_t i = 0; i < nnz; ++i) ++cnt[i32[i]];
+      std::vector<int> order(Xp), rank(Xp);
+      for (int64_t i = 0; i < Xp; ++i) order[i] = (int)i;
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cnt[a] > cnt[b]; });
+      for (int64_t i = 0; i < Xp; ++i) rank[order[i]] = (int)i;
+      std::vector<int> ih(nnz);
+      for (int64_t i = 0; i < nnz; ++i) ih[i] = rank[i32[i]];
+      int* dh;
+      CK(cudaMalloc(&dh, nnz * 4));
+      CK(cudaMemcpy(dh, ih.data(), nnz * 4, cudaMemcpyHostToDevice));
+      report("lsu_hot", timeit([&] { k_lsu<<<sms * 8, 256>>>(dh, dx, nnz, dout); }));
+      for (int64_t win : {int64_t(4096), int64_t(32768), int64_t(262144)}) {
+        for (int64_t i = 0; i < nnz; ++i) ih[i] = (int)(i32[i] % win);
+        CK(cudaMemcpy(dh, ih.data(), nnz * 4, cudaMemcpyHostToDevice));
+        char name[32];
+        snprintf(name, sizeof name, "lsu_win%lldk", (long long)(win * 8 / 1024));
+        report(name, timeit([&] { k_lsu<<<sms * 8, 256>>>(dh, dx, nnz, dout); }));
+      }
+      cudaFree(dh);
+      // hot share: fraction of gathers landing in the first 4k / 32k entries
+      int64_t h1 = 0, h2 = 0;
+      for (int64_t i = 0; i < nnz; ++i) { h1 += rank[i32[i]] < 4096; h2 += rank[i32[i]] < 32768; }
+      printf("  gathers into the 4k / 32k hottest entries: %.1f %% / %.1f %%\n", 100.0 * h1 / nnz, 100.0 * h2 / nnz);
+    }
+    for (double f : {0.0}) {
       const int64_t nL = ((int64_t)((1.0 - f) * nnz) / 128) * 128;
       char name[32];
       verify([&] { k_mix<1><<<sms * 4, 256>>>(map, di, dx, nL, nnz, dout); }, "mix1");
@@ -265,7 +295,7 @@ int main(int argc, char** argv) {
       report(name, timeit([&] { k_mix<2><<<sms * 4, 256>>>(map, di, dx, nL, nnz, dout); }));
     }
     for (int ctas : {4}) {
-      for (int n_tma : {0, 64, 128, 192, 256}) {
+      for (int n_tma : {256}) {
         char name[32];
         snprintf(name, sizeof name, "tma%d/c%d", n_tma, ctas);
         report(name, timeit([&] { k_tma<<<sms * ctas, kChunk>>>(map, di, dx, nnz, n_tma, dout); }));
