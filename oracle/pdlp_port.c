@@ -29,6 +29,45 @@ static int fail(int code, const char* msg) {
 static double dmax(double a, double b) { return (a < b) ? b : a; } /* std::max */
 static double dmin(double a, double b) { return (b < a) ? b : a; } /* std::min */
 
+/* ------------------------------------------------------- summation order
+ * g_order selects how scalar reductions are folded.  0 (default) is the
+ * reference's sequential fold, bit-identical to the compiled reference.  The
+ * other orders exist ONLY to measure the reference's own reduction-order
+ * noise floor (tests/test_noise_floor.py, tools/noise_floor.py): same
+ * algorithm, same per-element terms, only the association of the sums
+ * changes, exactly what any parallel implementation must do.
+ *   1  pairwise tree over the terms (leaves of 8, sequential inside)
+ *   2  reversed sequential fold
+ *   3  like 1, and segment dots longer than 256 entries (K x rows / K'y
+ *      columns) summed as 256-entry sequential parts whose sums are then
+ *      folded in part order (a warp/part split of long segments)
+ */
+static int g_order = 0;
+
+static double psum(const double* t, int64_t n) {
+  if (n <= 8) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += t[i];
+    return s;
+  }
+  const int64_t h = n / 2;
+  return psum(t, h) + psum(t + h, n - h);
+}
+
+/* Fold of n terms t[i] in the order g_order selects (t is scratch). */
+static double fold(const double* t, int64_t n) {
+  if (g_order == 1 || g_order == 3) return psum(t, n);
+  double s = 0.0;
+  if (g_order == 2) {
+    for (int64_t i = n - 1; i >= 0; --i) s += t[i];
+  } else {
+    for (int64_t i = 0; i < n; ++i) s += t[i];
+  }
+  return s;
+}
+
+void folp_port_set_sum_order(int order) { g_order = order; }
+
 /* ---------------------------------------------------------------- mt19937_64 */
 typedef struct {
   uint64_t mt[312];
@@ -146,36 +185,60 @@ static void lp_free(Lp* p) {
 }
 
 /* sparse_matrix.cpp:106-119 */
-static void kx(const Lp* p, const double* x, double* out) {
-  for (int64_t r = 0; r < p->m; ++r) {
+static double seg_dot(const int64_t* idx, const double* val, int64_t b, int64_t e,
+                      const double* v) {
+  if (g_order == 3 && e - b > 256) {  /* 256-entry parts, part sums in order */
     double s = 0.0;
-    for (int64_t k = p->rs[r]; k < p->rs[r + 1]; ++k) s += p->rv[k] * x[p->rc[k]];
-    out[r] = s;
+    for (int64_t p0 = b; p0 < e; p0 += 256) {
+      double ps = 0.0;
+      const int64_t p1 = p0 + 256 < e ? p0 + 256 : e;
+      for (int64_t k = p0; k < p1; ++k) ps += val[k] * v[idx[k]];
+      s += ps;
+    }
+    return s;
   }
+  double s = 0.0;
+  for (int64_t k = b; k < e; ++k) s += val[k] * v[idx[k]];
+  return s;
+}
+
+static void kx(const Lp* p, const double* x, double* out) {
+  for (int64_t r = 0; r < p->m; ++r) out[r] = seg_dot(p->rc, p->rv, p->rs[r], p->rs[r + 1], x);
 }
 
 /* sparse_matrix.cpp:127-140 */
 static void kty(const Lp* p, const double* y, double* out) {
-  for (int64_t c = 0; c < p->n; ++c) {
-    double s = 0.0;
-    for (int64_t k = p->cs[c]; k < p->cs[c + 1]; ++k) s += p->cv[k] * y[p->cr[k]];
-    out[c] = s;
-  }
+  for (int64_t c = 0; c < p->n; ++c) out[c] = seg_dot(p->cr, p->cv, p->cs[c], p->cs[c + 1], y);
 }
 
 /* linalg.hpp:25-60 */
+static void* xmalloc(size_t bytes);
 static double dot(const double* a, const double* b, int64_t n) {
   double s = 0.0;
+  if (g_order) {
+    double* t = (double*)xmalloc((size_t)(n ? n : 1) * sizeof(double));
+    for (int64_t i = 0; i < n; ++i) t[i] = a[i] * b[i];
+    s = fold(t, n);
+    free(t);
+    return s;
+  }
   for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
   return s;
 }
-static double nsq(const double* v, int64_t n) {
-  double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += v[i] * v[i];
+static double nsq(const double* v, int64_t n) { return dot(v, v, n); }
+static double dsq_folded(const double* a, const double* b, int64_t n) {
+  double* t = (double*)xmalloc((size_t)(n ? n : 1) * sizeof(double));
+  for (int64_t i = 0; i < n; ++i) {
+    const double d = a[i] - b[i];
+    t[i] = d * d;
+  }
+  const double s = fold(t, n);
+  free(t);
   return s;
 }
 static double dnorm(const double* a, const double* b, int64_t n) {
   double s = 0.0;
+  if (g_order) return sqrt(dsq_folded(a, b, n));
   for (int64_t i = 0; i < n; ++i) {
     const double d = a[i] - b[i];
     s += d * d;
@@ -302,17 +365,21 @@ static int conv_info(const Lp* p, const double* x, const double* y, folp_info_c*
     info->dual_objective = v;
     info->gap_abs = fabs(info->dual_objective - info->primal_objective);
     double ps = 0.0;
+    double* tt = g_order ? dvec(p->m > p->n ? p->m : p->n) : NULL;
     for (int64_t r = 0; r < p->m; ++r) {
       double t = p->q[r] - kxv[r];
       if (r < p->m1) t = dmax(t, 0.0);
-      ps += t * t;
+      if (g_order) tt[r] = t * t; else ps += t * t;
     }
+    if (g_order) ps = fold(tt, p->m);
     info->primal_residual_norm = sqrt(ps);
     double ds = 0.0;
     for (int64_t i = 0; i < p->n; ++i) {
       const double t = res[i] - lam[i];
-      ds += t * t;
+      if (g_order) tt[i] = t * t; else ds += t * t;
     }
+    if (g_order) ds = fold(tt, p->n);
+    free(tt);
     info->dual_residual_norm = sqrt(ds);
     info->norm_q = sqrt(nsq(p->q, p->m));
     info->norm_c = sqrt(nsq(p->c, p->n));
@@ -351,10 +418,12 @@ static double ndg(const Lp* p, const double* x, const double* y, double radius, 
   }
   double gsq = 0.0;
   int any = 0;
+  double* tt = g_order ? dvec(tot) : NULL;
   for (int64_t s = 0; s < tot; ++s) {
     if (g[s] != 0.0) any = 1;
-    gsq += g[s] * g[s] / w[s];
+    if (g_order) tt[s] = g[s] * g[s] / w[s]; else gsq += g[s] * g[s] / w[s];
   }
+  if (g_order) gsq = fold(tt, tot);
   double result = 0.0;
   if (any) {
     int bounded = 1;
@@ -365,7 +434,10 @@ static double ndg(const Lp* p, const double* x, const double* y, double radius, 
     int done = 0;
     if (bounded) {
       double ns = 0.0;
-      for (int64_t s = 0; s < tot; ++s) ns += w[s] * d[s] * d[s];
+      for (int64_t s = 0; s < tot; ++s) {
+        if (g_order) tt[s] = w[s] * d[s] * d[s]; else ns += w[s] * d[s] * d[s];
+      }
+      if (g_order) ns = fold(tt, tot);
       if (sqrt(ns) <= radius * (1.0 + 1e-12)) {
         result = dot(g, d, tot) / radius;
         done = 1;
@@ -380,15 +452,16 @@ static double ndg(const Lp* p, const double* x, const double* y, double radius, 
         for (int64_t s = 0; s < tot; ++s) {
           const double un = g[s] / (nu * w[s]);
           d[s] = dmin(dmax(un, lo[s]), hi[s]);
-          ns += w[s] * d[s] * d[s];
+          if (g_order) tt[s] = w[s] * d[s] * d[s]; else ns += w[s] * d[s] * d[s];
         }
+        if (g_order) ns = fold(tt, tot);
         if (fabs(sqrt(ns) - radius) <= 1e-10 * radius) break;
         if (ns > r2) nlo = nu; else nhi = nu;
       }
       result = dot(g, d, tot) / radius;
     }
   }
-  free(ktyv); free(kxv); free(g); free(w); free(lo); free(hi); free(d);
+  free(ktyv); free(kxv); free(g); free(w); free(lo); free(hi); free(d); free(tt);
   return result;
 }
 
@@ -408,19 +481,40 @@ static int trial(const Lp* w, const double* x, const double* y, const double* kx
   }
   kx(w, t->xn, t->kxn);
   double cross = 0.0, mv = 0.0;
+  double* tc = g_order ? dvec(w->m) : NULL;
+  double* tm = g_order ? dvec(w->m > w->n ? w->m : w->n) : NULL;
   for (int64_t j = 0; j < w->m; ++j) {
     const double ex = 2.0 * t->kxn[j] - kxv[j];
     double v = y[j] + sigma * (w->q[j] - ex);
     if (j < w->m1) v = dmax(v, 0.0);
     t->yn[j] = v;
     const double dy = v - y[j];
+    if (g_order) {
+      tc[j] = dy * (kxv[j] - t->kxn[j]);
+      tm[j] = dy * dy;
+      continue;
+    }
     cross += dy * (kxv[j] - t->kxn[j]);
     mv += dy * dy;
   }
+  if (g_order) {
+    cross = fold(tc, w->m);
+    mv = fold(tm, w->m);
+  }
   mv /= omega;
-  for (int64_t i = 0; i < w->n; ++i) {
-    const double dx = t->xn[i] - x[i];
-    mv += omega * dx * dx;
+  if (g_order) {
+    for (int64_t i = 0; i < w->n; ++i) {
+      const double dx = t->xn[i] - x[i];
+      tm[i] = omega * dx * dx;
+    }
+    mv += fold(tm, w->n);
+    free(tc);
+    free(tm);
+  } else {
+    for (int64_t i = 0; i < w->n; ++i) {
+      const double dx = t->xn[i] - x[i];
+      mv += omega * dx * dx;
+    }
   }
   t->movement = mv;
   t->cross = cross;
@@ -690,6 +784,11 @@ static double primal_weight(const Solver* s, const double* nx, const double* ny,
 static double wnorm_diff(const Solver* s, const double* ax_, const double* ay_, const double* bx,
                          const double* by, double omega) {
   double sx = 0.0, sy = 0.0; /* weighted_norm of the difference (lp_model.cpp:167-173) */
+  if (g_order) {
+    sx = dsq_folded(ax_, bx, s->w.n);
+    sy = dsq_folded(ay_, by, s->w.m);
+    return sqrt(omega * sx + sy / omega);
+  }
   for (int64_t i = 0; i < s->w.n; ++i) {
     const double d = ax_[i] - bx[i];
     sx += d * d;

@@ -52,6 +52,11 @@ int folp_port_malitsky_pock_step(const folp_lp_c* lp, const double* x,
                                  double* x_next, double* y_next, double* eta_next,
                                  double* theta_next, int64_t* trials);
 const char* folp_port_last_error(void);
+/* Summation order of the scalar reductions: 0 = the reference's sequential
+ * fold (default, bit-exact); 1 pairwise tree, 2 reversed, 3 tree + 256-entry
+ * parts for long segment dots.  Non-zero orders only measure the reference's
+ * reduction-order noise floor (tools/noise_floor.py).  Process-global. */
+void folp_port_set_sum_order(int order);
 
 #ifdef __cplusplus
 }

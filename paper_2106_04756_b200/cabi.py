@@ -305,9 +305,11 @@ class Binding:
     # ---- high-level wrappers --------------------------------------------
     def solve_lp(self, lp: LP, p: Optional[dict] = None, x0=None, y0=None,
                  trace_capacity: int = 100000, iterate_capacity: int = 0,
-                 shard: Optional[ShardC] = None) -> SolveResult:
+                 shard: Optional[ShardC] = None, copy_iterates: bool = True) -> SolveResult:
         """folp_solve, or folp_solve_sharded as one row shard when `shard`
-        is given (see paper_2106_04756_b200/shard.py)."""
+        is given (see paper_2106_04756_b200/shard.py).  copy_iterates=False
+        returns the iterate trace as views into one buffer (full-size
+        traces: 100 iterates of config 5 are 12.8 GB)."""
         p = p or params()
         lpc = lp.to_c()
         pc = params_to_c(p)
@@ -354,8 +356,9 @@ class Binding:
                  for i in range(nt)]
         ni = min(res.num_iterates, icap)
         inn, imm = res.iterate_n, res.iterate_m
-        iters = [(int(i_it[i]), float(i_eta[i]), i_x[i * inn:(i + 1) * inn].copy(),
-                  i_y[i * imm:(i + 1) * imm].copy()) for i in range(ni)]
+        cp = (lambda a: a.copy()) if copy_iterates else (lambda a: a)
+        iters = [(int(i_it[i]), float(i_eta[i]), cp(i_x[i * inn:(i + 1) * inn]),
+                  cp(i_y[i * imm:(i + 1) * imm])) for i in range(ni)]
         return SolveResult(
             termination_reason=TERMINATION[res.termination_reason], primal_solution=x,
             dual_solution=y, reduced_costs=rc, final_info=res.final_info.as_dict(),
