@@ -243,6 +243,18 @@ int folp_gpu_multiply_transpose(folp_gpu_ctx* ctx, int32_t working,
  * differs from the reference's sums in the last bits), 1 = ordered (every
  * sum folded in the reference's sequential order: results bit-identical to
  * the CPU reference; parity runs).  $FOLP_REDUCTION=ordered|tree overrides. */
+/* Diagnostics / tests of the exact parallel fold (engine exactfold.cuh):
+ * folds `jobs` (1..4) host arrays terms[j][0..counts[j]) sequentially in
+ * index order -- s = inits[j]; s += t[i] -- bit-identically to the plain loop,
+ * in one cooperative launch of `grid` CTAs (0 = all co-resident).  A job with
+ * init_from[j] = k >= 0 (k < j) starts from results[k] / init_div[j] instead
+ * (the movement sum of solver.cpp:81-88).  reps > 0 also times that many
+ * launches (ms = mean per launch).  Not part of the solve path. */
+int folp_gpu_test_exact_fold(int32_t device, int32_t jobs, const double* const* terms,
+                             const int64_t* counts, const double* inits,
+                             const int32_t* init_from, const double* init_div,
+                             int32_t grid, int32_t reps, double* results, double* ms);
+
 void folp_gpu_set_default_reduction(int32_t ordered);
 int32_t folp_gpu_reduction_ordered(const folp_gpu_ctx* ctx);
 /* The mode a context created now gets (the default, or $FOLP_REDUCTION). */

@@ -47,6 +47,7 @@
 
 #include "folp_gpu.h"
 #include "ops.cuh"
+#include "exactfold.cuh"
 
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
@@ -275,6 +276,50 @@ struct folp_gpu_ctx {
   }
   RedBuf red(int counter) { return RedBuf{partials, counters + counter, nullptr, 0}; }
 
+  // exact parallel fold (exactfold.cuh) of ordered mode's trial sums
+  FoldScratch fold{};
+  int fold_grid = 0;         // co-resident CTAs of k_exact_fold (0: not available)
+  bool defer_tail = false;   // ordered products store terms only (the fold finalizes)
+  double* oprod = nullptr;   // ordered mode: long-segment products (warp_exact_fold)
+  void alloc_fold() {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_exact_fold<FinTrial>, kFoldBlock, 0) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      return;
+    }
+    const int G = std::min(sms * per_sm, 1024);
+    fold.cap = G;
+    fold.cta_sum = alloc<double>(static_cast<size_t>(kFoldMaxJobs) * G);
+    fold.cta_abs = alloc<double>(static_cast<size_t>(kFoldMaxJobs) * G);
+    fold.cta_ntot = alloc<unsigned long long>(static_cast<size_t>(kFoldMaxJobs) * G);
+    fold.cta_nbp = alloc<int>(static_cast<size_t>(kFoldMaxJobs) * G);
+    fold.cta_bad = alloc<int>(static_cast<size_t>(kFoldMaxJobs) * G);
+    fold.cta_flag = alloc<int>(G);
+    fold.bps = alloc<FoldBp>(static_cast<size_t>(kFoldMaxJobs) * G * kFoldBpCap);
+    fold.results = alloc<double>(kFoldMaxJobs);
+    fold.counter = alloc<unsigned>(1);
+    CK(cudaMemsetAsync(fold.counter, 0, sizeof(unsigned), stream));
+    fold_grid = G;
+  }
+  // the trial's three folds + decision (replaces EpiDual::finalize_ordered)
+  void launch_trial_fold(const LoopBufs& b) {
+    FoldJobs fj{};
+    fj.count = 3;
+    fj.job[0] = FoldJob{terms[1], m, 0.0, -1, 1.0, nullptr};           // cross (solver.cpp:80)
+    fj.job[1] = FoldJob{terms[1] + m, m, 0.0, -1, 1.0, nullptr};       // sum dy^2 (:81)
+    fj.job[2] = FoldJob{terms[0], n, 0.0, 1, 1.0, &st_d->omega};       // /omega + sum omega dx^2 (:83-88)
+    fj.flag[0] = terms[0] + n;
+    fj.flag_n[0] = n;
+    fj.flag[1] = terms[1] + 2 * m;
+    fj.flag_n[1] = m;
+    FinTrial fin{b};
+    void* args[] = {&fj, &fold, &fin};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_exact_fold<FinTrial>),
+                                   dim3(fold_grid), dim3(kFoldBlock), args, 0, stream));
+    ++launches;
+  }
+
   // Launch of a segdot kernel; with `pdl` (the PDHG loop's products, see
   // segdot.cuh griddep_wait) as a programmatic dependent launch.
   bool pdl = false;
@@ -323,6 +368,8 @@ struct folp_gpu_ctx {
     if (ordered) {
       rb.terms = terms[region];
       rb.nterm = p.sp.S;
+      rb.defer = defer_tail ? 1 : 0;
+      rb.scratch = oprod;
       auto fn = segdot_kernel<Epi, true>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
@@ -632,6 +679,13 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
     if (c->ordered) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);
       c->terms[1] = c->alloc<double>(5 * (n + m) + 8);
+      // exact parallel folds of the trial sums (exactfold.cuh); FOLP_EXACT_FOLD=0
+      // keeps the one-thread sequential folds
+      const char* env = std::getenv("FOLP_EXACT_FOLD");
+      if (env == nullptr || std::atoi(env) != 0) {
+        c->alloc_fold();
+        c->oprod = c->alloc<double>(static_cast<size_t>(nnz) + 8);
+      }
     }
     {
       const char* env = std::getenv("FOLP_SMALL_LOOP");
@@ -1135,6 +1189,79 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     loop->last_movement = st->movement;
     loop->last_cross = st->cross;
     loop->slots = st->slots;
+  });
+}
+
+// Test / measurement entry of the exact parallel fold (exactfold.cuh): up to
+// kFoldMaxJobs folds of host arrays in one cooperative launch; reps > 0
+// times `reps` launches with CUDA events (ms = average per launch).
+int folp_gpu_test_exact_fold(int32_t device, int32_t jobs, const double* const* terms,
+                             const int64_t* counts, const double* inits, const int32_t* init_from,
+                             const double* init_div, int32_t grid, int32_t reps, double* results,
+                             double* ms) {
+  return guarded([&] {
+    if (jobs < 1 || jobs > kFoldMaxJobs) throw std::invalid_argument("test_exact_fold: 1..4 jobs");
+    CK(cudaSetDevice(device));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<void*> mem;
+    auto dev = [&](size_t bytes) {
+      void* p = nullptr;
+      CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+      mem.push_back(p);
+      return p;
+    };
+    FoldJobs fj{};
+    fj.count = jobs;
+    for (int j = 0; j < jobs; ++j) {
+      double* d = static_cast<double*>(dev(counts[j] * sizeof(double)));
+      if (counts[j] > 0) CK(cudaMemcpyAsync(d, terms[j], counts[j] * sizeof(double), cudaMemcpyHostToDevice, st));
+      fj.job[j] = FoldJob{d, counts[j], inits[j], init_from ? init_from[j] : -1,
+                          init_div ? init_div[j] : 1.0, nullptr};
+      if (fj.job[j].init_from >= j) throw std::invalid_argument("test_exact_fold: init_from must precede");
+    }
+    int dev_sms = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+    auto fn = k_exact_fold<FoldToMemory>;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFoldBlock, 0));
+    const int cap = dev_sms * per_sm;
+    const int G = grid > 0 ? std::min(grid, cap) : cap;
+    FoldScratch sc{};
+    sc.cap = G;
+    sc.cta_sum = static_cast<double*>(dev(sizeof(double) * kFoldMaxJobs * G));
+    sc.cta_abs = static_cast<double*>(dev(sizeof(double) * kFoldMaxJobs * G));
+    sc.cta_ntot = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * kFoldMaxJobs * G));
+    sc.cta_nbp = static_cast<int*>(dev(sizeof(int) * kFoldMaxJobs * G));
+    sc.cta_bad = static_cast<int*>(dev(sizeof(int) * kFoldMaxJobs * G));
+    sc.cta_flag = static_cast<int*>(dev(sizeof(int) * G));
+    sc.bps = static_cast<FoldBp*>(dev(sizeof(FoldBp) * kFoldMaxJobs * G * kFoldBpCap));
+    sc.results = static_cast<double*>(dev(sizeof(double) * kFoldMaxJobs));
+    sc.counter = static_cast<unsigned*>(dev(sizeof(unsigned)));
+    CK(cudaMemsetAsync(sc.counter, 0, sizeof(unsigned), st));
+    FoldToMemory fin{};
+    void* args[] = {&fj, &sc, &fin};
+    auto launch = [&] {
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(G), dim3(kFoldBlock), args, 0, st));
+    };
+    launch();
+    CK(cudaMemcpyAsync(results, sc.results, sizeof(double) * jobs, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (reps > 0 && ms != nullptr) {
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, st));
+      for (int r = 0; r < reps; ++r) launch();
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, e0, e1));
+      *ms = static_cast<double>(t) / reps;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    for (void* p : mem) cudaFree(p);
+    cudaStreamDestroy(st);
   });
 }
 

@@ -329,6 +329,19 @@ struct EpiDual {
   }
 };
 
+// Ordered mode's trial decision after the exact parallel folds
+// (exactfold.cuh k_exact_fold): jobs {cross = sum dy*(Kx-Kx') over m,
+// sum dy^2 over m, movement = (sum dy^2)/omega + sum omega*dx^2 over n},
+// each the reference's sequential fold bit for bit (solver.cpp:76-88);
+// flag arrays = kernel A's and kernel B's non-finite markers (:91-93).
+struct FinTrial {
+  LoopBufs b;
+  __device__ bool prepare() const { return __ldcg(&b.st->running) != 0; }
+  __device__ void finalize(const double* r, int, bool flagged) const {
+    decide_trial(b, r[0], r[2], flagged);
+  }
+};
+
 // ---------------------------------------------------------------------
 // Row-sharded trial (north_star: K row-partitioned across the
 // GPUs, all-reduce of the partial K'y and of the scalar reductions).  Rank p

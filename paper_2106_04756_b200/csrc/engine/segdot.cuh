@@ -44,6 +44,8 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+#include "exactfold.cuh"
+
 namespace folpgpu {
 
 constexpr int kBlock = 256;
@@ -92,6 +94,10 @@ struct RedBuf {
   unsigned* counter;  // zero between launches (reset by the last block)
   double* terms;      // ordered mode: [K * nterm] per-segment terms
   int64_t nterm;      // ordered mode: segment (element) count
+  int defer = 0;      // ordered mode: only store the terms; a k_exact_fold launch
+                      // folds them and runs the finalize (exactfold.cuh)
+  double* scratch = nullptr;  // ordered mode: [nnz] products of long segments
+                              // (warp_exact_fold); null = one lane folds them
 };
 
 // Reduction sinks.  Tree mode accumulates in registers (fast, deterministic
@@ -437,8 +443,18 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
             (d.x < 0 ? (1ull << 24) : (static_cast<unsigned long long>(d.y - d.x) << 36));
 #endif
     if (d.x >= 0 && k1 - k0 > kWarpTile) {
-      // ordered plan: one long segment, summed by one lane in index order
-      if (lane == 0) {
+      // ordered plan: one long segment, its dot the reference's sequential
+      // sum in index order -- by the whole warp through the exact fold
+      // (products staged in rb.scratch), or by one lane
+      if (rb.scratch != nullptr) {
+        for (int k = k0 + lane; k < k1; k += 32) {
+          rb.scratch[k] = PROD ? val[k] : val[k] * __ldg(&vec[idx[k]]);
+        }
+        __syncwarp();
+        const double sum = warp_exact_fold(rb.scratch + k0, k1 - k0, 0.0, wbuf);
+        if (lane == 0) epi.apply(d.x, sum, epi.load(d.x), acc);
+        __syncwarp();
+      } else if (lane == 0) {
         double sum = 0.0;
         for (int k = k0; k < k1; ++k) sum += PROD ? val[k] : val[k] * vec[idx[k]];
         epi.apply(d.x, sum, epi.load(d.x), acc);
@@ -535,7 +551,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
 #endif
   if constexpr (Epi::kReduce) {
     if constexpr (ORDERED) {
-      ordered_tail(epi, rb);
+      if (!rb.defer) ordered_tail(epi, rb);
     } else {
       reduce_tail(epi, acc.v, rb, p.n_multi);
     }

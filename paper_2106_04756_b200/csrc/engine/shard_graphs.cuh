@@ -158,11 +158,18 @@ void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
     // previous one drains (FOLP_PDL=0 disables)
     const char* env = std::getenv("FOLP_PDL");
     c->pdl = env == nullptr || std::atoi(env) > 0;
+    // ordered mode: the products only store their terms; one cooperative
+    // k_exact_fold folds them exactly in the reference's order and decides
+    const bool fold = c->ordered && c->fold_grid > 0 && !c->sharded();
     try {
+      c->defer_tail = fold;
       axis_product(c, false, true, EpiPrimal{b}, 2, 0);
       axis_product(c, true, true, EpiDual{b}, 3, 1);
+      c->defer_tail = false;
+      if (fold) c->launch_trial_fold(b);
     } catch (...) {
       c->pdl = false;
+      c->defer_tail = false;
       throw;
     }
     c->pdl = false;

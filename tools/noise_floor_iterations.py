@@ -1,0 +1,79 @@
+"""Iteration-count spread of the REFERENCE ALGORITHM under re-associated sums
+(test infrastructure; companion of tools/noise_floor.py).
+
+For each instance: the compiled reference (sequential folds) and the C
+restatement with sum orders 1 (pairwise tree) and 2 (reversed fold) solve to
+the default 1e-8; the script prints iterations, termination, restart count,
+relative KKT and objective deviation of each re-associated run against the
+reference.  Same instance set as profiles/r1_tree_mode_iteration_spread.txt.
+
+    python tools/noise_floor_iterations.py [--jobs 8] [--out f.jsonl]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import sys
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+FAMILIES = [(5, 0.01), (5, 0.02), (3, 0.0005), (2, 0.01), (4, 0.0001), (1, 0.3)]
+
+
+def one(case):
+    cfg, scale, seed = case
+    from _parity import rel_kkt
+    from oracle import port, ref
+    from paper_2106_04756_b200 import instances
+    lp = instances.generate(cfg, seed, scale)
+    want = ref.binding().solve_lp(lp, trace_capacity=4096)
+    lib = port.binding().lib
+    lib.folp_port_set_sum_order.argtypes = [C.c_int]
+    row = {"config": cfg, "scale": scale, "seed": seed,
+           "ref": {"termination": want.termination_reason, "iterations": want.iterations,
+                   "restarts": want.restarts, "rel_kkt": rel_kkt(want.final_info),
+                   "objective": want.final_info["primal_objective"]}}
+    for order in (1, 2):
+        lib.folp_port_set_sum_order(order)
+        try:
+            got = port.binding().solve_lp(lp, trace_capacity=4096)
+        finally:
+            lib.folp_port_set_sum_order(0)
+        o = want.final_info["primal_objective"]
+        row[f"order{order}"] = {
+            "termination": got.termination_reason, "iterations": got.iterations,
+            "restarts": got.restarts, "rel_kkt": rel_kkt(got.final_info),
+            "iter_dev": (got.iterations - want.iterations) / max(1, want.iterations),
+            "objective_rel_dev": abs(got.final_info["primal_objective"] - o) / max(1.0, abs(o)),
+        }
+    return row
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--jobs", type=int, default=8)
+    ap.add_argument("--seeds", type=int, default=6)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    cases = [(c, s, seed) for c, s in FAMILIES for seed in range(1, a.seeds + 1)]
+    with ProcessPoolExecutor(a.jobs) as ex:
+        rows = list(ex.map(one, cases))
+    for r in rows:
+        print(f"cfg{r['config']} x{r['scale']} seed {r['seed']}: ref {r['ref']['termination']} "
+              f"{r['ref']['iterations']}  tree-order {r['order1']['termination']} "
+              f"{r['order1']['iterations']} ({100 * r['order1']['iter_dev']:+.1f}%)  reversed "
+              f"{r['order2']['termination']} {r['order2']['iterations']} "
+              f"({100 * r['order2']['iter_dev']:+.1f}%)")
+    if a.out:
+        with open(a.out, "w") as f:
+            for r in rows:
+                f.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()
