@@ -283,12 +283,14 @@ struct folp_gpu_ctx {
   double* oprod = nullptr;   // ordered mode: long-segment products (warp_exact_fold)
   void alloc_fold() {
     int per_sm = 0;
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(k_exact_fold<FinTrial>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFoldDynSmem));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, k_exact_fold<FinTrial>, kFoldBlock, 0) != cudaSuccess || per_sm < 1) {
+            &per_sm, k_exact_fold<FinTrial>, kFoldBlock, kFoldDynSmem) != cudaSuccess || per_sm < 1) {
       cudaGetLastError();
       return;
     }
-    const int G = std::min(sms * per_sm, 1024);
+    const int G = std::min(sms * per_sm, kFoldMaxCtas);
     fold.cap = G;
     fold.cta_sum = alloc<double>(static_cast<size_t>(kFoldMaxJobs) * G);
     fold.cta_abs = alloc<double>(static_cast<size_t>(kFoldMaxJobs) * G);
@@ -296,19 +298,52 @@ struct folp_gpu_ctx {
     fold.cta_nbp = alloc<int>(static_cast<size_t>(kFoldMaxJobs) * G);
     fold.cta_bad = alloc<int>(static_cast<size_t>(kFoldMaxJobs) * G);
     fold.cta_flag = alloc<int>(G);
+    fold.cta_laste = alloc<int>(static_cast<size_t>(kFoldMaxJobs) * G);
+    fold.cta_lastc = alloc<unsigned long long>(static_cast<size_t>(kFoldMaxJobs) * G);
     fold.bps = alloc<FoldBp>(static_cast<size_t>(kFoldMaxJobs) * G * kFoldBpCap);
+    fold.chain = alloc<FoldEntry>(static_cast<size_t>(kFoldMaxJobs) * (static_cast<size_t>(G) * kFoldBpCap + 1));
     fold.results = alloc<double>(kFoldMaxJobs);
     fold.counter = alloc<unsigned>(1);
     CK(cudaMemsetAsync(fold.counter, 0, sizeof(unsigned), stream));
     fold_grid = G;
   }
+  // Ordered finalize of E through the exact parallel fold: e's stored terms
+  // (t, nterm as finalize_ordered sees them) folded by k_exact_fold<FinExact<E>>.
+  template <class E>
+  void launch_exact(const E& e, const double* t, int64_t nterm) {
+    using Fin = FinExact<E>;
+    const void* fn = reinterpret_cast<const void*>(k_exact_fold<Fin>);
+    static std::mutex mu;
+    static std::unordered_map<int, int> grid_of;  // device -> co-resident CTAs
+    int G = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = grid_of.find(device);
+      if (it == grid_of.end()) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kFoldDynSmem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFoldBlock, kFoldDynSmem));
+        it = grid_of.emplace(device, std::max(1, per_sm) * sms).first;
+      }
+      G = std::min(it->second, fold.cap);
+    }
+    FoldJobs fj{};
+    e.fold_plan(t, nterm, fj);
+    Fin fin{e};
+    void* args[] = {&fj, &fold, &fin};
+    CK(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kFoldBlock), args, kFoldDynSmem, stream));
+    ++launches;
+  }
+
   // the trial's three folds + decision (replaces EpiDual::finalize_ordered)
   void launch_trial_fold(const LoopBufs& b) {
     FoldJobs fj{};
     fj.count = 3;
-    fj.job[0] = FoldJob{terms[1], m, 0.0, -1, 1.0, nullptr};           // cross (solver.cpp:80)
-    fj.job[1] = FoldJob{terms[1] + m, m, 0.0, -1, 1.0, nullptr};       // sum dy^2 (:81)
-    fj.job[2] = FoldJob{terms[0], n, 0.0, 1, 1.0, &st_d->omega};       // /omega + sum omega dx^2 (:83-88)
+    fj.job[0] = FoldJob{terms[1], m, 0.0, -1, 1.0, nullptr, nullptr};      // cross (solver.cpp:80)
+    fj.job[1] = FoldJob{terms[1] + m, m, 0.0, -1, 1.0, nullptr, nullptr};  // sum dy^2 (:81)
+    fj.job[2] = FoldJob{terms[0], n, 0.0, 1, 1.0, &st_d->omega, nullptr};  // /omega + sum omega dx^2 (:83-88)
+    fj.nflags = 2;
     fj.flag[0] = terms[0] + n;
     fj.flag_n[0] = n;
     fj.flag[1] = terms[1] + 2 * m;
@@ -316,7 +351,7 @@ struct folp_gpu_ctx {
     FinTrial fin{b};
     void* args[] = {&fj, &fold, &fin};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_exact_fold<FinTrial>),
-                                   dim3(fold_grid), dim3(kFoldBlock), args, 0, stream));
+                                   dim3(fold_grid), dim3(kFoldBlock), args, kFoldDynSmem, stream));
     ++launches;
   }
 
@@ -370,10 +405,16 @@ struct folp_gpu_ctx {
       rb.nterm = p.sp.S;
       rb.defer = defer_tail ? 1 : 0;
       rb.scratch = oprod;
+      bool exact = false;
+      if constexpr (HasFoldPlan<Epi>::value) exact = fold_grid > 0 && !defer_tail;
+      if (exact) rb.defer = 1;
       auto fn = segdot_kernel<Epi, true>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, true, false>(grid, p.sp, val, epi, rb);
+      if constexpr (HasFoldPlan<Epi>::value) {
+        if (exact) launch_exact(epi, terms[region], p.sp.S);
+      }
     } else if (prod != nullptr && (&p == &rows || &p == &cols)) {
       // two phases (segdot.cuh): gathers over the whole axis, then the
       // segmented sums and the epilogue over the product stream
@@ -402,9 +443,15 @@ struct folp_gpu_ctx {
     if (ordered) {
       rb.terms = terms[region];
       rb.nterm = count;
+      bool exact = false;
+      if constexpr (HasFoldPlan<Op>::value) exact = fold_grid > 0;
+      if (exact) rb.defer = 1;
       auto fn = elementwise_kernel<Op, true>;
       const int grid = ew_grid(count, reinterpret_cast<const void*>(fn));
       fn<<<grid, kBlock, 0, stream>>>(count, op, rb);
+      if constexpr (HasFoldPlan<Op>::value) {
+        if (exact) launch_exact(op, terms[region], count);
+      }
     } else {
       auto fn = elementwise_kernel<Op, false>;
       const int grid = ew_grid(count, reinterpret_cast<const void*>(fn));
@@ -468,6 +515,14 @@ struct folp_gpu_ctx {
         }
       }
 #endif
+    }
+    if (fold_grid > 0 && std::getenv("FOLP_FOLD_TIMES") != nullptr) {
+      unsigned long long tt[8];
+      if (cudaMemcpyFromSymbol(tt, g_fold_times, sizeof tt) == cudaSuccess) {
+        std::fprintf(stderr, "[fold times us, last trial] phase1 %.2f sync %.2f phase2 %.2f ticket %.2f lists %.2f replay %.2f\n",
+                     1e-3 * (tt[1] - tt[0]), 1e-3 * (tt[2] - tt[1]), 1e-3 * (tt[3] - tt[2]),
+                     1e-3 * (double)(long long)(tt[4] - tt[3]), 1e-3 * (tt[5] - tt[4]), 1e-3 * (tt[6] - tt[5]));
+      }
     }
     if (device >= 0) cudaSetDevice(device);
     for (auto& e : chunk_exec)
@@ -1217,15 +1272,17 @@ int folp_gpu_test_exact_fold(int32_t device, int32_t jobs, const double* const* 
       double* d = static_cast<double*>(dev(counts[j] * sizeof(double)));
       if (counts[j] > 0) CK(cudaMemcpyAsync(d, terms[j], counts[j] * sizeof(double), cudaMemcpyHostToDevice, st));
       fj.job[j] = FoldJob{d, counts[j], inits[j], init_from ? init_from[j] : -1,
-                          init_div ? init_div[j] : 1.0, nullptr};
+                          init_div ? init_div[j] : 1.0, nullptr, nullptr};
       if (fj.job[j].init_from >= j) throw std::invalid_argument("test_exact_fold: init_from must precede");
     }
     int dev_sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
     auto fn = k_exact_fold<FoldToMemory>;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFoldBlock, 0));
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(kFoldDynSmem)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFoldBlock, kFoldDynSmem));
     const int cap = dev_sms * per_sm;
-    const int G = grid > 0 ? std::min(grid, cap) : cap;
+    const int G = std::min(grid > 0 ? std::min(grid, cap) : cap, kFoldMaxCtas);
     FoldScratch sc{};
     sc.cap = G;
     sc.cta_sum = static_cast<double*>(dev(sizeof(double) * kFoldMaxJobs * G));
@@ -1234,14 +1291,18 @@ int folp_gpu_test_exact_fold(int32_t device, int32_t jobs, const double* const* 
     sc.cta_nbp = static_cast<int*>(dev(sizeof(int) * kFoldMaxJobs * G));
     sc.cta_bad = static_cast<int*>(dev(sizeof(int) * kFoldMaxJobs * G));
     sc.cta_flag = static_cast<int*>(dev(sizeof(int) * G));
+    sc.cta_laste = static_cast<int*>(dev(sizeof(int) * kFoldMaxJobs * G));
+    sc.cta_lastc = static_cast<unsigned long long*>(dev(sizeof(unsigned long long) * kFoldMaxJobs * G));
     sc.bps = static_cast<FoldBp*>(dev(sizeof(FoldBp) * kFoldMaxJobs * G * kFoldBpCap));
+    sc.chain = static_cast<FoldEntry*>(dev(sizeof(FoldEntry) * kFoldMaxJobs * (static_cast<size_t>(G) * kFoldBpCap + 1)));
     sc.results = static_cast<double*>(dev(sizeof(double) * kFoldMaxJobs));
     sc.counter = static_cast<unsigned*>(dev(sizeof(unsigned)));
     CK(cudaMemsetAsync(sc.counter, 0, sizeof(unsigned), st));
     FoldToMemory fin{};
     void* args[] = {&fj, &sc, &fin};
     auto launch = [&] {
-      CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(G), dim3(kFoldBlock), args, 0, st));
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(G), dim3(kFoldBlock), args,
+                                     kFoldDynSmem, st));
     };
     launch();
     CK(cudaMemcpyAsync(results, sc.results, sizeof(double) * jobs, cudaMemcpyDeviceToHost, st));
@@ -1259,6 +1320,14 @@ int folp_gpu_test_exact_fold(int32_t device, int32_t jobs, const double* const* 
       *ms = static_cast<double>(t) / reps;
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
+    }
+    if (const char* env = std::getenv("FOLP_FOLD_TIMES")) {
+      (void)env;
+      unsigned long long tt[8];
+      CK(cudaMemcpyFromSymbol(tt, g_fold_times, sizeof tt));
+      std::fprintf(stderr, "[fold times us] phase1 %.2f sync %.2f phase2 %.2f ticket %.2f lists %.2f replay %.2f\n",
+                   1e-3 * (tt[1] - tt[0]), 1e-3 * (tt[2] - tt[1]), 1e-3 * (tt[3] - tt[2]),
+                   1e-3 * (double)(long long)(tt[4] - tt[3]), 1e-3 * (tt[5] - tt[4]), 1e-3 * (tt[6] - tt[5]));
     }
     for (void* p : mem) cudaFree(p);
     cudaStreamDestroy(st);

@@ -337,8 +337,8 @@ struct EpiDual {
 struct FinTrial {
   LoopBufs b;
   __device__ bool prepare() const { return __ldcg(&b.st->running) != 0; }
-  __device__ void finalize(const double* r, int, bool flagged) const {
-    decide_trial(b, r[0], r[2], flagged);
+  __device__ void finalize(const double* r, int, unsigned flags) const {
+    decide_trial(b, r[0], r[2], flags != 0u);
   }
 };
 
@@ -808,6 +808,16 @@ struct EpiStoreDotNorm {
     result[0] = fold(0.0, t, n);
     result[1] = fold(0.0, t + n, n);
   }
+  // ordered mode through the exact parallel fold (exactfold.cuh)
+  __host__ void fold_plan(const double* t, int64_t n, FoldJobs& f) const {
+    f.count = 2;
+    f.job[0] = FoldJob{t, n, 0.0, -1, 1.0, nullptr, nullptr};
+    f.job[1] = FoldJob{t + n, n, 0.0, -1, 1.0, nullptr, nullptr};
+  }
+  __device__ void finalize_exact(const double* r, unsigned) const {
+    result[0] = r[0];
+    result[1] = r[1];
+  }
 };
 
 // ---------------------------------------------------------------------
@@ -858,6 +868,20 @@ struct OpEvalPoint {
     result[1] = fold(0.0, t + tot + n, m);  // linalg::dot(q, y)
     result[2] = any_nonzero(t + 2 * tot, tot) ? 1.0 : 0.0;
   }
+  __host__ void fold_plan(const double* t, int64_t tot, FoldJobs& f) const {
+    f.count = 2;
+    f.job[0] = FoldJob{t, n, 0.0, -1, 1.0, nullptr, nullptr};
+    f.job[1] = FoldJob{t + tot + n, m, 0.0, -1, 1.0, nullptr, nullptr};
+    f.nflags = 1;
+    f.flag[0] = t + 2 * tot;
+    f.flag_n[0] = tot;
+    f.flag_group[0] = 0;
+  }
+  __device__ void finalize_exact(const double* r, unsigned flags) const {
+    result[0] = r[0];
+    result[1] = r[1];
+    result[2] = (flags & 1u) ? 1.0 : 0.0;
+  }
 };
 
 // Step 2 (rows, original values): primal residual (termination.cpp:54-61).
@@ -884,6 +908,11 @@ struct EpiPrimalResidual {
   __device__ void finalize_ordered(const double* t, int64_t m) const {
     result[0] = fold(0.0, t, m);
   }
+  __host__ void fold_plan(const double* t, int64_t m, FoldJobs& f) const {
+    f.count = 1;
+    f.job[0] = FoldJob{t, m, 0.0, -1, 1.0, nullptr, nullptr};
+  }
+  __device__ void finalize_exact(const double* r, unsigned) const { result[0] = r[0]; }
 };
 
 // Step 3 (columns, original values): reduced costs, dual residual and the
@@ -954,6 +983,24 @@ struct EpiDualResidual {
       if (bt != 0.0) v += bt;
     }
     *dual_objective = v;
+  }
+  // The bound terms are folded including the zero ones (the reference skips
+  // lambda == 0): adding +0.0 changes a partial sum only when it is -0.0, so
+  // the two agree except possibly in the sign of an exactly-zero objective.
+  __host__ void fold_plan(const double* t, int64_t nn, FoldJobs& f) const {
+    f.count = 2;
+    f.job[0] = FoldJob{t, nn, 0.0, -1, 1.0, nullptr, nullptr};
+    f.job[1] = FoldJob{t + nn, nn, constant, -1, 1.0, nullptr, q_dot_y};
+    f.nflags = 1;
+    f.flag[0] = t + 2 * nn;
+    f.flag_n[0] = nn;
+    f.flag_group[0] = 0;
+  }
+  __device__ void finalize_exact(const double* r, unsigned flags) const {
+    result[0] = r[0];
+    result[1] = 0.0;
+    result[2] = (flags & 1u) ? 1.0 : 0.0;
+    *dual_objective = r[1];
   }
 };
 
@@ -1073,6 +1120,28 @@ struct EpiNdgDual {
     result[4] = fold(fold(0.0, p + 4 * n, n), t + 4 * m, m);  // linalg::dot(g, d)
     for (int k = 5; k < 10; ++k) result[k] = 0.0;
   }
+  __host__ void fold_plan(const double* t, int64_t m, FoldJobs& f) const {
+    const double* p = primal_terms;
+    f.count = 6;
+    for (int h = 0; h < 3; ++h) {  // (x; y) folds of terms 1, 3, 4
+      const int k = h == 0 ? 1 : h + 2;
+      f.job[2 * h] = FoldJob{p + k * n, n, 0.0, -1, 1.0, nullptr, nullptr};
+      f.job[2 * h + 1] = FoldJob{t + k * m, m, 0.0, 2 * h, 1.0, nullptr, nullptr};
+    }
+    f.nflags = 4;
+    f.flag[0] = p;          f.flag_n[0] = n; f.flag_group[0] = 0;  // g != 0
+    f.flag[1] = t;          f.flag_n[1] = m; f.flag_group[1] = 0;
+    f.flag[2] = p + 2 * n;  f.flag_n[2] = n; f.flag_group[2] = 1;  // non-finite corner
+    f.flag[3] = t + 2 * m;  f.flag_n[3] = m; f.flag_group[3] = 1;
+  }
+  __device__ void finalize_exact(const double* r, unsigned flags) const {
+    result[0] = (flags & 1u) ? 1.0 : 0.0;
+    result[1] = r[1];
+    result[2] = (flags & 2u) ? 1.0 : 0.0;
+    result[3] = r[3];
+    result[4] = r[5];
+    for (int k = 5; k < 10; ++k) result[k] = 0.0;
+  }
 };
 
 // Same as EpiNdgDual but with Kx already cached (the loop keeps Kx of the
@@ -1091,6 +1160,8 @@ struct OpNdgDualCached {
   __device__ void finalize_ordered(const double* t, int64_t m) const {
     e.finalize_ordered(t, m);
   }
+  __host__ void fold_plan(const double* t, int64_t m, FoldJobs& f) const { e.fold_plan(t, m, f); }
+  __device__ void finalize_exact(const double* r, unsigned flags) const { e.finalize_exact(r, flags); }
 };
 
 // EpiNdgPrimal without touching K (tree mode): the working-space K~'y~ of
@@ -1311,6 +1382,12 @@ struct OpNdgPass {
     const double gd = fold(0.0, t + tot_n, tot_n);
     ndg_replay(ns, &norm_sq, &gd, 1);
   }
+  __host__ void fold_plan(const double* t, int64_t tot_n, FoldJobs& f) const {
+    f.count = 2;
+    f.job[0] = FoldJob{t, tot_n, 0.0, -1, 1.0, nullptr, nullptr};
+    f.job[1] = FoldJob{t + tot_n, tot_n, 0.0, -1, 1.0, nullptr, nullptr};
+  }
+  __device__ void finalize_exact(const double* r, unsigned) const { ndg_replay(ns, &r[0], &r[1], 1); }
 };
 
 // ---------------------------------------------------------------------
@@ -1344,6 +1421,15 @@ struct OpDistance {
   __device__ void finalize_ordered(const double* t, int64_t tot) const {
     result[0] = fold(0.0, t, n);
     result[1] = fold(0.0, t + tot + n, tot - n);
+  }
+  __host__ void fold_plan(const double* t, int64_t tot, FoldJobs& f) const {
+    f.count = 2;
+    f.job[0] = FoldJob{t, n, 0.0, -1, 1.0, nullptr, nullptr};
+    f.job[1] = FoldJob{t + tot + n, tot - n, 0.0, -1, 1.0, nullptr, nullptr};
+  }
+  __device__ void finalize_exact(const double* r, unsigned) const {
+    result[0] = r[0];
+    result[1] = r[1];
   }
 };
 
@@ -1397,5 +1483,20 @@ struct OpAverage {
   __device__ void finalize(const double (&)[K]) const {}
   __device__ void finalize_ordered(const double*, int64_t) const {}
 };
+
+// Ordered mode through the exact parallel fold: an epilogue / operator with
+// fold_plan (host: the folds of its stored terms) and finalize_exact
+// (device: the same results as finalize_ordered) is finalized by a
+// k_exact_fold<FinExact<E>> launch instead of one thread's sequential folds.
+template <class E>
+struct FinExact {
+  E e;
+  __device__ bool prepare() { return e.prepare(); }
+  __device__ void finalize(const double* r, int, unsigned flags) const { e.finalize_exact(r, flags); }
+};
+template <class E, class = void>
+struct HasFoldPlan : std::false_type {};
+template <class E>
+struct HasFoldPlan<E, std::void_t<decltype(&E::fold_plan)>> : std::true_type {};
 
 }  // namespace folpgpu

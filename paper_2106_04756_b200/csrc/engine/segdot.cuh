@@ -447,11 +447,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       // sum in index order -- by the whole warp through the exact fold
       // (products staged in rb.scratch), or by one lane
       if (rb.scratch != nullptr) {
-        for (int k = k0 + lane; k < k1; k += 32) {
-          rb.scratch[k] = PROD ? val[k] : val[k] * __ldg(&vec[idx[k]]);
-        }
-        __syncwarp();
-        const double sum = warp_exact_fold(rb.scratch + k0, k1 - k0, 0.0, wbuf);
+        const double sum = warp_exact_dot<PROD>(val, idx, vec, k0, k1, wbuf);
         if (lane == 0) epi.apply(d.x, sum, epi.load(d.x), acc);
         __syncwarp();
       } else if (lane == 0) {
@@ -705,7 +701,7 @@ __global__ void __launch_bounds__(kBlock) elementwise_kernel(int64_t n, Op op, R
   }
   if constexpr (Op::kReduce) {
     if constexpr (ORDERED) {
-      ordered_tail(op, rb);
+      if (!rb.defer) ordered_tail(op, rb);
     } else {
       reduce_tail(op, acc.v, rb, 0);
     }
