@@ -109,6 +109,7 @@ struct NcclComm final : ShardComm {
     std::memcpy(&id, id_bytes, sizeof(id));
     NCK(api.comm_init_rank(&comm, w, id, r));
     CK(cudaMalloc(&scratch, sizeof(double)));
+    CK(cudaMemset(scratch, 0, sizeof(double)));
   }
   double* area = nullptr;             // own receive area [2][W][cap]
   std::vector<double*> peer_areas;    // mapped areas of the other ranks (IPC)
@@ -162,7 +163,8 @@ struct NcclComm final : ShardComm {
   // Every rank's producer has completed (and its P2P stores with it) once
   // this one-element all-reduce completes on the stream.
   void peer_fence(cudaStream_t s) override {
-    if (world > 1) NCK(nccl_api().all_reduce(scratch, scratch, 1, ncclFloat64, ncclSum, comm, s));
+    // ncclMax of the same value on every rank: the scratch never changes
+    if (world > 1) NCK(nccl_api().all_reduce(scratch, scratch, 1, ncclFloat64, ncclMax, comm, s));
   }
   void allreduce_sum(double* buf, int64_t count, cudaStream_t s) override {
     if (count > 0) NCK(nccl_api().all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm, s));
@@ -210,9 +212,28 @@ struct LoopbackGroup {
   int arrived = 0;
   int64_t generation = 0;
   bool poisoned = false;  // a shard left early (error): the others must not wait forever
+  int live = 0;           // attached comms; the first of a new set resets the group
   std::vector<double*> ptrs;
   std::vector<double> scalars;
   explicit LoopbackGroup(int w) : world(w), ptrs(w, nullptr), scalars(w, 0.0) {}
+  // A group is reusable for consecutive solves: when a new set of shards
+  // attaches after every comm of the previous set has left, the poison of
+  // their departure and any half-counted barrier are cleared.
+  void attach() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (live == 0) {
+      poisoned = false;
+      arrived = 0;
+      ++generation;
+    }
+    ++live;
+  }
+  void detach() {
+    std::lock_guard<std::mutex> lk(mu);
+    --live;
+    poisoned = true;
+    cv.notify_all();
+  }
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const int64_t gen = generation;
@@ -242,12 +263,13 @@ struct LoopbackComm final : ShardComm {
   LoopbackComm(LoopbackGroup* group, int r) : g(group) {
     rank = r;
     world = group->world;
+    g->attach();
   }
   double* area = nullptr;  // own receive area [2][W][cap]
   ~LoopbackComm() override {
     // a shard that leaves releases anyone still waiting (after the last
     // collective nobody waits; before it, waiting would never end)
-    g->poison();
+    g->detach();
     free_tables();
     if (area) cudaFree(area);
     if (d_ptrs) cudaFree(d_ptrs);

@@ -367,32 +367,28 @@ struct folp_gpu_ctx {
     // -> 57.6 us per trial); other layouts keep the driver's choice (config
     // 4's window-blocked products lose 25 % with it, config 5 3 %).
     // FOLP_CARVEOUT=% forces one split everywhere, -1 = driver default.
-    // (A function attribute: contexts of both kinds in one process only
-    // trade performance, never results.)
-    {
-      static int applied = -2;
-      const char* env = std::getenv("FOLP_CARVEOUT");
-      const int want = env != nullptr ? std::atoi(env) : (hot_columns ? kSegdotCarveout : -1);
-      if (want != applied) {
-        cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                             cudaFuncAttributePreferredSharedMemoryCarveout, want);
-        cudaGetLastError();
-        applied = want;
-      }
-    }
-    if (!pdl) {
-      fn<<<grid, kBlock, 0, stream>>>(sp, val, epi, rb);
-      return;
-    }
+    // Set per launch (a launch attribute, captured into graph nodes too), so
+    // concurrent contexts of both kinds never share mutable state.
+    const char* env = std::getenv("FOLP_CARVEOUT");
+    const int want = env != nullptr ? std::atoi(env) : (hot_columns ? kSegdotCarveout : -1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kBlock);
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (want >= 0) {
+      attr[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+      attr[na].val.sharedMemCarveout = static_cast<unsigned>(want);
+      ++na;
+    }
+    if (pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     CK(cudaLaunchKernelEx(&cfg, fn, sp, val, epi, rb));
   }
 

@@ -579,9 +579,21 @@ __global__ void __launch_bounds__(kFoldBlock) k_exact_fold(FoldJobs jobs, FoldSc
       Eprev = fold_classify(P - tp, tp, D, N);
       if (Eprev == kFoldIrregular) Eprev = kFoldFromPrev;  // unknown: the owner decides
     }
+    // Zero terms are transparent (fl(S + 0) == S), so an undecidable zero step
+    // -- the running sum itself at or near zero, e.g. an all-zero residual or
+    // the leading zeros of a cross term -- is skipped instead of recorded as
+    // an event; a CTA of such steps would otherwise overflow its breakpoint
+    // list and be folded step by step.  The one exception is S == -0.0 and
+    // t == +0.0 (the sum becomes +0.0), possible only while every step so
+    // far added -0.0 to a -0.0 init.
+    const bool zpos = jb.init_from < 0 ? !(init == 0.0 && signbit(init))
+                                       : fabs(init) > s_einit[j];
+    bool any = false;
     for (int64_t i = a; i < e; ++i) {
       const double t = __ldcg(&jb.t[i]);
       const int E = fold_classify(P, t, D, N);
+      if (E == kFoldIrregular && t == 0.0 && (zpos || signbit(t))) continue;
+      any = true;
       int bp = -1;  // -1 none, 1 event, 0 flush
       if (E == kFoldIrregular) {
         bp = 1;
@@ -596,7 +608,7 @@ __global__ void __launch_bounds__(kFoldBlock) k_exact_fold(FoldJobs jobs, FoldSc
       Eprev = E == kFoldIrregular ? kFoldAfterEvent : E;
       P += t;
     }
-    s_laste_t[tid] = a < e ? Eprev : kFoldEmpty;
+    s_laste_t[tid] = any ? Eprev : kFoldEmpty;
     unsigned long long ctot;
     const unsigned long long coff = fold_block_exscan_u64(c, s_u64, &ctot);
     s_off[tid] = coff;
@@ -779,11 +791,16 @@ __device__ __forceinline__ double warp_exact_dot(const double* __restrict__ val,
     long long bc[2] = {0, 0};
     int Efirst = kFoldEmpty, Eprev = kFoldEmpty;  // kFoldEmpty: before the lane's first step
     bool first_flush_pending = false;
+    int first = -1;  // the lane's first non-transparent step
     if (!slow_chunk) {
       for (int i = a; i < e; ++i) {
         const double v = wbuf[i];
         long long N = 0;
         const int E = fold_classify(P, v, D, N);
+        // a zero product at an undecidable sum is transparent (S starts at
+        // +0.0, so S + 0 == S always holds here)
+        if (E == kFoldIrregular && v == 0.0) continue;
+        if (first < 0) first = i;
         int bp = -1;
         if (E == kFoldIrregular) {
           bp = 1;
@@ -792,7 +809,7 @@ __device__ __forceinline__ double warp_exact_dot(const double* __restrict__ val,
         } else if (Eprev != kFoldAfterEvent && Eprev != E) {
           bp = 0;
         }
-        if (i == a) Efirst = E == kFoldIrregular ? kFoldAfterEvent : E;
+        if (i == first) Efirst = E == kFoldIrregular ? kFoldAfterEvent : E;
         if (bp >= 0) {
           if (nb < 2) {
             bpos[nb] = i;
@@ -823,7 +840,7 @@ __device__ __forceinline__ double warp_exact_dot(const double* __restrict__ val,
       const int lastlane = __shfl_sync(0xffffffffu, carry, 31);
       if (lastlane != kFoldEmpty) Elast = lastlane;  // for the next chunk
     }
-    if (!slow_chunk && first_flush_pending && a < e) {
+    if (!slow_chunk && first_flush_pending && first >= 0) {
       // the lane's first step is regular: a flush unless the grid continues
       // (or the previous step was a breakpoint)
       if (prevE != kFoldAfterEvent && prevE != Efirst) {
@@ -831,7 +848,7 @@ __device__ __forceinline__ double warp_exact_dot(const double* __restrict__ val,
         if (nb < 2) {
           bpos[1] = bpos[0]; bev[1] = bev[0]; beb[1] = beb[0]; bc[1] = bc[0];
         }
-        bpos[0] = a; bev[0] = 0; beb[0] = prevE; bc[0] = 0;
+        bpos[0] = first; bev[0] = 0; beb[0] = prevE; bc[0] = 0;
         ++nb;
       }
     }

@@ -27,13 +27,20 @@ void parallel_for(int64_t n, F&& f) {
     f(int64_t(0), n, 0);
     return;
   }
-  std::vector<std::thread> pool;
-  pool.reserve(t);
+  // joins on every exit path: a failed thread start must not leave joinable
+  // threads behind (std::terminate in ~thread)
+  struct Pool {
+    std::vector<std::thread> v;
+    ~Pool() {
+      for (auto& th : v)
+        if (th.joinable()) th.join();
+    }
+  } pool;
+  pool.v.reserve(t);
   for (int i = 0; i < t; ++i) {
     const int64_t b = n * i / t, e = n * (i + 1) / t;
-    pool.emplace_back([&f, b, e, i] { f(b, e, i); });
+    pool.v.emplace_back([&f, b, e, i] { f(b, e, i); });
   }
-  for (auto& th : pool) th.join();
 }
 
 template <class T>

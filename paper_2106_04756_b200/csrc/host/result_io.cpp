@@ -2,11 +2,13 @@
 // (reference /root/reference/proj/src/result_io.cpp:53-98,
 // which serializes through nlohmann::ordered_json dump(2)).  Written directly:
 // the same keys in the same order, two-space indentation, integers as
-// integers, doubles as the shortest round-trip digits laid out like the
-// reference's writer (fixed notation for exponents in [-4, 15), otherwise
+// integers, doubles as the reference writer's Grisu2 digits (grisu.hpp,
+// round-trip but not always shortest) laid out like it (fixed notation for exponents in [-4, 15), otherwise
 // d.ddde+XX with at least two exponent digits, ".0" on integral values,
 // non-finite values as null).
 #include "folp/result_io.hpp"
+
+#include "grisu.hpp"
 
 #include <algorithm>
 #include <charconv>
@@ -33,17 +35,10 @@ void json_double(std::string& out, double v) {
     out += "0.0";
     return;
   }
-  char sci[64];
-  const auto res = std::to_chars(sci, sci + sizeof(sci), v, std::chars_format::scientific);
-  const char* end = res.ptr;
-  const char* e = sci;
-  while (e < end && *e != 'e') ++e;
   char digits[32];
-  int k = 0;
-  for (const char* c = sci; c < e; ++c) {
-    if (*c != '.') digits[k++] = *c;
-  }
-  const int exp10 = std::atoi(std::string(e + 1, static_cast<std::size_t>(end - e - 1)).c_str());
+  int K = 0;
+  const int k = grisu::digits(v, digits, K);  // the reference writer's digits (grisu.hpp)
+  const int exp10 = K + k - 1;
   const int n = exp10 + 1;  // decimal point position relative to the digits
   constexpr int kMinExp = -4, kMaxExp = 15;
   if (k <= n && n <= kMaxExp) {

@@ -79,6 +79,25 @@ def cases():
     grow = 2.0 ** np.arange(-60, 60, 0.25)
     out.append(("growing_binades", np.concatenate([grow, -grow[::-1]]), 0.0))
     out.append(("sparse_nonzeros", np.where(rng.random(500000) < 0.01, rng.standard_normal(500000), 0.0), 0.0))
+    # zero terms at an undecidable running sum are skipped as transparent steps:
+    # all zeros (a dual residual with every bound finite), leading zeros, the
+    # signed-zero corner (-0.0 init: +0.0 terms turn the sum into +0.0, -0.0
+    # terms keep it), zero runs around an exact return to zero
+    out.append(("zeros_1e6", np.zeros(1000000), 0.0))
+    lead = np.zeros(400000)
+    lead[300000:] = rng.standard_normal(100000)
+    out.append(("leading_zeros", lead, 0.0))
+    out.append(("negzero_init_poszeros", np.zeros(50000), -0.0))
+    out.append(("negzero_init_negzeros", np.full(50000, -0.0), -0.0))
+    nz = np.full(50000, -0.0)
+    nz[40000] = 0.0
+    out.append(("negzero_init_mixed", nz, -0.0))
+    ret = np.zeros(300000)
+    ret[1000], ret[2000] = 1.5, -1.5
+    ret[250000:250010] = rng.standard_normal(10)
+    out.append(("return_to_zero", ret, 0.0))
+    cross = np.where(rng.random(600000) < 0.1, rng.standard_normal(600000) * 1e-4, 0.0)
+    out.append(("cross_like_sparse", cross, 0.0))
     big = rng.standard_normal(3000000) * 10.0 ** rng.uniform(-3, 3, 3000000)
     out.append(("config2_like_3e6", big, 0.0))
     return out
@@ -153,5 +172,14 @@ def test_exact_fold_speed_report(eng, capsys):
     t3 = [dy * rng.standard_normal(m), dy * dy, 3.0 * rng.standard_normal(n) ** 2 * 1e-6]
     _, ms = gpu_fold(eng, t3, inits=[0.0, 0.0, 0.0], init_from=[-1, -1, 1],
                      init_div=[1.0, 1.0, 3.0], reps=50)
+    # the same with the zero patterns of early iterates (inactive rows: dy = 0)
+    keep = rng.random(m) < 0.2
+    dyz = np.where(keep, dy, 0.0)
+    t3z = [dyz * rng.standard_normal(m), dyz * dyz, np.where(rng.random(n) < 0.3, t3[2], 0.0)]
+    _, msz = gpu_fold(eng, t3z, inits=[0.0, 0.0, 0.0], init_from=[-1, -1, 1],
+                      init_div=[1.0, 1.0, 3.0], reps=50)
+    (gz,), _ = gpu_fold(eng, [np.zeros(n)], reps=50)
+    _, ms0 = gpu_fold(eng, [np.zeros(n)], reps=50)
     with capsys.disabled():
-        print(f"\n[exact fold] config-2 trial folds (200k + 200k + 400k terms): {1e3 * ms:.1f} us per launch")
+        print(f"\n[exact fold] config-2 trial folds (200k + 200k + 400k terms): {1e3 * ms:.1f} us per launch; "
+              f"80 % zero terms: {1e3 * msz:.1f} us; 400k zeros: {1e3 * ms0:.1f} us")

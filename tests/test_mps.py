@@ -257,6 +257,29 @@ def _reference_results(ref):
     return out
 
 
+def test_result_json_numbers_match_reference_writer(ref):
+    """Doubles as the reference's JSON writer prints them (nlohmann's Grisu2:
+    round-trip, not always the shortest digits -- e.g. 0.0012036080000000001,
+    a wall time that once made the comparison below flaky), on adversarial
+    and random values placed in every double field of a result."""
+    import dataclasses
+    eng = engine()
+    base = _reference_results(ref)[2]
+    rng = np.random.default_rng(11)
+    bits = rng.integers(0, 2 ** 63 - 1, 3000, dtype=np.int64).view(np.float64)
+    vals = [0.0012036080000000001, 5e-324, 2.2250738585072014e-308, 1.7976931348623157e308,
+            1e15, 1e16, 1e-5, 1e-4, 0.1, 1.0 / 3, 123456789012345678.0, -0.0, 9.999999999999999e22]
+    vals += [float(v) for v in bits if np.isfinite(v)]
+    vals += list(rng.random(2000) * 0.01) + list(np.ldexp(rng.random(2000), rng.integers(-100, 100, 2000)))
+    fields = list(base.final_info)
+    for i in range(0, len(vals), len(fields) + 2):
+        chunk = vals[i:i + len(fields) + 2]
+        info = {f: chunk[j % len(chunk)] for j, f in enumerate(fields)}
+        r = dataclasses.replace(base, final_info=info, wall_seconds=chunk[-1],
+                                kkt_passes=abs(chunk[0]))
+        assert eng.result_to_json(r) == ref.result_to_json(r), chunk
+
+
 def test_result_json_matches_reference(ref):  # test_cli_io.cpp:218-248
     eng = engine()
     for res in _reference_results(ref):
