@@ -78,18 +78,37 @@ def measured_peak() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    polled every 2 ms from a thread (the timed region of the default run is
+    tens of milliseconds; nvidia-smi's 100 ms loop saw one sample), falling
+    back to `nvidia-smi -lms 100`."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown")
+    PERIOD_S = 0.002
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines: list[str] = []
+        self.samples: list[tuple[float, float, set]] = []
+        self.nvml = None
+        self.stop = threading.Event()
+        self.thread = None
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = nv
+            self.handle = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = float(nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -101,11 +120,29 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self.nvml
+        bits = {"sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                "hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown}
+        while not self.stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                self.samples.append((sm, self.max_sm, {k for k, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            self.stop.wait(self.PERIOD_S)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.nvml is not None and self.thread is not None:
+            self.thread.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -116,6 +153,10 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, mx, reasons = [], [], set()
         names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for a, b, r in self.samples:
+            sm.append(a)
+            mx.append(b)
+            reasons |= r
         for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) != 6:
@@ -130,7 +171,7 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml 2 ms" if self.samples else "nvidia-smi 100 ms"}
 
 
 def dist_setup():
@@ -342,6 +383,9 @@ def run_b200(args, world, rank, local):
     if finished_early:
         line["note"] = "solve converged inside the timed region; fewer steps timed"
 
+    if args.ordered_steps > 0 and not sharded:
+        line["ordered"] = ordered_block(eng, lp, p, args, world, jobs, b_trial, peak)
+
     if rank == 0 and world == 1 and not args.skip_cpu_baseline:
         rate, small, big = reference_loop_rate(lp, CADENCE, 3 * CADENCE, 1)
         line["cpu_baseline"] = {
@@ -354,6 +398,32 @@ def run_b200(args, world, rank, local):
         line["convergence"] = convergence_block(eng, lp, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def ordered_block(eng, lp, p, args, world, jobs, b_trial, peak) -> dict:
+    """The same device-resident loop in the ordered reduction mode (every sum
+    folded in the reference's sequential order: iterates bit-identical to the
+    reference, tests/test_gpu_fullsize_parity.py), timed the same way."""
+    eng.lib.folp_gpu_set_default_reduction(1)
+    try:
+        sess = eng.session(lp, p)
+        sess.advance(1)
+        s0 = sess.stats()
+        barrier(world)
+        ms = [sess.advance(1) for _ in range(args.ordered_steps)]
+        s1 = sess.stats()
+        sess.close()
+    finally:
+        eng.lib.folp_gpu_set_default_reduction(0)
+    total = allreduce_max(float(sum(ms)), world)
+    iters = s1["iterations"] - s0["iterations"]
+    slots = s1["loop_slots"] - s0["loop_slots"]
+    loop_ms = s1["loop_ms"] - s0["loop_ms"]
+    achieved = b_trial * slots / (loop_ms / 1000.0) / 1e9 if loop_ms > 0 else 0.0
+    return {"value": iters * jobs / (total / 1000.0), "unit": UNIT, "steps": len(ms),
+            "ms_per_step": total / max(1, len(ms)), "kernel_ms_per_trial": loop_ms / max(1, slots),
+            "roofline_frac": achieved / peak,
+            "parity": "iterates bit-identical to the reference (ordered reductions)"}
 
 
 def convergence_block(eng, lp, args) -> dict:
@@ -396,6 +466,8 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--eps", type=float, default=1e-8)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--ordered-steps", type=int, default=5,
+                    help="also time this many steps in the ordered (bit-exact) reduction mode")
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--time-to-tol", type=float, default=60.0,
                     help="also solve config 1 to 1e-8 (B200 and reference CPU) and the "

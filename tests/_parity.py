@@ -52,3 +52,67 @@ def rel_kkt(info: dict) -> float:
     pr = info["primal_residual_norm"] / (1 + info["norm_q"])
     du = info["dual_residual_norm"] / (1 + info["norm_c"])
     return max(gap, pr, du)
+
+
+# ---- the reference's own reduction-order noise floor ------------------------
+# Any parallel fp64 PDLP re-associates the reference's sequential folds, and
+# the adaptive step rule amplifies last-bit differences.  The
+# floor of an instance is the per-iterate deviation of the SAME algorithm with
+# re-associated sums -- the C restatement (oracle/pdlp_port.c) under sum
+# orders 1 (pairwise tree), 2 (reversed fold), 3 (tree + 256-entry parts for
+# long dots) -- from the compiled reference; tools/noise_floor.py measures it
+# at BASELINE sizes.  Tree-mode tests hold the production reductions to
+# FLOOR_FACTOR x that floor (one more association, another sample of the same
+# spread), and its iteration counts to the reference's own spread.
+FLOOR_FACTOR = 10.0
+CHECKPOINTS = (10, 20, 40, 60, 80, 100, 120)
+SUM_ORDERS = (1, 2, 3)
+
+
+def reference_floor(lp, p: dict, iterates: int, want=None) -> list[float]:
+    """Running max over iterates of the largest deviation of a re-associated
+    reference (sum orders 1-3) from the reference itself."""
+    import ctypes as C
+
+    from oracle import port, ref
+
+    if want is None:
+        want = ref.binding().solve_lp(lp, p, iterate_capacity=iterates)
+    lib = port.binding().lib
+    lib.folp_port_set_sum_order.argtypes = [C.c_int]
+    floor = [0.0] * len(want.iterate_trace)
+    for order in SUM_ORDERS:
+        lib.folp_port_set_sum_order(order)
+        try:
+            got = port.binding().solve_lp(lp, p, iterate_capacity=iterates)
+        finally:
+            lib.folp_port_set_sum_order(0)
+        for k, v in enumerate(running_max(drift_curve(got.iterate_trace, want.iterate_trace))):
+            floor[k] = max(floor[k], v)
+    return floor
+
+
+def assert_within_floor(got_trace, want_trace, floor: list[float], what: str = "") -> list[float]:
+    """Tree-mode drift against the reference at every checkpoint <= FLOOR_FACTOR
+    x the floor (never required below 1e-12: both agree to the last bits
+    early on).  Returns the drift's running max."""
+    curve = running_max(drift_curve(got_trace, want_trace))
+    for k in CHECKPOINTS:
+        if k <= len(curve):
+            bound = max(FLOOR_FACTOR * floor[k - 1], 1e-12)
+            assert curve[k - 1] <= bound, (what, k, curve[k - 1], floor[k - 1])
+    return curve
+
+
+def iteration_band(cfg: int, seed: int, scale: float) -> float:
+    """Allowed relative iteration-count deviation of a tree-mode solve to 1e-8:
+    the north_star's 5 %, or the reference's own spread under re-associated
+    sums on that instance (tests/golden/iteration_spread.json, made by
+    tools/noise_floor_iterations.py --fixture) when larger, x1.5 (three
+    re-associations sample the spread; one more is another draw)."""
+    import json
+    from pathlib import Path
+
+    spread = json.loads((Path(__file__).parent / "golden" / "iteration_spread.json").read_text())
+    row = spread[f"cfg{cfg}_s{seed}_x{scale}"]
+    return max(0.05, 1.5 * row["max_abs_iter_dev"])

@@ -16,6 +16,8 @@ import pytest
 
 from paper_2106_04756_b200 import cabi, instances, shard
 
+from _parity import iteration_band
+
 pytestmark = pytest.mark.gpu
 
 
@@ -50,9 +52,9 @@ def test_loopback_shards_solve_to_1e8(ref, cfg, scale, world, partition):
     assert _rel_kkt(a.final_info) <= 1e-8
     pa, pb = a.final_info["primal_objective"], b.final_info["primal_objective"]
     assert abs(pa - pb) <= 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
-    # tree-order sums: the iteration count moves like the single-GPU tree
-    # mode's (profiles/r1_tree_mode_iteration_spread.txt)
-    assert abs(a.iterations - b.iterations) <= 0.30 * b.iterations
+    # tree-order sums: the iteration count moves like that of a re-associated
+    # reference (tests/_parity.py iteration_band)
+    assert abs(a.iterations - b.iterations) <= iteration_band(cfg, 1, scale) * b.iterations
     assert a.step_condition_violations == 0
 
 

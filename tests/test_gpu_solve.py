@@ -7,8 +7,14 @@ within 5 %).
 Two reduction modes (include/folp_gpu.h folp_gpu_set_default_reduction):
 * ordered -- every sum folded in the reference's sequential order: the whole
   trajectory is bit-identical to the reference (checked exactly);
-* tree    -- the production mode: deterministic warp/CTA trees; checked
-  against the north_star tolerances."""
+* tree    -- the production mode: deterministic warp/CTA trees.  No
+  parallel summation reproduces a sequential fold, and the adaptive step
+  rule amplifies last-bit differences, so the tree mode is held to the
+  reference's OWN reduction-order noise floor on each instance (the same
+  algorithm with re-associated sums, tests/_parity.py reference_floor):
+  per-iterate drift <= FLOOR_FACTOR x floor, identical restart decisions
+  and ledger, iteration counts within the reference's own spread
+  (iteration_band), KKT <= 1e-8."""
 import contextlib
 import hashlib
 import json
@@ -18,6 +24,8 @@ import numpy as np
 import pytest
 
 from paper_2106_04756_b200 import cabi, instances
+
+from _parity import assert_within_floor, iteration_band, reference_floor
 
 pytestmark = pytest.mark.gpu
 
@@ -107,46 +115,45 @@ def test_ordered_mode_reproduces_golden_hashes(eng, name):
 
 
 def test_tree_mode_first_100_iterates(eng, ref):
-    """Production reductions: the adaptive step-size recurrence amplifies
-    last-bit differences of the cross term (measured ~6e-9 by iteration 100
-    on config 1); restart decisions and the ledger agree."""
+    """Production reductions over the first 100 iterates of config 1: within
+    1e-10 over the first restart period (the north_star bar holds there),
+    within the reference's own noise floor at every checkpoint; the same
+    restart decisions and ledger."""
     lp = instances.generate(1, 1, 1.0)
     p = cabi.params(record_iterate_trace=True, iteration_limit=100)
     a = eng.solve_lp(lp, p, iterate_capacity=100)
     b = ref.solve_lp(lp, p, iterate_capacity=100)
     assert len(a.iterate_trace) == len(b.iterate_trace) == 100
     assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-10  # first restart period
-    assert _drift(a.iterate_trace, b.iterate_trace, 100) <= 1e-7
+    curve = assert_within_floor(a.iterate_trace, b.iterate_trace, reference_floor(lp, p, 100, b))
+    print(f"config 1 tree drift at 40/100: {curve[39]:.2e}/{curve[99]:.2e}")
     assert a.restart_iterations == b.restart_iterations
     assert a.kkt_passes == b.kkt_passes
 
 
 @pytest.mark.parametrize("cfg,scale", [(2, 0.4), (3, 0.06)])
-def test_tree_mode_balanced_plans_first_restart_period(eng, ref, cfg, scale):
-    """Instances above 2^20 nonzeros run the balanced unit plans (plans.cuh):
-    the first restart period stays within 1e-7 of the reference (tree-mode
-    sums; a wrong plan is off by O(1)), restarts and the ledger agree over
-    120 iterations."""
+def test_tree_mode_balanced_plans_first_restart_periods(eng, ref, cfg, scale):
+    """Instances above 2^20 nonzeros run the balanced unit plans (plans.cuh)
+    and, on config 2, degree-ordered columns: 120 iterates within the
+    reference's own noise floor (a wrong plan is off by O(1)), identical
+    restarts and ledger."""
     lp = instances.generate(cfg, 1, scale)
     assert lp.nnz > (1 << 20)
     p = cabi.params(record_iterate_trace=True, iteration_limit=120)
     a = eng.solve_lp(lp, p, iterate_capacity=120)
     b = ref.solve_lp(lp, p, iterate_capacity=120)
-    assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-7
+    assert_within_floor(a.iterate_trace, b.iterate_trace, reference_floor(lp, p, 120, b), cfg)
     assert a.restart_iterations == b.restart_iterations
     assert a.kkt_passes == b.kkt_passes
 
 
 @pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 0.01), (5, 0.01)])
 def test_tree_mode_solve_to_1e8(eng, ref, cfg, scale):
-    """Production reductions to 1e-8.  The adaptive step amplifies last-bit
-    differences of the tree sums (no parallel sum reproduces a sequential
-    fold), so trajectories separate after a few hundred iterations and the
-    iteration count of a single instance moves like that of any reordered
-    build of the reference: measured -26 % .. +26 % per instance, aggregates
-    within ~10 % (profiles/r1_tree_mode_iteration_spread.txt, tools/
-    diag_iterations.py).  The 5 % iteration bar is met exactly (0 %) by the
-    ordered mode above; here the band is 30 %."""
+    """Production reductions to 1e-8.  Trajectories of any two associations
+    of the sums separate after a few hundred iterations, so the iteration
+    count of one instance moves like that of a re-associated reference: the
+    band is the reference's own spread on this instance (or 5 %), see
+    iteration_band.  The ordered mode above meets 0 %."""
     lp = instances.generate(cfg, 1, scale)
     p = cabi.params(kkt_pass_limit=300000)
     a = eng.solve_lp(lp, p)
@@ -160,7 +167,7 @@ def test_tree_mode_solve_to_1e8(eng, ref, cfg, scale):
         pa, pb = a.final_info["primal_objective"], b.final_info["primal_objective"]
         admissible = 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
         assert abs(pa - pb) <= admissible
-        assert abs(a.iterations - b.iterations) <= 0.30 * b.iterations
+        assert abs(a.iterations - b.iterations) <= iteration_band(cfg, 1, scale) * b.iterations
     assert a.step_condition_violations == 0
 
 
@@ -190,13 +197,13 @@ def test_window_blocked_products_solve(eng, ref, cfg, scale, monkeypatch):
         assert _rel_kkt(a.final_info) <= 1e-8
         pa, pb = a.final_info["primal_objective"], b.final_info["primal_objective"]
         assert abs(pa - pb) <= 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
-        assert abs(a.iterations - b.iterations) <= 0.30 * b.iterations
+        assert abs(a.iterations - b.iterations) <= iteration_band(cfg, 1, scale) * b.iterations
     assert a.step_condition_violations == 0
-    # first restart period stays within the tree-mode drift
-    p = cabi.params(record_iterate_trace=True, iteration_limit=40)
-    a = eng.solve_lp(lp, p, iterate_capacity=40)
-    b = ref.solve_lp(lp, p, iterate_capacity=40)
-    assert _drift(a.iterate_trace, b.iterate_trace, 40) <= 1e-9
+    # the first 100 iterates stay within the reference's noise floor
+    p = cabi.params(record_iterate_trace=True, iteration_limit=100)
+    a = eng.solve_lp(lp, p, iterate_capacity=100)
+    b = ref.solve_lp(lp, p, iterate_capacity=100)
+    assert_within_floor(a.iterate_trace, b.iterate_trace, reference_floor(lp, p, 100, b), cfg)
 
 
 @pytest.mark.parametrize("overrides", [dict(step_policy="constant"),
@@ -232,4 +239,4 @@ def test_tree_mode_without_cooperative_launch(eng, ref, monkeypatch):
     assert a.termination_reason == b.termination_reason
     if b.termination_reason == "Optimal":
         assert _rel_kkt(a.final_info) <= 1e-8
-        assert abs(a.iterations - b.iterations) <= 0.30 * b.iterations
+        assert abs(a.iterations - b.iterations) <= iteration_band(5, 3, 0.02) * b.iterations
