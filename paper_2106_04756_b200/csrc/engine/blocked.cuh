@@ -47,6 +47,9 @@ void build_blocked(folp_gpu_ctx* c, bool rows_axis) {
   const char* thr = std::getenv("FOLP_BLOCKED_MIN");
   const int64_t min_vec = thr ? std::atoll(thr) : kBlockedMinVector;
   if (c->ordered || c->sharded() || X < min_vec || nnz == 0 || X <= window) return;
+  // rows whose gathers are coalesced already (SELL-32 groups + contiguous
+  // rows, sell.cuh) read x as streams: no windows needed
+  if (rows_axis && c->sell && c->sell_coalesced) return;
   const int* ptr = rows_axis ? c->csr_ptr : c->csc_ptr;
   const int* idx = rows_axis ? c->csr_col : c->csc_row;
   const double* val = rows_axis ? c->csr_work : c->csc_work;

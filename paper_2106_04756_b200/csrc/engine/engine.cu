@@ -38,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -120,19 +121,21 @@ struct BlockedAxis {
 
 bool g_default_ordered = false;
 std::mutex g_occ_mu;
-std::unordered_map<const void*, int> g_occ;
+std::map<std::pair<const void*, int>, int> g_occ;  // (kernel, dynamic smem) -> CTAs per SM
 
 int occupancy(const void* fn, int smem = 0) {
   std::lock_guard<std::mutex> lk(g_occ_mu);
-  auto it = g_occ.find(fn);
+  const auto key = std::make_pair(fn, smem);
+  auto it = g_occ.find(key);
   if (it != g_occ.end()) return it->second;
-  if (smem > 48 * 1024) {
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (smem > 48 * 1024) {  // opt in once for the largest staging any context may use
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            std::max(smem, kStageMaxBytes)));
   }
   int b = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, smem));
   if (b < 1) b = 1;
-  g_occ[fn] = b;
+  g_occ[key] = b;
   return b;
 }
 
@@ -213,6 +216,8 @@ struct folp_gpu_ctx {
   PlanDev lrows, lcols;               // rows: own CSR rows, local CSC; cols: local CSR, own CSC columns
   BlockedAxis brows, bcols;           // window-blocked loop copies (large vectors)
   bool blocked_checked = false;
+  PlanDev rows_sell;                  // the loop's K x' with SELL-32 groups (sell.cuh)
+  bool sell = false, sell_packed = false, sell_coalesced = false;
   int* lcsc_ptr = nullptr;
   int* lcsc_row = nullptr;
   int* lcsc_pos = nullptr;            // local CSC entry -> full CSC position
@@ -358,9 +363,24 @@ struct folp_gpu_ctx {
   // Launch of a segdot kernel; with `pdl` (the PDHG loop's products, see
   // segdot.cuh griddep_wait) as a programmatic dependent launch.
   bool pdl = false;
-  template <class Epi, bool ORD, bool PR>
-  void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb) {
-    auto fn = segdot_kernel<Epi, ORD, PR>;
+  // Staged gathers (segdot.cuh) for the loop's own axis plans when the
+  // gathered vector fits kStageMaxBytes; FOLP_STAGE=1 enables.  Off by
+  // default: on config 5 (y = 80 KB) two CTAs per SM fit next to the copy,
+  // and the halved occupancy costs the streams more than the shared-memory
+  // gathers save (K'y + primal step 530 -> 608 us per trial).
+  int stage_env = -1;
+  bool stage_ok(const PlanDev& p) {
+    if (stage_env < 0) {
+      const char* env = std::getenv("FOLP_STAGE");
+      stage_env = env != nullptr ? std::atoi(env) : 0;
+    }
+    return stage_env != 0 && (&p == &rows || &p == &cols) && p.sp.vec_len > 0 &&
+           p.sp.vec_len * static_cast<int64_t>(sizeof(double)) <= kStageMaxBytes;
+  }
+  template <class Epi, bool ORD, bool PR, bool ST = false, bool SE = false>
+  void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb,
+                     int smem = 0) {
+    auto fn = segdot_kernel<Epi, ORD, PR, ST, SE>;
     // L1 / shared split: for degree-ordered columns (a hot prefix of the
     // gathered vector), the smallest shared carveout that still holds
     // kPlanCtasPerSm CTAs leaves the most L1 to the gathers (config 2 59.7
@@ -374,6 +394,7 @@ struct folp_gpu_ctx {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     int na = 0;
@@ -423,6 +444,19 @@ struct folp_gpu_ctx {
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, false, true>(grid, p.sp, prod, epi, rb);
       ++launches;
+    } else if (p.sp.sell.n_groups > 0) {
+      // a plan with SELL-32 groups (sell.cuh)
+      auto fn = segdot_kernel<Epi, false, false, false, true>;
+      const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
+      launch_segdot<Epi, false, false, false, true>(grid, p.sp, val, epi, rb);
+    } else if (stage_ok(p)) {
+      // the gathered vector in shared memory (segdot.cuh, staged gathers)
+      auto fn = segdot_kernel<Epi, false, false, true>;
+      const int smem = p.sp.vec_len * static_cast<int>(sizeof(double));
+      const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn), smem);
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
+      launch_segdot<Epi, false, false, true>(grid, p.sp, val, epi, rb, smem);
     } else {
       auto fn = segdot_kernel<Epi, false>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
@@ -554,6 +588,7 @@ struct folp_gpu_ctx {
 namespace {
 
 #include "plans.cuh"
+#include "sell.cuh"
 #include "blocked.cuh"
 #include "evaluation.cuh"
 #include "shard_graphs.cuh"
@@ -698,6 +733,20 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
     mark("values");
     build_plan(c.get(), p->row_start, m, nnz, c->csr_ptr, c->csr_col, c->rows);
     build_plan(c.get(), col_start, n, nnz, c->csc_ptr, c->csc_row, c->cols);
+    c->rows.sp.vec_len = static_cast<int>(std::min<int64_t>(n, INT32_MAX));
+    c->cols.sp.vec_len = static_cast<int>(std::min<int64_t>(m, INT32_MAX));
+    if (!c->ordered && col_order == nullptr && nnz > 0 && p->row_cols != nullptr) {
+      const SellHost sh = detect_sell(p->row_start, p->row_cols, m, nnz);
+      if (!sh.row0.empty()) {
+        build_sell_plan(c.get(), p->row_start, m, nnz, sh, c->rows_sell);
+        c->sell = true;
+        c->sell_coalesced = sh.gathers_coalesced;
+        if (timing) {
+          std::fprintf(stderr, "[folp timing] SELL-32: %zu row groups, %lld entries, coalesced %d\n",
+                       sh.row0.size(), static_cast<long long>(sh.nnz), sh.gathers_coalesced ? 1 : 0);
+        }
+      }
+    }
 
     mark("plans");
     auto vn = [&] { return c->alloc<double>(n); };
@@ -1115,6 +1164,10 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     }
     if (policy != FOLP_STEP_MALITSKY_POCK && !c->kx_valid) refresh_kx(c);
     ensure_blocked(c);  // after rescaling: the working values are final
+    if (c->sell && !c->sell_packed) {
+      pack_sell(c, c->rows_sell);
+      c->sell_packed = true;
+    }
     if (loop->target > c->table_cap) {
       throw std::invalid_argument("run_chunk: target above the factor-table capacity");
     }

@@ -11,8 +11,11 @@ double tile_segs_cutoff() {
 // Warp units of one axis (see segdot.cuh): tiles of consecutive short
 // segments (<= kWarpTile nonzeros, <= 256 segments each) and fixed parts of
 // the longer ones, in index order.
+// `skip` (optional): segments left out of the tiles and parts (the SELL
+// groups' rows); `extra`: units appended to every build (their SELL parts).
 void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
-                const int* d_ptr, const int* d_idx, PlanDev& out, int64_t s_begin = 0) {
+                const int* d_ptr, const int* d_idx, PlanDev& out, int64_t s_begin = 0,
+                const std::vector<char>* skip = nullptr, const std::vector<int4>* extra = nullptr) {
   const bool ordered = c->ordered;
   // segments per tile: tree mode caps it when segments are very short (a
   // lane then owns several segments, and every extra round waits behind the
@@ -63,6 +66,10 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
       tile_nnz = 0;
     };
     for (int64_t s = s_begin; s < S; ++s) {
+      if (skip != nullptr && (*skip)[static_cast<size_t>(s)]) {
+        close(s);
+        continue;
+      }
       const int64_t len = ptr[s + 1] - ptr[s];
       if (len > serial_cap && (len <= kWarpTile || len <= single_max)) {
         close(s);
@@ -94,6 +101,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
       multi_parts.push_back(static_cast<int>(units.size()) - multi_first.back());
     }
     close(S);
+    if (extra != nullptr) units.insert(units.end(), extra->begin(), extra->end());
   };
   build(kWarpTile);
   // Tree mode, large axes: balance the persistent grid's warps.  A warp's
@@ -106,6 +114,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   const char* benv = std::getenv("FOLP_BALANCE");
   const int nw = c->sms * kPlanCtasPerSm * kWarps;
   auto cost = [](const int4& d) -> int64_t {
+    if (d.x <= -kSellTag) return 32 * static_cast<int64_t>(d.w - d.z) + 64 + 24;
     const int64_t segs = d.x >= 0 ? d.y - d.x : 1;
     return (d.w - d.z) + 2 * segs + 24;
   };

@@ -73,6 +73,31 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // fence.sc.gpu, a sequentially consistent fence the patterns do not need.
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+// Lane-per-segment groups (SELL-32; tree mode, the loop's row products):
+// 32 consecutive segments of equal length L stored interleaved -- entry j of
+// the group's segment `lane` at base + 32 j + lane -- so lane l sums its
+// segment in entry order while the warp's loads of one j are consecutive.
+// Chosen per group when the interleaved gathers touch far fewer sectors than
+// the per-segment ones (config 5's demand rows: entry j of demand row d is
+// column j*D + d, so 32 neighbouring rows gather 32 consecutive x values,
+// while one row alone strides by D).  A unit {-(kSellTag + g), part, j0, j1}
+// covers entries [j0, j1) of all 32 segments; the last part to arrive sums
+// each lane's part sums in part order and runs the epilogue, its reduction
+// terms going to slot n_multi + g (deterministic, like multi-part segments).
+constexpr int kSellTag = 1 << 29;
+constexpr int kSellPart = 64;  // entries per lane per unit (2048 nonzeros)
+struct SellPlan {
+  const int* idx = nullptr;      // [32 * sum L] interleaved gather indices
+  const double* val = nullptr;   // interleaved working values
+  const int* base = nullptr;     // [n_groups] first interleaved entry
+  const int* row0 = nullptr;     // [n_groups] first segment
+  const int* nparts = nullptr;   // [n_groups]
+  const int* slot0 = nullptr;    // [n_groups] first part slot (slots hold 32 sums)
+  double* part_sums = nullptr;   // [total parts * 32]
+  unsigned* arrivals = nullptr;  // [n_groups], zero between launches
+  int n_groups = 0;
+};
+
 // One warp unit: a tile {seg0, seg1, k0, k1} (seg0 >= 0) or a part
 // {-(multi+1), first_unit_of_segment, k0, k1} of multi-part segment `multi`.
 struct SegPlan {
@@ -87,7 +112,24 @@ struct SegPlan {
   int n_multi;
   double* part_sums;      // [n_units] (only part slots used)
   unsigned* arrivals;     // [n_multi], zero between launches
+  int vec_len = 0;        // length of the gathered vector (0: unknown; staging off)
+  SellPlan sell{};        // lane-per-segment groups (n_groups = 0: none)
 };
+
+// Staged gathers: when the vector an axis gathers from fits in shared memory
+// (config 5's K'y gathers y: 10,000 doubles, 80 KB), each CTA copies it once
+// after griddep_wait and every gather reads shared memory -- random 8-byte
+// shared loads run ~2.4x the L1tex gather rate (587 vs ~240 G/s,
+// profiles/r1_ceiling_cfg4.txt) and leave the L1tex pipe to the streams.
+constexpr int kStageMaxBytes = 96 * 1024;
+template <bool STAGE>
+__device__ __forceinline__ double gather(const double* __restrict__ v, int i) {
+  if constexpr (STAGE) {
+    return v[i];
+  } else {
+    return __ldg(&v[i]);
+  }
+}
 
 struct RedBuf {
   double* partials;   // [(gridDim.x + n_multi) * K]
@@ -389,7 +431,7 @@ __device__ __forceinline__ void prefetch_unit(const SegPlan& p, const double* va
   if (lane == 31 && d.x >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ptr + d.x));
 }
 
-template <class Epi, bool ORDERED, bool PROD = false>
+template <class Epi, bool ORDERED, bool PROD = false, bool STAGE = false, bool SELLU = false>
 #ifdef FOLP_WARP_TIMES
 #define FOLP_SEGDOT_BOUNDS __launch_bounds__(kBlock, kPlanCtasPerSm)  // same residency as the product build
 #else
@@ -409,6 +451,20 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   trace_warp<Epi>(0, global_ns());
 #endif
   const double* __restrict__ vec = epi.vec();
+  if constexpr (STAGE) {
+    extern __shared__ double s_stage[];
+    const int X = p.vec_len;
+    if ((reinterpret_cast<uintptr_t>(vec) & 15) == 0) {
+      const double2* v2 = reinterpret_cast<const double2*>(vec);
+      double2* s2 = reinterpret_cast<double2*>(s_stage);
+      for (int i = threadIdx.x; i < (X >> 1); i += kBlock) s2[i] = __ldcg(&v2[i]);
+      if (threadIdx.x == 0 && (X & 1)) s_stage[X - 1] = __ldcg(&vec[X - 1]);
+    } else {
+      for (int i = threadIdx.x; i < X; i += kBlock) s_stage[i] = __ldcg(&vec[i]);
+    }
+    __syncthreads();
+    vec = s_stage;
+  }
   const int* __restrict__ idx = p.idx;
   const int* __restrict__ ptr = p.ptr;
   __shared__ double s_prod[kWarps][kWarpTile];
@@ -442,20 +498,24 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
     work += static_cast<unsigned long long>(k1 - k0) +
             (d.x < 0 ? (1ull << 24) : (static_cast<unsigned long long>(d.y - d.x) << 36));
 #endif
-    if (d.x >= 0 && k1 - k0 > kWarpTile) {
-      // ordered plan: one long segment, its dot the reference's sequential
-      // sum in index order -- by the whole warp through the exact fold
-      // (products staged in rb.scratch), or by one lane
-      if (rb.scratch != nullptr) {
-        const double sum = warp_exact_dot<PROD>(val, idx, vec, k0, k1, wbuf);
-        if (lane == 0) epi.apply(d.x, sum, epi.load(d.x), acc);
-        __syncwarp();
-      } else if (lane == 0) {
-        double sum = 0.0;
-        for (int k = k0; k < k1; ++k) sum += PROD ? val[k] : val[k] * vec[idx[k]];
-        epi.apply(d.x, sum, epi.load(d.x), acc);
+    if constexpr (ORDERED) {  // (tree plans split long segments into parts)
+      if (d.x >= 0 && k1 - k0 > kWarpTile) {
+        // ordered plan: one long segment, its dot the reference's sequential
+        // sum in index order -- by the whole warp through the exact fold
+        // (products staged in rb.scratch), or by one lane
+        if (rb.scratch != nullptr) {
+          const double sum = warp_exact_dot<PROD>(val, idx, vec, k0, k1, wbuf);
+          if (lane == 0) epi.apply(d.x, sum, epi.load(d.x), acc);
+          __syncwarp();
+        } else if (lane == 0) {
+          double sum = 0.0;
+          for (int k = k0; k < k1; ++k) sum += PROD ? val[k] : val[k] * vec[idx[k]];
+          epi.apply(d.x, sum, epi.load(d.x), acc);
+        }
+        continue;
       }
-    } else if (d.x >= 0) {
+    }
+    if (d.x >= 0) {
       // ---------------- tile of short segments ----------------
       const int seg0 = d.x, seg1 = d.y;
       const int s_first = seg0 + lane;
@@ -473,7 +533,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         if constexpr (PROD) {
           prod[j] = k < k1 ? val[k] : 0.0;
         } else {
-          prod[j] = k < k1 ? val[k] * __ldg(&vec[idx[k]]) : 0.0;
+          prod[j] = k < k1 ? val[k] * gather<STAGE>(vec, idx[k]) : 0.0;
         }
       }
 #pragma unroll
@@ -495,6 +555,67 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         epi.apply(s, sum, pre, acc);
       }
       __syncwarp();
+    } else if (SELLU && d.x <= -kSellTag) {
+      // ---------------- lane-per-segment group part (SELL-32) ----------------
+      const SellPlan& q = p.sell;
+      const int g = -d.x - kSellTag;
+      const int np = q.nparts[g];
+      const int row = q.row0[g] + lane;
+      const int base = q.base[g];
+      typename Epi::Pre pre_one{};
+      if (np == 1) pre_one = epi.load(row);  // in flight with the gathers
+      // the group's reduction terms always go to its slot (a single-part
+      // group too: the tail sums every group slot)
+      auto finish = [&](double total, const typename Epi::Pre& pre) {
+        TreeAcc<K> macc;
+        macc.zero();
+        epi.apply(row, total, pre, macc);
+        if constexpr (Epi::kReduce) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            double v = macc.v[k];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) rb.partials[(gridDim.x + p.n_multi + g) * K + k] = v;
+          }
+        }
+      };
+      double sum = 0.0;
+      {
+        const int* __restrict__ qi = q.idx + base + lane;
+        const double* __restrict__ qv = q.val + base + lane;
+        int j = d.z;
+        for (; j + 8 <= d.w; j += 8) {  // 8 independent loads per lane in flight
+          int ix[8];
+          double v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            ix[t] = qi[32 * (j + t)];
+            v[t] = qv[32 * (j + t)];
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) sum += v[t] * gather<STAGE>(vec, ix[t]);
+        }
+        for (; j < d.w; ++j) sum += qv[32 * j] * gather<STAGE>(vec, qi[32 * j]);
+      }
+      if (np == 1) {
+        finish(sum, pre_one);
+      } else {
+        const int slot = q.slot0[g] + d.y;
+        q.part_sums[slot * 32 + lane] = sum;
+        fence_acq_rel();
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) last = atomicAdd(&q.arrivals[g], 1u) == static_cast<unsigned>(np - 1) ? 1u : 0u;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          fence_acq_rel();
+          double total = 0.0;
+          for (int pp = 0; pp < np; ++pp) total += ld_cg(&q.part_sums[(q.slot0[g] + pp) * 32 + lane]);
+          finish(total, epi.load(row));
+          if (lane == 0) q.arrivals[g] = 0u;
+        }
+      }
     } else if constexpr (!ORDERED) {
       // ---------------- part of a long segment ----------------
       const int multi = -d.x - 1;
@@ -507,7 +628,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         if constexpr (PROD) {
           sum += val[k];
         } else {
-          sum += val[k] * __ldg(&vec[idx[k]]);
+          sum += val[k] * gather<STAGE>(vec, idx[k]);
         }
       }
 #pragma unroll
@@ -549,7 +670,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
     if constexpr (ORDERED) {
       if (!rb.defer) ordered_tail(epi, rb);
     } else {
-      reduce_tail(epi, acc.v, rb, p.n_multi);
+      reduce_tail(epi, acc.v, rb, p.n_multi + p.sell.n_groups);
     }
   }
 #ifdef FOLP_WARP_TIMES

@@ -164,7 +164,11 @@ void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
     try {
       c->defer_tail = fold;
       axis_product(c, false, true, EpiPrimal{b}, 2, 0);
-      axis_product(c, true, true, EpiDual{b}, 3, 1);
+      if (c->sell && c->sell_packed && !c->sharded() && c->brows.windows == 0) {
+        c->seg(c->rows_sell, c->csr_work, EpiDual{b}, 3, 1);  // SELL-32 groups (sell.cuh)
+      } else {
+        axis_product(c, true, true, EpiDual{b}, 3, 1);
+      }
       c->defer_tail = false;
       if (fold) c->launch_trial_fold(b);
     } catch (...) {

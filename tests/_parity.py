@@ -107,12 +107,14 @@ def assert_within_floor(got_trace, want_trace, floor: list[float], what: str = "
 def iteration_band(cfg: int, seed: int, scale: float) -> float:
     """Allowed relative iteration-count deviation of a tree-mode solve to 1e-8:
     the north_star's 5 %, or the reference's own spread under re-associated
-    sums on that instance (tests/golden/iteration_spread.json, made by
-    tools/noise_floor_iterations.py --fixture) when larger, x1.5 (three
-    re-associations sample the spread; one more is another draw)."""
+    sums when larger (tests/golden/iteration_spread.json, made by
+    tools/noise_floor_iterations.py): the largest deviation over the config
+    family (6 seeds x 2 re-associations, ~ the 92 % quantile of a single
+    re-associated run) or over this instance's three re-associations.  A
+    tree-mode run is one more draw from that distribution."""
     import json
     from pathlib import Path
 
     spread = json.loads((Path(__file__).parent / "golden" / "iteration_spread.json").read_text())
-    row = spread[f"cfg{cfg}_s{seed}_x{scale}"]
-    return max(0.05, 1.5 * row["max_abs_iter_dev"])
+    inst = spread.get(f"cfg{cfg}_s{seed}_x{scale}", {}).get("max_abs_iter_dev", 0.0)
+    return max(0.05, inst, spread["family_spread"][f"cfg{cfg}"])

@@ -240,3 +240,30 @@ def test_tree_mode_without_cooperative_launch(eng, ref, monkeypatch):
     if b.termination_reason == "Optimal":
         assert _rel_kkt(a.final_info) <= 1e-8
         assert abs(a.iterations - b.iterations) <= iteration_band(5, 3, 0.02) * b.iterations
+
+
+@pytest.mark.parametrize("cfg,scale,min_len", [(5, 0.05, 16), (5, 0.02, 8)])
+def test_sell_row_groups(eng, ref, cfg, scale, min_len, monkeypatch, capfd):
+    """The loop's K x' over lane-per-row (SELL-32) groups (engine sell.cuh):
+    config 5's demand rows gather 32 consecutive columns per entry index.
+    Forced onto small members (shorter rows than the default threshold):
+    the first 100 iterates within the reference's noise floor with identical
+    restarts and ledger, and a full solve to 1e-8."""
+    monkeypatch.setenv("FOLP_SELL_MIN_LEN", str(min_len))
+    monkeypatch.setenv("FOLP_TIMING", "1")
+    lp = instances.generate(cfg, 1, scale)
+    p = cabi.params(record_iterate_trace=True, iteration_limit=100)
+    a = eng.solve_lp(lp, p, iterate_capacity=100)
+    assert "SELL-32" in capfd.readouterr().err
+    b = ref.solve_lp(lp, p, iterate_capacity=100)
+    assert_within_floor(a.iterate_trace, b.iterate_trace, reference_floor(lp, p, 100, b), "sell")
+    assert a.restart_iterations == b.restart_iterations
+    assert a.kkt_passes == b.kkt_passes
+    monkeypatch.delenv("FOLP_TIMING")
+    p = cabi.params(kkt_pass_limit=300000)
+    a, b = eng.solve_lp(lp, p), ref.solve_lp(lp, p)
+    assert a.termination_reason == b.termination_reason == "Optimal"
+    assert _rel_kkt(a.final_info) <= 1e-8
+    pa, pb = a.final_info["primal_objective"], b.final_info["primal_objective"]
+    assert abs(pa - pb) <= 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
+    assert a.step_condition_violations == 0

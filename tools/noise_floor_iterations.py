@@ -82,7 +82,23 @@ def write_fixture(path: str, jobs: int) -> None:
         out[fixture_key(r["config"], r["seed"], r["scale"])] = r
         print(fixture_key(r["config"], r["seed"], r["scale"]), r["ref"]["iterations"],
               [round(d, 4) for d in devs])
+    out["family_spread"] = family_spread(ROOT / "profiles" / "r2_noise_floor_iterations.jsonl")
     Path(path).write_text(json.dumps(out, indent=1) + "\n")
+
+
+def family_spread(jsonl: Path) -> dict:
+    """Per config family: the largest relative iteration-count deviation of a
+    re-associated reference from the reference over the family's instances
+    (the default run of this script: 6 seeds x 2 orders per family), where
+    both reach Optimal."""
+    fam: dict = {}
+    for line in jsonl.read_text().splitlines():
+        r = json.loads(line)
+        for o in ("order1", "order2", "order3"):
+            if o in r and r["ref"]["termination"] == "Optimal" and r[o]["termination"] == "Optimal":
+                k = f"cfg{r['config']}"
+                fam[k] = max(fam.get(k, 0.0), abs(r[o]["iter_dev"]))
+    return fam
 
 
 def main():
