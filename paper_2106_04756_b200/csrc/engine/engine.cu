@@ -47,6 +47,7 @@
 #include <vector>
 
 #include "folp_gpu.h"
+#include "../host/parallel.hpp"
 #include "ops.cuh"
 #include "exactfold.cuh"
 
@@ -697,12 +698,42 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
       c->loop_block = blk;
       c->loop_block_bytes = 2 * vb + 2 * ib;
     }
+    // the CSR streams: narrowed / copied into pinned blocks by all host
+    // threads, then one DMA each (pageable copies ran at ~8 GB/s: 7 ms of
+    // config 2's end-to-end solve)
+    std::vector<void*> pinned;
+    auto stage_in = [&](void* dst, const void* src, int64_t count, bool narrow) {
+      if (count <= 0) return;
+      const size_t bytes = static_cast<size_t>(count) * (narrow ? sizeof(int) : sizeof(double));
+      void* h = block_alloc(bytes, true);
+      pinned.push_back(h);
+      folp::host::parallel_for(count, [&](int64_t b, int64_t e, int) {
+        if (narrow) {
+          const int64_t* s64 = static_cast<const int64_t*>(src);
+          int* d32 = static_cast<int*>(h);
+          for (int64_t i = b; i < e; ++i) d32[i] = static_cast<int>(s64[i]);
+        } else {
+          std::memcpy(static_cast<double*>(h) + b, static_cast<const double*>(src) + b,
+                      static_cast<size_t>(e - b) * sizeof(double));
+        }
+      });
+      CK(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    };
+    auto release_pinned = [&] {
+      cudaStreamSynchronize(c->stream);
+      for (void* h : pinned) block_free(h);
+      pinned.clear();
+    };
     {
       const int64_t cap = std::min<int64_t>(std::max<int64_t>({m + 1, n + 1, nnz}), int64_t(1) << 26);
       int64_t* stage = dalloc<int64_t>(cap);
       try {
         upload_index(c.get(), p->row_start, c->csr_ptr, m + 1, stage, cap);
-        upload_index(c.get(), p->row_cols, c->csr_col, nnz, stage, cap);
+        if (nnz < (int64_t(1) << 20)) {
+          upload_index(c.get(), p->row_cols, c->csr_col, nnz, stage, cap);
+        } else {
+          stage_in(c->csr_col, p->row_cols, nnz, true);
+        }
         if (rank_d != nullptr && nnz > 0) {
           k_renumber<<<c->simple_grid(nnz), kBlock, 0, c->stream>>>(c->csr_col, rank_d, nnz);
           ++c->launches;
@@ -715,12 +746,22 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
         CK(cudaStreamSynchronize(c->stream));
       } catch (...) {
         block_free(stage);
+        release_pinned();
         throw;
       }
       block_free(stage);
     }
     mark("indices");
-    upload(c.get(), c->csr_orig, p->row_values, nnz);
+    try {
+      if (nnz < (int64_t(1) << 20) || p->row_values == nullptr) {
+        upload(c.get(), c->csr_orig, p->row_values, nnz);
+      } else {
+        stage_in(c->csr_orig, p->row_values, nnz, false);
+      }
+    } catch (...) {
+      release_pinned();
+      throw;
+    }
     if (device_csc) {
       device_transpose(c.get(), cs);
       col_start = cs.data();
@@ -729,6 +770,7 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
     }
     copy_d2d(c.get(), c->csr_work, c->csr_orig, nnz);
     copy_d2d(c.get(), c->csc_work, c->csc_orig, nnz);
+    release_pinned();
 
     mark("values");
     build_plan(c.get(), p->row_start, m, nnz, c->csr_ptr, c->csr_col, c->rows);

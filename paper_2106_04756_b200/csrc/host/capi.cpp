@@ -108,11 +108,10 @@ SparseMatrix matrix_from_csr(const folp_lp_c* in) {
         }
       }
     }
-  });
+  }, nnz + m);
   const bool canonical = std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
   if (canonical) {
-    std::vector<Index> start(in->row_start, in->row_start + m + 1);
-    return SparseMatrixAccess::build(m, n, std::move(start),
+    return SparseMatrixAccess::build(m, n, host::parallel_copy(in->row_start, m + 1),
                                      host::parallel_copy(in->row_cols, nnz),
                                      host::parallel_copy(in->row_values, nnz));
   }

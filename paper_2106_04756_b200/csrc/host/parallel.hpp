@@ -15,14 +15,15 @@ namespace folp::host {
 
 inline int host_threads(int64_t work) {
   const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  const int64_t by_work = std::max<int64_t>(1, work / (int64_t(1) << 20));  // >= 1M items each
+  const int64_t by_work = std::max<int64_t>(1, work / (int64_t(1) << 17));  // >= 128K items each
   return static_cast<int>(std::min<int64_t>({hw, by_work, 32}));
 }
 
-// f(begin, end, thread) over [0, n) split into contiguous chunks.
+// f(begin, end, thread) over [0, n) split into contiguous chunks; `work`
+// (default n) sizes the thread count (a row loop passes its nonzeros).
 template <class F>
-void parallel_for(int64_t n, F&& f) {
-  const int t = host_threads(n);
+void parallel_for(int64_t n, F&& f, int64_t work = -1) {
+  const int t = static_cast<int>(std::min<int64_t>(host_threads(work < 0 ? n : work), std::max<int64_t>(n, 1)));
   if (t <= 1) {
     f(int64_t(0), n, 0);
     return;
@@ -50,11 +51,27 @@ std::vector<T> parallel_copy(const T* src, int64_t n) {
   return out;
 }
 
-// counts[v] += 1 for every v in keys[0, n) (0 <= v < bins); relaxed atomic
-// increments on the shared array (per-thread histograms would cost bins x
-// threads of memory for config 4's 4*10^7 columns).
+// counts[v] += 1 for every v in keys[0, n) (0 <= v < bins).  Per-thread
+// 32-bit histograms merged by bin range when they fit (config 2: 400k bins;
+// no contention on the power law's hot bins), relaxed atomics on the shared
+// array otherwise (config 4's 4*10^7 columns x threads would not fit).
 inline void parallel_histogram(const int64_t* keys, int64_t n, int64_t bins, int64_t* counts) {
-  (void)bins;
+  const int t = host_threads(n);
+  if (t > 1 && bins * t * 4 <= (int64_t(256) << 20) && bins < (int64_t(1) << 31) && n < (int64_t(1) << 31)) {
+    std::vector<std::vector<int32_t>> local(static_cast<std::size_t>(t));
+    parallel_for(n, [&](int64_t b, int64_t e, int i) {
+      std::vector<int32_t>& h = local[static_cast<std::size_t>(i)];
+      h.assign(static_cast<std::size_t>(bins), 0);
+      for (int64_t k = b; k < e; ++k) ++h[static_cast<std::size_t>(keys[k])];
+    });
+    parallel_for(bins, [&](int64_t b, int64_t e, int) {
+      for (const auto& h : local) {
+        if (h.empty()) continue;
+        for (int64_t v = b; v < e; ++v) counts[v] += h[static_cast<std::size_t>(v)];
+      }
+    }, bins * t);
+    return;
+  }
   parallel_for(n, [&](int64_t b, int64_t e, int) {
     for (int64_t k = b; k < e; ++k) {
       std::atomic_ref<int64_t>(counts[keys[k]]).fetch_add(1, std::memory_order_relaxed);

@@ -6,6 +6,7 @@
 
 #include <memory>
 
+#include "folp/presolve.hpp"
 #include "folp/solver.hpp"
 #include "folp_gpu.h"
 
@@ -37,5 +38,11 @@ class SolveSession {
 // the same result.
 SolveResult solve_sharded(const LinearProgram& lp_raw, const SolverParams& params,
                           const PrimalDualPoint& z0, const folp_gpu_shard& shard);
+
+namespace detail {
+// presolve_for_solve that also returns the column degrees of `lp`
+// (presolve.cpp; the driver's column ordering reuses them)
+PresolveResult presolve_for_solve(const LinearProgram& lp, std::vector<Index>* degrees);
+}  // namespace detail
 
 }  // namespace folp

@@ -204,6 +204,7 @@ class Driver {
   PresolveTransform transform_;
   LinearProgram presolved_storage_;
   std::vector<Index> col_order_;   // working column order on the device (empty: identity)
+  std::vector<Index> raw_degrees_; // column degrees of raw_ (from presolve)
   bool raw_on_device_ = false;      // the device matrix is raw K (column order aside)
   const LinearProgram* work_ = nullptr;  // the presolved LP (raw_ when identity)
   std::unique_ptr<device::Context> dev_;
@@ -448,9 +449,14 @@ void Driver::order_columns() {
   const SparseMatrix& k = work_->constraint_matrix;
   const Index n = work_->num_variables(), nnz = k.nnz();
   if (nnz == 0 || (mode != 1 && n < (Index(1) << 16))) return;
-  const std::span<const Index> cols = k.row_cols();
-  std::vector<Index> deg(static_cast<std::size_t>(n), 0);
-  host::parallel_histogram(cols.data(), nnz, n, deg.data());
+  std::vector<Index> deg;
+  if (work_ == &raw_ && static_cast<Index>(raw_degrees_.size()) == n) {
+    deg.swap(raw_degrees_);  // counted by presolve already
+  } else {
+    const std::span<const Index> cols = k.row_cols();
+    deg.assign(static_cast<std::size_t>(n), 0);
+    host::parallel_histogram(cols.data(), nnz, n, deg.data());
+  }
   const Index max_deg = *std::max_element(deg.begin(), deg.end());
   if (mode != 1 && static_cast<double>(max_deg) < 16.0 * static_cast<double>(nnz) / static_cast<double>(n)) {
     return;
@@ -486,7 +492,7 @@ std::optional<SolveResult> Driver::start() {
 
   mark("validated");
   if (p_.use_presolve) {
-    PresolveResult pre = presolve_for_solve(raw_);
+    PresolveResult pre = detail::presolve_for_solve(raw_, &raw_degrees_);
     if (pre.status != PresolveStatus::kReduced) return finish_detected(pre.status);
     transform_ = std::move(pre.transform);
     if (transform_.is_identity() && pre.reduced.objective_constant == raw_.objective_constant) {
