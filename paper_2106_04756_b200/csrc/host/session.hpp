@@ -7,6 +7,7 @@
 #include <memory>
 
 #include "folp/presolve.hpp"
+#include "folp/sharded.hpp"
 #include "folp/solver.hpp"
 #include "folp_gpu.h"
 
@@ -33,11 +34,7 @@ class SolveSession {
   std::unique_ptr<Impl> impl_;
 };
 
-// folp::solve as one row shard of a multi-GPU solve: every
-// shard calls it with the same LP, parameters and start point and receives
-// the same result.
-SolveResult solve_sharded(const LinearProgram& lp_raw, const SolverParams& params,
-                          const PrimalDualPoint& z0, const folp_gpu_shard& shard);
+// folp::solve_sharded: include/folp/sharded.hpp
 
 namespace detail {
 // presolve_for_solve that also returns the column degrees of `lp`

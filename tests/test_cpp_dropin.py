@@ -156,3 +156,49 @@ def test_unit_suites_on_gpu(tmp_path):
     assert m, r.stdout[-2000:]
     assert int(m.group(3)) == 0 and int(m.group(1)) >= 100, m.group(0)
     assert r.returncode == 0
+
+
+SHARDED = r'''
+#include "folp/sharded.hpp"
+#include <cstdio>
+#include <vector>
+// two loopback shards (include/folp_gpu.h) of one solve through the public
+// C++ entry point; run only where a GPU is visible (argv[1] == "run")
+int main(int argc, char** argv) {
+  folp::LinearProgram lp;
+  const std::vector<folp::Triplet> t = {{0, 0, 1.0}, {0, 1, 1.0}};
+  lp.constraint_matrix = folp::SparseMatrix::from_triplets(1, 2, t);
+  lp.objective = {1.0, 2.0};
+  lp.right_hand_side = {1.0};
+  lp.variable_lower = {0.0, 0.0};
+  lp.variable_upper = {10.0, 10.0};
+  lp.num_inequality_rows = 0;
+  if (argc < 2) return 0;
+  void* group = nullptr;
+  if (folp_gpu_loopback_create(1, &group) != 0) return 3;
+  folp_gpu_shard spec{};
+  spec.rank = 0;
+  spec.world = 1;
+  spec.backend = FOLP_SHARD_LOOPBACK;
+  spec.loopback = group;
+  const folp::SolveResult r = folp::solve_sharded(lp, folp::SolverParams{}, folp::PrimalDualPoint{}, spec);
+  std::printf("%s %.6f\n", folp::to_string(r.termination_reason).c_str(), r.final_info.primal_objective);
+  folp_gpu_loopback_destroy(group);
+  return r.termination_reason == folp::TerminationReason::kOptimal ? 0 : 1;
+}
+'''
+
+
+def test_solve_sharded_public_header_compiles_and_links(tmp_path):
+    """folp::solve_sharded is declared in the public include/folp/sharded.hpp
+    and exported by the product library (a caller compiles and links)."""
+    src = tmp_path / "sharded.cpp"
+    src.write_text(SHARDED)
+    exe = tmp_path / "sharded"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ROOT / 'include'}", str(src), "-o", str(exe),
+                    f"-L{PRODUCT.parent}", "-lfolp_b200", f"-Wl,-rpath,{PRODUCT.parent}"],
+                   check=True)
+    assert subprocess.run([str(exe)]).returncode == 0
+    if _has_gpu():
+        r = subprocess.run([str(exe), "run"], capture_output=True, text=True)
+        assert r.returncode == 0 and r.stdout.startswith("Optimal"), (r.stdout, r.stderr)
