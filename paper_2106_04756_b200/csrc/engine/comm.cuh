@@ -34,6 +34,10 @@ struct ShardComm {
   double** peer_src_d = nullptr;  // [2][W] device: this rank's W slots
   virtual void peer_setup(int64_t count) { (void)count; }
   virtual void peer_fence(cudaStream_t s) { (void)s; }
+  // Every rank's `mine` (a cudaMalloc base pointer of this rank's buffer)
+  // as addressable from this rank: [W] (CUDA IPC on NCCL ranks, plain
+  // pointers on the loopback group).  Collective: every rank calls it.
+  virtual std::vector<double*> exchange_pointers(double* mine) = 0;
   double* const* peer_dst(int parity) const { return peer_dst_d + parity * world; }
   const double* const* peer_src(int parity) const { return peer_src_d + parity * world; }
   // device pointer tables from host vectors ([2][W] each)
@@ -117,10 +121,39 @@ struct NcclComm final : ShardComm {
     for (size_t r = 0; r < peer_areas.size(); ++r) {
       if (peer_areas[r] && static_cast<int>(r) != rank) cudaIpcCloseMemHandle(peer_areas[r]);
     }
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
     free_tables();
     if (area) cudaFree(area);
     if (scratch) cudaFree(scratch);
     if (comm) nccl_api().comm_destroy(comm);
+  }
+  std::vector<void*> opened;  // IPC mappings of exchange_pointers, closed at exit
+  std::vector<double*> exchange_pointers(double* mine_ptr) override {
+    const NcclApi& api = nccl_api();
+    if (api.all_gather == nullptr) throw EngineError(FOLP_E_RUNTIME, "ncclAllGather missing");
+    cudaIpcMemHandle_t mine;
+    CK(cudaIpcGetMemHandle(&mine, mine_ptr));
+    std::vector<cudaIpcMemHandle_t> all(world);
+    char* dev = nullptr;
+    CK(cudaMalloc(&dev, world * sizeof(cudaIpcMemHandle_t)));
+    CK(cudaMemcpy(dev + rank * sizeof(cudaIpcMemHandle_t), &mine, sizeof(mine), cudaMemcpyHostToDevice));
+    NCK(api.all_gather(dev + rank * sizeof(cudaIpcMemHandle_t), dev, sizeof(cudaIpcMemHandle_t),
+                       ncclUint8, comm, nullptr));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(all.data(), dev, world * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    std::vector<double*> out(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) {
+        out[r] = mine_ptr;
+      } else {
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess));
+        opened.push_back(ptr);
+        out[r] = static_cast<double*>(ptr);
+      }
+    }
+    return out;
   }
   // Receive areas: allocated here, exported as CUDA IPC handles, the handles
   // all-gathered through NCCL, the peers' areas opened with peer access.
@@ -292,6 +325,13 @@ struct LoopbackComm final : ShardComm {
     g->barrier();
     upload_tables(dst, src);
     peer = true;
+  }
+  std::vector<double*> exchange_pointers(double* mine) override {
+    g->ptrs[rank] = mine;
+    g->barrier();
+    std::vector<double*> out(g->ptrs.begin(), g->ptrs.end());
+    g->barrier();
+    return out;
   }
   // The producers of every shard have finished: no kernel ever waits on
   // another shard's kernel (they share one GPU).

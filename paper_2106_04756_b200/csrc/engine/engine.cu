@@ -225,6 +225,12 @@ struct folp_gpu_ctx {
   double* lcsc_val = nullptr;
   double* kty_part = nullptr;
   int peer_parity = 0;  // receive-area parity of the next peer exchange
+  // partitioned dual epilogue (column partition + peer exchange, DESIGN 7):
+  // own rows [pd_bounds[rank], pd_bounds[rank+1]) of equal chunks pd_chunk
+  bool pdual = false;
+  int64_t pd_chunk = 0;
+  std::vector<int64_t> pd_bounds;
+  double** pd_ydst = nullptr;  // device [2][W]: every rank's y[0], y[1]
   bool hot_columns = false;  // created with a degree order (folp_gpu_create_ordered)
   double* shard_sums = nullptr;
   bool shard_values_ready = false;
@@ -1724,7 +1730,31 @@ int folp_gpu_shard_attach(folp_gpu_ctx* c, const folp_gpu_shard* spec, const int
       bool peer = spec->backend == FOLP_SHARD_LOOPBACK;
       if (env != nullptr && std::strcmp(env, "peer") == 0) peer = true;
       if (env != nullptr && std::strcmp(env, "collective") == 0) peer = false;
-      if (peer) c->comm->peer_setup(c->col_part ? m + 2 : n);
+      // column partition over the peer exchange: the dual epilogue runs on
+      // each rank's own rows (FOLP_SHARD_EPILOGUE=replicated keeps it on
+      // every rank for all m rows)
+      const char* epi = std::getenv("FOLP_SHARD_EPILOGUE");
+      c->pdual = peer && c->col_part && spec->world > 1 &&
+                 !(epi != nullptr && std::strcmp(epi, "replicated") == 0);
+      if (peer) c->comm->peer_setup(c->col_part ? m + (c->pdual ? 8 : 2) : n);
+      if (c->pdual) {
+        const int W = spec->world;
+        c->pd_chunk = (m + W - 1) / W;
+        c->pd_bounds.assign(static_cast<size_t>(W) + 1, 0);
+        for (int r = 0; r <= W; ++r) c->pd_bounds[r] = std::min<int64_t>(m, r * c->pd_chunk);
+        std::vector<double*> tab(2 * static_cast<size_t>(W));
+        for (int par = 0; par < 2; ++par) {
+          const std::vector<double*> ptrs = c->comm->exchange_pointers(c->y[par]);
+          for (int r = 0; r < W; ++r) tab[par * W + r] = ptrs[r];
+        }
+        c->pd_ydst = c->alloc<double*>(tab.size());
+        CK(cudaMemcpy(c->pd_ydst, tab.data(), tab.size() * sizeof(double*), cudaMemcpyHostToDevice));
+        if (std::getenv("FOLP_TIMING") != nullptr) {
+          std::fprintf(stderr, "[folp timing] shard %d/%d: partitioned dual epilogue, rows [%lld, %lld)\n",
+                       spec->rank, W, static_cast<long long>(c->pd_bounds[spec->rank]),
+                       static_cast<long long>(c->pd_bounds[spec->rank + 1]));
+        }
+      }
     }
     c->shard_sums = c->alloc<double>(4);
     c->shard_values_ready = false;

@@ -370,6 +370,9 @@ struct EpiShardPart {
   int world = 0;
   const double* extra = nullptr;
   int64_t extra_at = 0;
+  // partitioned dual epilogue (column partition): row j's partial goes to
+  // its owner's area only, owner = j / own_chunk (0: every rank's)
+  int64_t own_chunk = 0;
   __device__ bool prepare() {
     if (!b.st->running) return false;
     v = trial_x ? pick(b.x, b.st->cur ^ 1) : pick(b.y, b.st->cur);
@@ -384,7 +387,12 @@ struct EpiShardPart {
       out[j] = dot;
       return;
     }
-    for (int r = 0; r < world; ++r) outs[r][j] = dot;
+    if (own_chunk > 0) {
+      const int64_t o = j / own_chunk;
+      outs[o < world ? o : world - 1][j] = dot;
+    } else {
+      for (int r = 0; r < world; ++r) outs[r][j] = dot;
+    }
     if (j == 0 && extra != nullptr) {
       const double e0 = extra[0], e1 = extra[1];
       for (int r = 0; r < world; ++r) {
@@ -463,6 +471,60 @@ struct OpShardDual {
   }
   __device__ void finalize_ordered(const double*, int64_t) const {}
 };
+
+// Partitioned dual epilogue of the column partition (peer exchange; DESIGN
+// 7): rank p owns rows [r0, r1) = [p c, (p+1) c).  The partial products
+// reached their owner only (EpiShardPart own_chunk), so the owner sums the
+// W slots of its rows in rank order, runs kernel B's epilogue on them --
+// y', Kx', the lazy average, the trial sums over its rows -- and stores y'
+// straight into every rank's y' vector and its three partial sums into
+// slot p of every rank's area at [m + 2, m + 5).  After the second fence
+// k_shard_decide_rows folds the W partial sums in rank order (identical on
+// every rank) and decides.  The replicated epilogue ran all m rows on every
+// rank; this one runs m / W (config 4 at W = 8: 1.2 GB -> 150 MB per rank
+// and trial).
+struct OpShardDualOwn {
+  static constexpr int K = 3;
+  static constexpr bool kReduce = true;
+  EpiDual e;
+  const double* const* src;   // this rank's W slots (current parity)
+  double* const* sdst;        // slot `rank` of every rank's area (current parity)
+  double* const* ydst2;       // [2][W] every rank's y[0], y[1]
+  double* const* ydst = nullptr;
+  int world = 0, rank = 0;
+  int64_t r0 = 0, m = 0;
+  __device__ bool prepare() {
+    if (!e.prepare()) return false;
+    ydst = ydst2 + (e.b.st->cur ^ 1) * world;
+    return true;
+  }
+  template <class Acc>
+  __device__ void apply(int64_t k, Acc& acc) const {
+    const int i = static_cast<int>(r0 + k);
+    e.apply(i, sum_slots(src, world, i), e.load(i), acc);
+    const double v = e.yn[i];
+    for (int r = 0; r < world; ++r) {
+      if (r != rank) ydst[r][i] = v;
+    }
+  }
+  __device__ void finalize(const double (&tot)[K]) const {
+    for (int r = 0; r < world; ++r) {
+      for (int k = 0; k < K; ++k) sdst[r][m + 2 + k] = tot[k];
+    }
+  }
+  __device__ void finalize_ordered(const double*, int64_t) const {}
+};
+
+__global__ void k_shard_decide_rows(LoopBufs b, const double* const* src, int world, int64_t m) {
+  const DevState* st = b.st;
+  if (!st->running) return;
+  const double sx = sum_slots(src, world, m), bad = sum_slots(src, world, m + 1);
+  const double cross = sum_slots(src, world, m + 2), dy2 = sum_slots(src, world, m + 3);
+  const double flag = sum_slots(src, world, m + 4);
+  double movement = dy2 / st->omega;  // solver.cpp:83, on the global sums
+  movement = movement + sx;
+  decide_trial(b, cross, movement, bad != 0.0 || flag != 0.0);
+}
 
 // ---------------------------------------------------------------------
 // Small problems (config 1: 10^4 nonzeros): a whole chunk of trials in ONE

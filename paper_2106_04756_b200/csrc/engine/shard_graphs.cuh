@@ -66,6 +66,10 @@ void ensure_gathered(folp_gpu_ctx* c) {
   if (c->col_part) {  // y, Kx and avg_y are replicated; x and avg_x are not
     c->comm->gather_rows(c->x[cur], c->shard_bounds, c->stream);
     c->comm->gather_rows(c->avg_x, c->shard_bounds, c->stream);
+    if (c->pdual) {  // ... and with the partitioned dual epilogue Kx, avg_y are not
+      c->comm->gather_rows(c->kx[cur], c->pd_bounds, c->stream);
+      c->comm->gather_rows(c->avg_y, c->pd_bounds, c->stream);
+    }
   } else {
     c->comm->gather_rows(c->y[cur], c->shard_bounds, c->stream);
     c->comm->gather_rows(c->kx[cur], c->shard_bounds, c->stream);
@@ -97,8 +101,22 @@ void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
       sp.world = comm.world;
       sp.extra = c->kty_part + c->m;
       sp.extra_at = c->m;
+      if (c->pdual) sp.own_chunk = c->pd_chunk;
       c->seg(c->lrows, c->lcsc_val, sp, 1);
       comm.peer_fence(c->stream);
+      if (c->pdual) {  // own rows only, y' and the partial sums to every rank
+        OpShardDualOwn od{EpiDual{b}, comm.peer_src(par), comm.peer_dst(par), c->pd_ydst};
+        od.world = comm.world;
+        od.rank = comm.rank;
+        od.r0 = c->pd_bounds[comm.rank];
+        od.m = c->m;
+        c->ew(c->pd_bounds[comm.rank + 1] - od.r0, od, 3);
+        comm.peer_fence(c->stream);
+        k_shard_decide_rows<<<1, 1, 0, c->stream>>>(b, comm.peer_src(par), comm.world, c->m);
+        ++c->launches;
+        CK(cudaGetLastError());
+        return;
+      }
       OpShardDual od{EpiDual{b}, nullptr, nullptr};
       od.src = comm.peer_src(par);
       od.world = comm.world;

@@ -180,3 +180,88 @@ def test_gloo_world2_exchange_algebra():
         assert kx_exact
         assert same
         assert rows > 0
+
+
+def _pdual_rank_main(rank, world, port, out):
+    """The partitioned dual epilogue (engine OpShardDualOwn) restated with
+    gloo collectives: owner-only partial rows (a reduce-scatter in rank
+    order), the dual step on the own rows, y' to every rank (all-gather) and
+    the three trial sums folded over the ranks in rank order."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lp = instances.generate(5, 2, 0.004)
+        a, c = _csc(lp)
+        m = lp.num_rows
+        rng = np.random.default_rng(11)
+        x1 = rng.random(lp.num_cols)          # trial primal
+        y0 = rng.standard_normal(m)
+        y0[:lp.num_inequality_rows] = np.abs(y0[:lp.num_inequality_rows])
+        kx0 = a @ rng.random(lp.num_cols)     # previous Kx
+        sigma = 0.37
+        bc = shard.shard_rows(lp.num_cols, c.indptr, world)
+        c0, c1 = int(bc[rank]), int(bc[rank + 1])
+        lptr, pos = shard.local_csr(m, c.indptr, c.indices, c0, c1)
+        cols = np.searchsorted(c.indptr, pos, side="right") - 1
+        rows = np.repeat(np.arange(m), np.diff(lptr))
+        part = np.zeros(m)
+        np.add.at(part, rows, c.data[pos] * x1[cols])
+        chunk = (m + world - 1) // world
+        r0, r1 = min(m, rank * chunk), min(m, (rank + 1) * chunk)
+        # owner-only stores: every rank's partial rows of [r0, r1) reach this rank
+        slots = [torch.zeros(m, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(slots, torch.from_numpy(part))
+        kx1 = slots[0][r0:r1].numpy().copy()
+        for r in range(1, world):
+            kx1 = kx1 + slots[r][r0:r1].numpy()
+        # dual step on the own rows (solver.cpp:66-82)
+        i = np.arange(r0, r1)
+        v = y0[i] + sigma * (lp.right_hand_side[i] - (2.0 * kx1 - kx0[i]))
+        ineq = i < lp.num_inequality_rows
+        v[ineq] = np.maximum(v[ineq], 0.0)
+        dy = v - y0[i]
+        sums = torch.tensor([np.sum(dy * (kx0[i] - kx1)), np.sum(dy * dy)], dtype=torch.float64)
+        allsums = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allsums, sums)
+        tot = allsums[0].clone()
+        for r in range(1, world):
+            tot += allsums[r]
+        # y' assembled on every rank
+        ypart = torch.zeros(m, dtype=torch.float64)
+        ypart[r0:r1] = torch.from_numpy(v)
+        yall = [torch.zeros(m, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(yall, ypart)
+        y1 = sum(yall).numpy()
+        # the unpartitioned dual step
+        kx1f = a @ x1
+        vf = y0 + sigma * (lp.right_hand_side - (2.0 * kx1f - kx0))
+        vf[:lp.num_inequality_rows] = np.maximum(vf[:lp.num_inequality_rows], 0.0)
+        dyf = vf - y0
+        want = np.array([np.sum(dyf * (kx0 - kx1f)), np.sum(dyf * dyf)])
+        scale = 1.0 + np.max(np.abs(vf))
+        out.put((rank, float(np.max(np.abs(y1 - vf)) / scale),
+                 float(np.max(np.abs(tot.numpy() - want) / (1.0 + np.abs(want)))),
+                 tot.numpy().tolist(), r1 - r0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_partitioned_dual_epilogue():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pdual_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    assert [r[0] for r in res] == [0, 1]
+    assert res[0][3] == res[1][3]  # identical folded sums on both ranks
+    for _, y_err, sum_err, _, rows in res:
+        assert y_err <= 1e-13 and sum_err <= 1e-12 and rows > 0
