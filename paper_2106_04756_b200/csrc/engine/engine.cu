@@ -286,7 +286,12 @@ struct folp_gpu_ctx {
     const int64_t need = (count + kBlock - 1) / kBlock;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, sms * 8)));
   }
-  RedBuf red(int counter) { return RedBuf{partials, counters + counter, nullptr, 0}; }
+  RedBuf red(int counter) {
+    RedBuf rb{partials, counters + counter, nullptr, 0};
+    rb.cap = partial_cap;
+    return rb;
+  }
+  int partial_cap = 0;  // slots (of kMaxAcc doubles) in `partials`
 
   // exact parallel fold (exactfold.cuh) of ordered mode's trial sums
   FoldScratch fold{};
@@ -384,7 +389,18 @@ struct folp_gpu_ctx {
     return stage_env != 0 && (&p == &rows || &p == &cols) && p.sp.vec_len > 0 &&
            p.sp.vec_len * static_cast<int64_t>(sizeof(double)) <= kStageMaxBytes;
   }
-  template <class Epi, bool ORD, bool PR, bool ST = false, bool SE = false>
+  // Hot-prefix staging for the rows plan of a degree-ordered context:
+  // FOLP_HOT_STAGE = entries (0 off).
+  int hot_stage = -1;
+  int hot_stage_len(const PlanDev& p) {
+    if (hot_stage < 0) {
+      const char* env = std::getenv("FOLP_HOT_STAGE");
+      hot_stage = env != nullptr ? std::max(0, std::atoi(env)) : 0;
+    }
+    if (hot_stage == 0 || !hot_columns || &p != &rows || p.sp.vec_len <= 0) return 0;
+    return std::min(hot_stage, p.sp.vec_len);
+  }
+  template <class Epi, bool ORD, bool PR, int ST = 0, bool SE = false>
   void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb,
                      int smem = 0) {
     auto fn = segdot_kernel<Epi, ORD, PR, ST, SE>;
@@ -397,7 +413,7 @@ struct folp_gpu_ctx {
     // Set per launch (a launch attribute, captured into graph nodes too), so
     // concurrent contexts of both kinds never share mutable state.
     const char* env = std::getenv("FOLP_CARVEOUT");
-    const int want = env != nullptr ? std::atoi(env) : (hot_columns ? kSegdotCarveout : -1);
+    const int want = ST != 0 ? 100 : env != nullptr ? std::atoi(env) : (hot_columns ? kSegdotCarveout : -1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kBlock);
@@ -453,17 +469,26 @@ struct folp_gpu_ctx {
       ++launches;
     } else if (p.sp.sell.n_groups > 0) {
       // a plan with SELL-32 groups (sell.cuh)
-      auto fn = segdot_kernel<Epi, false, false, false, true>;
+      auto fn = segdot_kernel<Epi, false, false, 0, true>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
-      launch_segdot<Epi, false, false, false, true>(grid, p.sp, val, epi, rb);
+      launch_segdot<Epi, false, false, 0, true>(grid, p.sp, val, epi, rb);
     } else if (stage_ok(p)) {
       // the gathered vector in shared memory (segdot.cuh, staged gathers)
-      auto fn = segdot_kernel<Epi, false, false, true>;
+      auto fn = segdot_kernel<Epi, false, false, 1>;
       const int smem = p.sp.vec_len * static_cast<int>(sizeof(double));
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn), smem);
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
-      launch_segdot<Epi, false, false, true>(grid, p.sp, val, epi, rb, smem);
+      launch_segdot<Epi, false, false, 1>(grid, p.sp, val, epi, rb, smem);
+    } else if (hot_stage_len(p) > 0) {
+      // the hot prefix of a degree-ordered x in shared memory (segdot.cuh STAGE 2)
+      SegPlan sp = p.sp;
+      sp.stage_len = hot_stage_len(p);
+      auto fn = segdot_kernel<Epi, false, false, 2>;
+      const int smem = sp.stage_len * static_cast<int>(sizeof(double));
+      const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn), smem);
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
+      launch_segdot<Epi, false, false, 2>(grid, sp, val, epi, rb, smem);
     } else {
       auto fn = segdot_kernel<Epi, false>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
@@ -824,6 +849,7 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
       c->ndg_compact = c->alloc<int>(2 * static_cast<size_t>(kBisectSmall));
     }
     c->partials = c->alloc<double>(static_cast<size_t>(kMaxGrid + c->max_giant + 8) * kMaxAcc);
+    c->partial_cap = kMaxGrid + c->max_giant + 8;
     if (c->ordered) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);
       c->terms[1] = c->alloc<double>(5 * (n + m) + 8);

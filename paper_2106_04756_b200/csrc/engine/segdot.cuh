@@ -48,6 +48,24 @@
 
 namespace folpgpu {
 
+// Checked build (lib/libfolp_b200_checked.so, -DFOLP_CHECKED): device-side
+// bounds and invariant checks on the products' index arithmetic -- gather
+// indices inside the gathered vector, tile / part / group ranges inside
+// their buffers, reduction slots inside the partials -- trapping with the
+// failing line.  compute-sanitizer is closed on this GPU pool; the checked
+// library runs the GPU parity cases instead (tests/test_gpu_checked.py).
+#ifdef FOLP_CHECKED
+#define FOLP_DCHECK(cond)                                                            \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("folp device check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define FOLP_DCHECK(cond) ((void)0)
+#endif
+
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kWarpTile = 256;        // nonzeros per tile / part (8 per lane)
@@ -113,6 +131,7 @@ struct SegPlan {
   double* part_sums;      // [n_units] (only part slots used)
   unsigned* arrivals;     // [n_multi], zero between launches
   int vec_len = 0;        // length of the gathered vector (0: unknown; staging off)
+  int stage_len = 0;      // STAGE 2: leading entries of the vector staged (hot prefix)
   SellPlan sell{};        // lane-per-segment groups (n_groups = 0: none)
 };
 
@@ -121,18 +140,24 @@ struct SegPlan {
 // after griddep_wait and every gather reads shared memory -- random 8-byte
 // shared loads run ~2.4x the L1tex gather rate (587 vs ~240 G/s,
 // profiles/r1_ceiling_cfg4.txt) and leave the L1tex pipe to the streams.
+// STAGE 2 stages only a prefix: with degree-ordered columns (config 2) the
+// hottest 4,096 columns of x take 34 % of K x's gathers, and the 4 CTAs an
+// SM holds at 64 registers leave ~160 KB of shared memory unused.
 constexpr int kStageMaxBytes = 96 * 1024;
-template <bool STAGE>
-__device__ __forceinline__ double gather(const double* __restrict__ v, int i) {
-  if constexpr (STAGE) {
-    return v[i];
+template <int STAGE>
+__device__ __forceinline__ double gather(const double* __restrict__ v, const double* sv, int i,
+                                         int stage_len) {
+  if constexpr (STAGE == 1) {
+    return sv[i];
+  } else if constexpr (STAGE == 2) {
+    return i < stage_len ? sv[i] : __ldg(&v[i]);
   } else {
     return __ldg(&v[i]);
   }
 }
 
 struct RedBuf {
-  double* partials;   // [(gridDim.x + n_multi) * K]
+  double* partials;   // [(gridDim.x + n_multi) * K]  (capacity `cap` slots of kMaxAcc)
   unsigned* counter;  // zero between launches (reset by the last block)
   double* terms;      // ordered mode: [K * nterm] per-segment terms
   int64_t nterm;      // ordered mode: segment (element) count
@@ -140,6 +165,7 @@ struct RedBuf {
                       // folds them and runs the finalize (exactfold.cuh)
   double* scratch = nullptr;  // ordered mode: [nnz] products of long segments
                               // (warp_exact_fold); null = one lane folds them
+  int cap = 0;                // partial slots allocated (checked build; 0 = unknown)
 };
 
 // Reduction sinks.  Tree mode accumulates in registers (fast, deterministic
@@ -304,6 +330,7 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   __shared__ int s_last;
   double tot[K];
   block_sum_vec<K>(acc, s_vec, tot);
+  FOLP_DCHECK(rb.cap == 0 || static_cast<int>(gridDim.x) + n_extra <= rb.cap);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) rb.partials[blockIdx.x * K + k] = tot[k];
@@ -431,7 +458,7 @@ __device__ __forceinline__ void prefetch_unit(const SegPlan& p, const double* va
   if (lane == 31 && d.x >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ptr + d.x));
 }
 
-template <class Epi, bool ORDERED, bool PROD = false, bool STAGE = false, bool SELLU = false>
+template <class Epi, bool ORDERED, bool PROD = false, int STAGE = 0, bool SELLU = false>
 #ifdef FOLP_WARP_TIMES
 #define FOLP_SEGDOT_BOUNDS __launch_bounds__(kBlock, kPlanCtasPerSm)  // same residency as the product build
 #else
@@ -451,9 +478,10 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   trace_warp<Epi>(0, global_ns());
 #endif
   const double* __restrict__ vec = epi.vec();
-  if constexpr (STAGE) {
-    extern __shared__ double s_stage[];
-    const int X = p.vec_len;
+  extern __shared__ double s_stage[];
+  const int stage_len = STAGE == 2 ? p.stage_len : p.vec_len;
+  if constexpr (STAGE != 0) {
+    const int X = stage_len;
     if ((reinterpret_cast<uintptr_t>(vec) & 15) == 0) {
       const double2* v2 = reinterpret_cast<const double2*>(vec);
       double2* s2 = reinterpret_cast<double2*>(s_stage);
@@ -463,7 +491,6 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       for (int i = threadIdx.x; i < X; i += kBlock) s_stage[i] = __ldcg(&vec[i]);
     }
     __syncthreads();
-    vec = s_stage;
   }
   const int* __restrict__ idx = p.idx;
   const int* __restrict__ ptr = p.ptr;
@@ -518,6 +545,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
     if (d.x >= 0) {
       // ---------------- tile of short segments ----------------
       const int seg0 = d.x, seg1 = d.y;
+      FOLP_DCHECK(seg0 <= seg1 && seg1 <= p.S && k1 - k0 <= kWarpTile && k0 <= k1);
       const int s_first = seg0 + lane;
       int b_first = 0, e_first = 0;
       typename Epi::Pre pre_first{};
@@ -530,10 +558,11 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
 #pragma unroll
       for (int j = 0; j < kWarpTile / 32; ++j) {
         const int k = k0 + lane + 32 * j;
+        FOLP_DCHECK(k >= k1 || p.vec_len == 0 || (idx[k] >= 0 && idx[k] < p.vec_len));
         if constexpr (PROD) {
           prod[j] = k < k1 ? val[k] : 0.0;
         } else {
-          prod[j] = k < k1 ? val[k] * gather<STAGE>(vec, idx[k]) : 0.0;
+          prod[j] = k < k1 ? val[k] * gather<STAGE>(vec, s_stage, idx[k], stage_len) : 0.0;
         }
       }
 #pragma unroll
@@ -551,6 +580,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
           pre = epi.load(s);
         }
         double sum = 0.0;
+        FOLP_DCHECK(b >= k0 && e <= k1 && b <= e);
         for (int k = b; k < e; ++k) sum += wbuf[k - k0];
         epi.apply(s, sum, pre, acc);
       }
@@ -559,7 +589,10 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       // ---------------- lane-per-segment group part (SELL-32) ----------------
       const SellPlan& q = p.sell;
       const int g = -d.x - kSellTag;
+      FOLP_DCHECK(g >= 0 && g < q.n_groups && d.z <= d.w);
+      FOLP_DCHECK(rb.cap == 0 || static_cast<int>(gridDim.x) + p.n_multi + g < rb.cap);
       const int np = q.nparts[g];
+      FOLP_DCHECK(d.y >= 0 && d.y < np);
       const int row = q.row0[g] + lane;
       const int base = q.base[g];
       typename Epi::Pre pre_one{};
@@ -594,9 +627,9 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
             v[t] = qv[32 * (j + t)];
           }
 #pragma unroll
-          for (int t = 0; t < 8; ++t) sum += v[t] * gather<STAGE>(vec, ix[t]);
+          for (int t = 0; t < 8; ++t) sum += v[t] * gather<STAGE>(vec, s_stage, ix[t], stage_len);
         }
-        for (; j < d.w; ++j) sum += qv[32 * j] * gather<STAGE>(vec, qi[32 * j]);
+        for (; j < d.w; ++j) sum += qv[32 * j] * gather<STAGE>(vec, s_stage, qi[32 * j], stage_len);
       }
       if (np == 1) {
         finish(sum, pre_one);
@@ -620,15 +653,18 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       // ---------------- part of a long segment ----------------
       const int multi = -d.x - 1;
       const bool single = d.y < 0;
+      FOLP_DCHECK(single ? (-d.y - 2 < p.S) : (multi < p.n_multi && d.y < p.n_units));
+      FOLP_DCHECK(single || rb.cap == 0 || static_cast<int>(gridDim.x) + multi < rb.cap);
       typename Epi::Pre pre_single{};
       if (single && lane == 0) pre_single = epi.load(-d.y - 2);  // in flight with the gathers
       double sum = 0.0;
 #pragma unroll 8
       for (int k = k0 + lane; k < k1; k += 32) {
+        FOLP_DCHECK(PROD || p.vec_len == 0 || (idx[k] >= 0 && idx[k] < p.vec_len));
         if constexpr (PROD) {
           sum += val[k];
         } else {
-          sum += val[k] * gather<STAGE>(vec, idx[k]);
+          sum += val[k] * gather<STAGE>(vec, s_stage, idx[k], stage_len);
         }
       }
 #pragma unroll
