@@ -129,7 +129,7 @@ int occupancy(const void* fn, int smem = 0) {
   const auto key = std::make_pair(fn, smem);
   auto it = g_occ.find(key);
   if (it != g_occ.end()) return it->second;
-  if (smem > 48 * 1024) {  // opt in once for the largest staging any context may use
+  if (smem > 0) {  // opt in once for the largest staging any context may use (static + dynamic > 48 KB)
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             std::max(smem, kStageMaxBytes)));
   }
@@ -389,17 +389,6 @@ struct folp_gpu_ctx {
     return stage_env != 0 && (&p == &rows || &p == &cols) && p.sp.vec_len > 0 &&
            p.sp.vec_len * static_cast<int64_t>(sizeof(double)) <= kStageMaxBytes;
   }
-  // Hot-prefix staging for the rows plan of a degree-ordered context:
-  // FOLP_HOT_STAGE = entries (0 off).
-  int hot_stage = -1;
-  int hot_stage_len(const PlanDev& p) {
-    if (hot_stage < 0) {
-      const char* env = std::getenv("FOLP_HOT_STAGE");
-      hot_stage = env != nullptr ? std::max(0, std::atoi(env)) : 0;
-    }
-    if (hot_stage == 0 || !hot_columns || &p != &rows || p.sp.vec_len <= 0) return 0;
-    return std::min(hot_stage, p.sp.vec_len);
-  }
   template <class Epi, bool ORD, bool PR, int ST = 0, bool SE = false>
   void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb,
                      int smem = 0) {
@@ -480,15 +469,6 @@ struct folp_gpu_ctx {
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn), smem);
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, false, false, 1>(grid, p.sp, val, epi, rb, smem);
-    } else if (hot_stage_len(p) > 0) {
-      // the hot prefix of a degree-ordered x in shared memory (segdot.cuh STAGE 2)
-      SegPlan sp = p.sp;
-      sp.stage_len = hot_stage_len(p);
-      auto fn = segdot_kernel<Epi, false, false, 2>;
-      const int smem = sp.stage_len * static_cast<int>(sizeof(double));
-      const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn), smem);
-      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
-      launch_segdot<Epi, false, false, 2>(grid, sp, val, epi, rb, smem);
     } else {
       auto fn = segdot_kernel<Epi, false>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));

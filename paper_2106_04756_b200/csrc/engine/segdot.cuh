@@ -131,7 +131,6 @@ struct SegPlan {
   double* part_sums;      // [n_units] (only part slots used)
   unsigned* arrivals;     // [n_multi], zero between launches
   int vec_len = 0;        // length of the gathered vector (0: unknown; staging off)
-  int stage_len = 0;      // STAGE 2: leading entries of the vector staged (hot prefix)
   SellPlan sell{};        // lane-per-segment groups (n_groups = 0: none)
 };
 
@@ -140,17 +139,15 @@ struct SegPlan {
 // after griddep_wait and every gather reads shared memory -- random 8-byte
 // shared loads run ~2.4x the L1tex gather rate (587 vs ~240 G/s,
 // profiles/r1_ceiling_cfg4.txt) and leave the L1tex pipe to the streams.
-// STAGE 2 stages only a prefix: with degree-ordered columns (config 2) the
-// hottest 4,096 columns of x take 34 % of K x's gathers, and the 4 CTAs an
-// SM holds at 64 registers leave ~160 KB of shared memory unused.
+// (Staging only the hot prefix of a degree-ordered x -- config 2's 2,048
+// hottest columns take 26 % of K x's gathers -- measured 56.3 -> 75.7 us per
+// trial: the shared carveout it needs takes the L1 that already held that
+// prefix.)
 constexpr int kStageMaxBytes = 96 * 1024;
 template <int STAGE>
-__device__ __forceinline__ double gather(const double* __restrict__ v, const double* sv, int i,
-                                         int stage_len) {
+__device__ __forceinline__ double gather(const double* __restrict__ v, const double* sv, int i) {
   if constexpr (STAGE == 1) {
     return sv[i];
-  } else if constexpr (STAGE == 2) {
-    return i < stage_len ? sv[i] : __ldg(&v[i]);
   } else {
     return __ldg(&v[i]);
   }
@@ -479,9 +476,8 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
 #endif
   const double* __restrict__ vec = epi.vec();
   extern __shared__ double s_stage[];
-  const int stage_len = STAGE == 2 ? p.stage_len : p.vec_len;
   if constexpr (STAGE != 0) {
-    const int X = stage_len;
+    const int X = p.vec_len;
     if ((reinterpret_cast<uintptr_t>(vec) & 15) == 0) {
       const double2* v2 = reinterpret_cast<const double2*>(vec);
       double2* s2 = reinterpret_cast<double2*>(s_stage);
@@ -562,7 +558,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         if constexpr (PROD) {
           prod[j] = k < k1 ? val[k] : 0.0;
         } else {
-          prod[j] = k < k1 ? val[k] * gather<STAGE>(vec, s_stage, idx[k], stage_len) : 0.0;
+          prod[j] = k < k1 ? val[k] * gather<STAGE>(vec, s_stage, idx[k]) : 0.0;
         }
       }
 #pragma unroll
@@ -627,9 +623,9 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
             v[t] = qv[32 * (j + t)];
           }
 #pragma unroll
-          for (int t = 0; t < 8; ++t) sum += v[t] * gather<STAGE>(vec, s_stage, ix[t], stage_len);
+          for (int t = 0; t < 8; ++t) sum += v[t] * gather<STAGE>(vec, s_stage, ix[t]);
         }
-        for (; j < d.w; ++j) sum += qv[32 * j] * gather<STAGE>(vec, s_stage, qi[32 * j], stage_len);
+        for (; j < d.w; ++j) sum += qv[32 * j] * gather<STAGE>(vec, s_stage, qi[32 * j]);
       }
       if (np == 1) {
         finish(sum, pre_one);
@@ -664,7 +660,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
         if constexpr (PROD) {
           sum += val[k];
         } else {
-          sum += val[k] * gather<STAGE>(vec, s_stage, idx[k], stage_len);
+          sum += val[k] * gather<STAGE>(vec, s_stage, idx[k]);
         }
       }
 #pragma unroll
