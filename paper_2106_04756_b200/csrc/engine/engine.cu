@@ -307,7 +307,12 @@ struct folp_gpu_ctx {
       cudaGetLastError();
       return;
     }
-    const int G = std::min(sms * per_sm, kFoldMaxCtas);
+    if (const char* env = std::getenv("FOLP_FOLD_SKIP_ZEROS")) {
+      const int v = std::atoi(env) != 0 ? 1 : 0;
+      CK(cudaMemcpyToSymbol(g_fold_skip_zeros, &v, sizeof v));
+    }
+    int G = std::min(sms * per_sm, kFoldMaxCtas);
+    if (const char* env = std::getenv("FOLP_FOLD_GRID")) G = std::max(1, std::min(G, std::atoi(env)));
     fold.cap = G;
     fold.cta_sum = alloc<double>(static_cast<size_t>(kFoldMaxJobs) * G);
     fold.cta_abs = alloc<double>(static_cast<size_t>(kFoldMaxJobs) * G);

@@ -86,6 +86,9 @@ struct FoldEntry {
 // folp_gpu_test_exact_fold): start, phase 1 done, grid sync done, phase 2
 // done (CTA 0); ticket, lists built, replay done (last CTA).
 __device__ unsigned long long g_fold_times[8];
+// zero terms at undecidable sums skipped as transparent steps (1, default)
+// or folded as events (0, FOLP_FOLD_SKIP_ZEROS=0: diagnostics)
+__device__ int g_fold_skip_zeros = 1;
 __device__ __forceinline__ unsigned long long fold_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -592,7 +595,7 @@ __global__ void __launch_bounds__(kFoldBlock) k_exact_fold(FoldJobs jobs, FoldSc
     for (int64_t i = a; i < e; ++i) {
       const double t = __ldcg(&jb.t[i]);
       const int E = fold_classify(P, t, D, N);
-      if (E == kFoldIrregular && t == 0.0 && (zpos || signbit(t))) continue;
+      if (E == kFoldIrregular && t == 0.0 && (zpos || signbit(t)) && g_fold_skip_zeros) continue;
       any = true;
       int bp = -1;  // -1 none, 1 event, 0 flush
       if (E == kFoldIrregular) {
@@ -799,7 +802,7 @@ __device__ __forceinline__ double warp_exact_dot(const double* __restrict__ val,
         const int E = fold_classify(P, v, D, N);
         // a zero product at an undecidable sum is transparent (S starts at
         // +0.0, so S + 0 == S always holds here)
-        if (E == kFoldIrregular && v == 0.0) continue;
+        if (E == kFoldIrregular && v == 0.0 && g_fold_skip_zeros) continue;
         if (first < 0) first = i;
         int bp = -1;
         if (E == kFoldIrregular) {
