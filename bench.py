@@ -16,7 +16,7 @@ session (include/folp_c.h folp_session_*).
                algorithmic bytes per trial slot 24*nnz + 68*(m+n)
                (SURVEY.md 8d) over their CUDA-event time, vs measured HBM peak;
                traffic = the DRAM bytes ncu measured for one trial
-               (profiles/r1_traffic.json, profiles/r1_step_kernels_ncu.txt)
+               (profiles/r2_traffic.json)
   cpu_baseline: the compiled reference (oracle/_ref) on 1 host core
 
 ``--impl reference`` times the reference CPU solver (oracle/_ref, compiled
@@ -60,13 +60,16 @@ def bytes_per_trial(m: int, n: int, nnz: int) -> int:
 
 
 def measured_traffic(config: int):
-    """DRAM bytes per trial (kernel A + kernel B) from the committed ncu --set
-    full capture (profiles/r1_traffic.json), or None for other configs."""
-    try:
-        d = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())
-        return d[f"config{config}"]["trial_dram_bytes"]
-    except Exception:
-        return None
+    """DRAM bytes per trial (kernel A + kernel B, window phases included) from
+    the committed ncu captures (profiles/r2_traffic.json: tools/
+    ncu_step_summary.py, tools/launch_traffic.py), or None."""
+    for name in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            d = json.loads((ROOT / "profiles" / name).read_text())
+            return d[f"config{config}"]["trial_dram_bytes"]
+        except Exception:
+            continue
+    return None
 
 
 def measured_peak() -> tuple[float, str]:
