@@ -225,12 +225,13 @@ struct folp_gpu_ctx {
   double* lcsc_val = nullptr;
   double* kty_part = nullptr;
   int peer_parity = 0;  // receive-area parity of the next peer exchange
-  // partitioned dual epilogue (column partition + peer exchange, DESIGN 7):
-  // own rows [pd_bounds[rank], pd_bounds[rank+1]) of equal chunks pd_chunk
+  // partitioned epilogue over the peer exchange (DESIGN 7): the column
+  // partition's dual step on own rows, the row partition's primal step on
+  // own columns -- [pd_bounds[rank], pd_bounds[rank+1]) of equal chunks
   bool pdual = false;
   int64_t pd_chunk = 0;
   std::vector<int64_t> pd_bounds;
-  double** pd_ydst = nullptr;  // device [2][W]: every rank's y[0], y[1]
+  double** pd_vdst = nullptr;  // device [2][W]: every rank's y[0], y[1] (cols) / x[0], x[1] (rows)
   bool hot_columns = false;  // created with a degree order (folp_gpu_create_ordered)
   double* shard_sums = nullptr;
   bool shard_values_ready = false;
@@ -1745,24 +1746,26 @@ int folp_gpu_shard_attach(folp_gpu_ctx* c, const folp_gpu_shard* spec, const int
       // each rank's own rows (FOLP_SHARD_EPILOGUE=replicated keeps it on
       // every rank for all m rows)
       const char* epi = std::getenv("FOLP_SHARD_EPILOGUE");
-      c->pdual = peer && c->col_part && spec->world > 1 &&
-                 !(epi != nullptr && std::strcmp(epi, "replicated") == 0);
-      if (peer) c->comm->peer_setup(c->col_part ? m + (c->pdual ? 8 : 2) : n);
+      c->pdual = peer && spec->world > 1 && !(epi != nullptr && std::strcmp(epi, "replicated") == 0);
+      // the epilogue's axis: rows (column partition) or columns (row partition)
+      const int64_t ax = c->col_part ? m : n;
+      if (peer) c->comm->peer_setup(c->col_part ? m + (c->pdual ? 8 : 2) : n + (c->pdual ? 8 : 0));
       if (c->pdual) {
         const int W = spec->world;
-        c->pd_chunk = (m + W - 1) / W;
+        c->pd_chunk = (ax + W - 1) / W;
         c->pd_bounds.assign(static_cast<size_t>(W) + 1, 0);
-        for (int r = 0; r <= W; ++r) c->pd_bounds[r] = std::min<int64_t>(m, r * c->pd_chunk);
+        for (int r = 0; r <= W; ++r) c->pd_bounds[r] = std::min<int64_t>(ax, r * c->pd_chunk);
         std::vector<double*> tab(2 * static_cast<size_t>(W));
         for (int par = 0; par < 2; ++par) {
-          const std::vector<double*> ptrs = c->comm->exchange_pointers(c->y[par]);
+          const std::vector<double*> ptrs = c->comm->exchange_pointers(c->col_part ? c->y[par] : c->x[par]);
           for (int r = 0; r < W; ++r) tab[par * W + r] = ptrs[r];
         }
-        c->pd_ydst = c->alloc<double*>(tab.size());
-        CK(cudaMemcpy(c->pd_ydst, tab.data(), tab.size() * sizeof(double*), cudaMemcpyHostToDevice));
+        c->pd_vdst = c->alloc<double*>(tab.size());
+        CK(cudaMemcpy(c->pd_vdst, tab.data(), tab.size() * sizeof(double*), cudaMemcpyHostToDevice));
         if (std::getenv("FOLP_TIMING") != nullptr) {
-          std::fprintf(stderr, "[folp timing] shard %d/%d: partitioned dual epilogue, rows [%lld, %lld)\n",
-                       spec->rank, W, static_cast<long long>(c->pd_bounds[spec->rank]),
+          std::fprintf(stderr, "[folp timing] shard %d/%d: partitioned %s epilogue, %s [%lld, %lld)\n",
+                       spec->rank, W, c->col_part ? "dual" : "primal", c->col_part ? "rows" : "columns",
+                       static_cast<long long>(c->pd_bounds[spec->rank]),
                        static_cast<long long>(c->pd_bounds[spec->rank + 1]));
         }
       }

@@ -284,11 +284,25 @@ struct EpiDual {
     acc.add(2, i, isfinite(v) ? 0.0 : 1.0);
   }
   double* shard_out = nullptr;  // row shard: local sums for the all-reduce
-  __device__ void finalize(const double (&tot)[K]) const {
+  // row shard, partitioned primal epilogue: the sums go to slot `rank` of
+  // every rank's area at [shard_at, shard_at + 3)
+  double* const* shard_peers = nullptr;
+  int shard_world = 0;
+  int64_t shard_at = 0;
+  __device__ bool shard_sums(const double (&tot)[K]) const {
+    if (shard_peers != nullptr) {
+      for (int r = 0; r < shard_world; ++r)
+        for (int k = 0; k < K; ++k) shard_peers[r][shard_at + k] = tot[k];
+      return true;
+    }
     if (shard_out != nullptr) {
       for (int k = 0; k < K; ++k) shard_out[k] = tot[k];
-      return;
+      return true;
     }
+    return false;
+  }
+  __device__ void finalize(const double (&tot)[K]) const {
+    if (shard_sums(tot)) return;
     const DevState* st = b.st;
     double movement = tot[1] / st->omega;  // solver.cpp:83
     movement = movement + st->sx;
@@ -309,10 +323,7 @@ struct EpiDual {
   }
   __device__ void finalize_state(const double (&tot)[K], unsigned long long* words,
                                  const double* rg) const {
-    if (shard_out != nullptr) {
-      for (int k = 0; k < K; ++k) shard_out[k] = tot[k];
-      return;
-    }
+    if (shard_sums(tot)) return;
     DevState* st = reinterpret_cast<DevState*>(words);
     double movement = tot[1] / st->omega;  // solver.cpp:83
     movement = movement + st->sx;
@@ -510,6 +521,45 @@ struct OpShardDualOwn {
   __device__ void finalize(const double (&tot)[K]) const {
     for (int r = 0; r < world; ++r) {
       for (int k = 0; k < K; ++k) sdst[r][m + 2 + k] = tot[k];
+    }
+  }
+  __device__ void finalize_ordered(const double*, int64_t) const {}
+};
+
+// The row partition's counterpart (DESIGN 7): rank p owns columns [r0, r1)
+// (equal chunks); the partial K'y of every column reached its owner only,
+// the owner sums the W slots in rank order, runs kernel A's epilogue on its
+// columns, stores x' into every rank's x' vector and its two sums (sx, bad)
+// into slot p of every rank's area at [n, n + 2).  EpiDual over the own
+// rows then adds its three sums at [n + 2, n + 5) (shard_peers) and
+// k_shard_decide_rows(..., n) folds all five in rank order.
+struct OpShardPrimalOwn {
+  static constexpr int K = 2;
+  static constexpr bool kReduce = true;
+  EpiPrimal e;
+  const double* const* src;   // this rank's W slots (current parity)
+  double* const* sdst;        // slot `rank` of every rank's area (current parity)
+  double* const* xdst2;       // [2][W] every rank's x[0], x[1]
+  double* const* xdst = nullptr;
+  int world = 0, rank = 0;
+  int64_t r0 = 0, n = 0;
+  __device__ bool prepare() {
+    if (!e.prepare()) return false;
+    xdst = xdst2 + (e.b.st->cur ^ 1) * world;
+    return true;
+  }
+  template <class Acc>
+  __device__ void apply(int64_t k, Acc& acc) const {
+    const int j = static_cast<int>(r0 + k);
+    e.apply(j, sum_slots(src, world, j), e.load(j), acc);
+    const double v = e.xn[j];
+    for (int r = 0; r < world; ++r) {
+      if (r != rank) xdst[r][j] = v;
+    }
+  }
+  __device__ void finalize(const double (&tot)[K]) const {
+    for (int r = 0; r < world; ++r) {
+      for (int k = 0; k < K; ++k) sdst[r][n + k] = tot[k];
     }
   }
   __device__ void finalize_ordered(const double*, int64_t) const {}

@@ -74,6 +74,7 @@ void ensure_gathered(folp_gpu_ctx* c) {
     c->comm->gather_rows(c->y[cur], c->shard_bounds, c->stream);
     c->comm->gather_rows(c->kx[cur], c->shard_bounds, c->stream);
     c->comm->gather_rows(c->avg_y, c->shard_bounds, c->stream);
+    if (c->pdual) c->comm->gather_rows(c->avg_x, c->pd_bounds, c->stream);  // own columns only
   }
   c->rows_dirty = false;
 }
@@ -105,7 +106,7 @@ void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
       c->seg(c->lrows, c->lcsc_val, sp, 1);
       comm.peer_fence(c->stream);
       if (c->pdual) {  // own rows only, y' and the partial sums to every rank
-        OpShardDualOwn od{EpiDual{b}, comm.peer_src(par), comm.peer_dst(par), c->pd_ydst};
+        OpShardDualOwn od{EpiDual{b}, comm.peer_src(par), comm.peer_dst(par), c->pd_vdst};
         od.world = comm.world;
         od.rank = comm.rank;
         od.r0 = c->pd_bounds[comm.rank];
@@ -127,8 +128,28 @@ void launch_shard_slot(folp_gpu_ctx* c, const LoopBufs& b) {
     EpiShardPart sp{b, c->kty_part, nullptr, false};
     sp.outs = comm.peer_dst(par);
     sp.world = comm.world;
+    if (c->pdual) sp.own_chunk = c->pd_chunk;
     c->seg(c->lcols, c->lcsc_val, sp, 1);
     comm.peer_fence(c->stream);
+    if (c->pdual) {  // primal step on own columns, x' and its sums to every rank
+      OpShardPrimalOwn op{EpiPrimal{b}, comm.peer_src(par), comm.peer_dst(par), c->pd_vdst};
+      op.world = comm.world;
+      op.rank = comm.rank;
+      op.r0 = c->pd_bounds[comm.rank];
+      op.n = c->n;
+      c->ew(c->pd_bounds[comm.rank + 1] - op.r0, op, 2);
+      comm.peer_fence(c->stream);
+      EpiDual ed{b};
+      ed.shard_peers = comm.peer_dst(par);  // its three sums to every rank's area
+      ed.shard_world = comm.world;
+      ed.shard_at = c->n + 2;
+      c->seg(c->lrows, c->csr_work, ed, 3);
+      comm.peer_fence(c->stream);
+      k_shard_decide_rows<<<1, 1, 0, c->stream>>>(b, comm.peer_src(par), comm.world, c->n);
+      ++c->launches;
+      CK(cudaGetLastError());
+      return;
+    }
     OpShardPrimal op{EpiPrimal{b}, nullptr};
     op.src = comm.peer_src(par);
     op.world = comm.world;

@@ -198,28 +198,32 @@ def test_nccl_world1_peer_exchange(eng, monkeypatch, partition):
     assert worst <= 1e-12
 
 
+@pytest.mark.parametrize("partition", ["cols", "rows"])
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_partitioned_dual_epilogue(ref, world, capfd, monkeypatch):
-    """Column partition over the peer exchange with the dual epilogue on each
-    rank's own rows (engine ops.cuh OpShardDualOwn): partial rows stored to
-    their owner only, owner sums in rank order, y' stored into every rank's
-    y', the three trial sums folded in rank order by every rank.  All shards
-    agree bit for bit; the first 100 iterates stay within the reference's
-    noise floor with its restarts; the solve reaches 1e-8 like the
-    reference (config 5 family: W = 8 leaves 12-13 rows per rank)."""
+def test_partitioned_epilogue(ref, world, partition, capfd, monkeypatch):
+    """The peer exchange with the epilogue on each rank's own range (engine
+    ops.cuh OpShardDualOwn for the column partition: dual step on own rows;
+    OpShardPrimalOwn for the row partition: primal step on own columns):
+    partial products stored to their owner only, the owner sums in rank
+    order, the new iterate stored into every rank's vector, the trial sums
+    folded in rank order by every rank.  All shards agree bit for bit; the
+    first 100 iterates stay within the reference's noise floor with its
+    restarts; the solve reaches 1e-8 like the reference (config 5 family:
+    W = 8 leaves 12-13 rows per rank)."""
     from _parity import assert_within_floor, reference_floor
     monkeypatch.setenv("FOLP_TIMING", "1")
     lp = instances.generate(5, 1, 0.01)
     p = cabi.params(record_iterate_trace=True, iteration_limit=100)
-    res = shard.solve_loopback(lp, world, p, partition="cols", iterate_capacity=100)
-    assert "partitioned dual epilogue" in capfd.readouterr().err
+    res = shard.solve_loopback(lp, world, p, partition=partition, iterate_capacity=100)
+    want = "partitioned dual epilogue" if partition == "cols" else "partitioned primal epilogue"
+    assert want in capfd.readouterr().err
     _same(res)
     b = ref.solve_lp(lp, p, iterate_capacity=100)
     assert_within_floor(res[0].iterate_trace, b.iterate_trace, reference_floor(lp, p, 100, b), world)
     assert res[0].restart_iterations == b.restart_iterations
     monkeypatch.delenv("FOLP_TIMING")
     p = cabi.params(kkt_pass_limit=300000)
-    res = shard.solve_loopback(lp, world, p, partition="cols")
+    res = shard.solve_loopback(lp, world, p, partition=partition)
     _same(res)
     a, b = res[0], ref.solve_lp(lp, p)
     assert a.termination_reason == b.termination_reason == "Optimal"
