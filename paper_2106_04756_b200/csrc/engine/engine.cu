@@ -40,6 +40,7 @@
 #include <memory>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -769,6 +770,28 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
       block_free(stage);
     }
     mark("indices");
+    // the rows plan (and the SELL groups) on a second host thread while this
+    // one uploads the values, transposes on the device and plans the columns
+    std::exception_ptr rows_err;
+    SellHost sh;
+    std::thread rows_worker([&] {
+      try {
+        CK(cudaSetDevice(c->device));
+        build_plan(c.get(), p->row_start, m, nnz, c->csr_ptr, c->csr_col, c->rows);
+        if (!c->ordered && col_order == nullptr && nnz > 0 && p->row_cols != nullptr) {
+          sh = detect_sell(p->row_start, p->row_cols, m, nnz);
+          if (!sh.row0.empty()) build_sell_plan(c.get(), p->row_start, m, nnz, sh, c->rows_sell);
+        }
+      } catch (...) {
+        rows_err = std::current_exception();
+      }
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{rows_worker};
     try {
       if (nnz < (int64_t(1) << 20) || p->row_values == nullptr) {
         upload(c.get(), c->csr_orig, p->row_values, nnz);
@@ -790,20 +813,17 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
     release_pinned();
 
     mark("values");
-    build_plan(c.get(), p->row_start, m, nnz, c->csr_ptr, c->csr_col, c->rows);
     build_plan(c.get(), col_start, n, nnz, c->csc_ptr, c->csc_row, c->cols);
+    rows_worker.join();
+    if (rows_err) std::rethrow_exception(rows_err);
     c->rows.sp.vec_len = static_cast<int>(std::min<int64_t>(n, INT32_MAX));
     c->cols.sp.vec_len = static_cast<int>(std::min<int64_t>(m, INT32_MAX));
-    if (!c->ordered && col_order == nullptr && nnz > 0 && p->row_cols != nullptr) {
-      const SellHost sh = detect_sell(p->row_start, p->row_cols, m, nnz);
-      if (!sh.row0.empty()) {
-        build_sell_plan(c.get(), p->row_start, m, nnz, sh, c->rows_sell);
-        c->sell = true;
-        c->sell_coalesced = sh.gathers_coalesced;
-        if (timing) {
-          std::fprintf(stderr, "[folp timing] SELL-32: %zu row groups, %lld entries, coalesced %d\n",
-                       sh.row0.size(), static_cast<long long>(sh.nnz), sh.gathers_coalesced ? 1 : 0);
-        }
+    if (!sh.row0.empty()) {
+      c->sell = true;
+      c->sell_coalesced = sh.gathers_coalesced;
+      if (timing) {
+        std::fprintf(stderr, "[folp timing] SELL-32: %zu row groups, %lld entries, coalesced %d\n",
+                     sh.row0.size(), static_cast<long long>(sh.nnz), sh.gathers_coalesced ? 1 : 0);
       }
     }
 

@@ -50,6 +50,10 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   }
   std::vector<int4> units;
   std::vector<int> multi_seg, multi_parts, multi_first;
+  // segments above giant_min entries are cut in kGiantPart-entry parts
+  // (fewer part sums, fences and arrival atomics); FOLP_GIANT_MIN overrides
+  const char* genv = std::getenv("FOLP_GIANT_MIN");
+  const int64_t giant_min = genv != nullptr ? std::max<int64_t>(kWarpTile, std::atoll(genv)) : kGiantMin;
   // One pass over the segments with tiles of at most `target` nonzeros.
   auto build = [&](int64_t target) {
     units.clear();
@@ -91,7 +95,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
       }
       // parts: d.y = the part's own slot (its index in this original order)
       const int multi = static_cast<int>(multi_seg.size());
-      const int64_t part = len > kGiantMin ? kGiantPart : kWarpTile;
+      const int64_t part = len > giant_min ? kGiantPart : kWarpTile;
       multi_first.push_back(static_cast<int>(units.size()));
       for (int64_t b = ptr[s]; b < ptr[s + 1]; b += part) {
         units.push_back(make_int4(-(multi + 1), static_cast<int>(units.size()), static_cast<int>(b),
@@ -270,7 +274,11 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   p.arrivals = dalloc<unsigned>(multi_seg.size());
   out.owned.push_back(p.arrivals);
   CK(cudaMemset(p.arrivals, 0, std::max<size_t>(1, multi_seg.size()) * sizeof(unsigned)));
-  c->max_giant = std::max(c->max_giant, p.n_multi);
+  {
+    static std::mutex mu;  // plans of one context may be built on two host threads
+    std::lock_guard<std::mutex> lk(mu);
+    c->max_giant = std::max(c->max_giant, p.n_multi);
+  }
 }
 
 void upload_index(folp_gpu_ctx* c, const int64_t* src, int* dst, int64_t count, int64_t* stage,

@@ -93,14 +93,16 @@ void build_sell_plan(folp_gpu_ctx* c, const int64_t* rs, int64_t m, int64_t nnz,
   std::vector<int4> extra;
   int64_t b = 0;
   int slots = 0;
+  const char* penv = std::getenv("FOLP_SELL_PART");  // entries per lane per unit
+  const int part = penv != nullptr ? std::max(8, std::atoi(penv)) : kSellPart;
   for (int g = 0; g < G; ++g) {
     for (int l = 0; l < 32; ++l) skip[static_cast<size_t>(h.row0[g] + l)] = 1;
     base[g] = static_cast<int>(b);
     const int L = h.len[g];
-    nparts[g] = (L + kSellPart - 1) / kSellPart;
+    nparts[g] = (L + part - 1) / part;
     slot0[g] = slots;
     for (int q = 0; q < nparts[g]; ++q) {
-      extra.push_back(make_int4(-(kSellTag + g), q, q * kSellPart, std::min(L, (q + 1) * kSellPart)));
+      extra.push_back(make_int4(-(kSellTag + g), q, q * part, std::min(L, (q + 1) * part)));
     }
     slots += nparts[g];
     b += 32 * static_cast<int64_t>(L);
@@ -129,7 +131,11 @@ void build_sell_plan(folp_gpu_ctx* c, const int64_t* rs, int64_t m, int64_t nnz,
   q.idx = idx;
   q.val = val;
   q.n_groups = G;
-  c->max_giant = std::max(c->max_giant, out.sp.n_multi + G);
+  {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    c->max_giant = std::max(c->max_giant, out.sp.n_multi + G);
+  }
 }
 
 // interleave: entry j of row row0[g] + lane -> base[g] + 32 j + lane
