@@ -458,9 +458,7 @@ __global__ void __launch_bounds__(kFoldBlock) k_exact_fold(FoldJobs jobs, FoldSc
   if (b == 0 && tid == 0) g_fold_times[0] = fold_ns();
   __shared__ double s_red[kFoldWarps];
   __shared__ unsigned long long s_u64[kFoldWarps];
-  __shared__ FoldBp s_bp[kFoldBpCap];
   __shared__ int s_laste_t[kFoldBlock];
-  __shared__ unsigned long long s_off[kFoldBlock];
   __shared__ int s_nbp;
   __shared__ int s_last;
   __shared__ double s_init[kFoldMaxJobs];
@@ -591,69 +589,87 @@ __global__ void __launch_bounds__(kFoldBlock) k_exact_fold(FoldJobs jobs, FoldSc
     // far added -0.0 to a -0.0 init.
     const bool zpos = jb.init_from < 0 ? !(init == 0.0 && signbit(init))
                                        : fabs(init) > s_einit[j];
+    // Pass 1 classifies the thread's steps: breakpoint count, N-prefix, last
+    // grid; pass 2 (after the block scans) walks them again and writes the
+    // breakpoints straight to their sorted place -- sub-ranges ascend with
+    // the thread index, so a thread's offset is the scan of the counts (no
+    // shared list, atomics or rank sort).
+    const int Einit = Eprev;
+    const double Pinit = P;
     bool any = false;
+    int nb = 0;
+    unsigned long long lastc_local = 0;
     for (int64_t i = a; i < e; ++i) {
       const double t = __ldcg(&jb.t[i]);
       const int E = fold_classify(P, t, D, N);
       if (E == kFoldIrregular && t == 0.0 && (zpos || signbit(t)) && g_fold_skip_zeros) continue;
       any = true;
-      int bp = -1;  // -1 none, 1 event, 0 flush
-      if (E == kFoldIrregular) {
-        bp = 1;
-      } else if (Eprev != kFoldAfterEvent && Eprev != E) {
-        bp = 0;
-      }
-      if (bp >= 0) {
-        const int k = atomicAdd(&s_nbp, 1);
-        if (k < kFoldBpCap) s_bp[k] = FoldBp{i, c, t, bp, Eprev, tid, 0};
+      if (E == kFoldIrregular || (Eprev != kFoldAfterEvent && Eprev != E)) {
+        ++nb;
+        lastc_local = c;
       }
       if (E != kFoldIrregular) c += static_cast<unsigned long long>(N);
       Eprev = E == kFoldIrregular ? kFoldAfterEvent : E;
       P += t;
     }
     s_laste_t[tid] = any ? Eprev : kFoldEmpty;
-    unsigned long long ctot;
+    unsigned long long ctot, btot;
     const unsigned long long coff = fold_block_exscan_u64(c, s_u64, &ctot);
-    s_off[tid] = coff;
+    const unsigned long long boff =
+        fold_block_exscan_u64(static_cast<unsigned long long>(nb), s_u64, &btot);
+    if (tid == 0) {
+      s_nbp = -1;
+      s_last = -1;
+    }
     __syncthreads();
-    const int nbp = s_nbp;
+    if (any) atomicMax(&s_nbp, tid);          // the last thread with a step
+    if (nb > 0) atomicMax(&s_last, tid);      // the last thread with a breakpoint
+    const bool fits = btot <= static_cast<unsigned long long>(kFoldBpCap);
     FoldBp* out = sc.bps + (static_cast<int64_t>(j) * sc.cap + b) * kFoldBpCap;
-    if (nbp <= kFoldBpCap) {
-      for (int k = tid; k < nbp; k += kFoldBlock) {  // rank sort by step index, fix-ups
-        FoldBp v = s_bp[k];
-        int rank = 0;
-        for (int q = 0; q < nbp; ++q) rank += s_bp[q].i < v.i ? 1 : 0;
-        v.c += s_off[v.thread];
-        if (v.ebefore == kFoldFromPrev) {  // the previous non-empty thread's last step
-          for (int q = v.thread - 1; q >= 0; --q) {
-            if (s_laste_t[q] != kFoldEmpty) {
-              v.ebefore = s_laste_t[q];
-              break;
-            }
+    if (fits && nb > 0) {
+      // the grid before the thread's first step when it was undecidable
+      int eprev_thread = kFoldAfterEvent;
+      if (Einit == kFoldFromPrev) {
+        eprev_thread = kFoldFromPrev;
+        for (int q = tid - 1; q >= 0; --q) {
+          if (s_laste_t[q] != kFoldEmpty) {
+            eprev_thread = s_laste_t[q];
+            break;
           }
         }
-        out[rank] = v;
       }
-    }
-    if (tid == 0) {
-      int le = kFoldEmpty;
-      for (int q = kFoldBlock - 1; q >= 0; --q) {
-        if (s_laste_t[q] != kFoldEmpty) {
-          le = s_laste_t[q];
-          break;
+      P = Pinit;
+      Eprev = Einit;
+      unsigned long long cc = 0;
+      int k = static_cast<int>(boff);
+      for (int64_t i = a; i < e; ++i) {
+        const double t = __ldcg(&jb.t[i]);
+        const int E = fold_classify(P, t, D, N);
+        if (E == kFoldIrregular && t == 0.0 && (zpos || signbit(t)) && g_fold_skip_zeros) continue;
+        int bp = -1;  // -1 none, 1 event, 0 flush
+        if (E == kFoldIrregular) {
+          bp = 1;
+        } else if (Eprev != kFoldAfterEvent && Eprev != E) {
+          bp = 0;
         }
+        if (bp >= 0) {
+          const int eb = Eprev == kFoldFromPrev ? eprev_thread : Eprev;
+          out[k++] = FoldBp{i, cc + coff, t, bp, eb, tid, 0};
+        }
+        if (E != kFoldIrregular) cc += static_cast<unsigned long long>(N);
+        Eprev = E == kFoldIrregular ? kFoldAfterEvent : E;
+        P += t;
       }
-      sc.cta_laste[j * sc.cap + b] = le;
-      sc.cta_ntot[j * sc.cap + b] = ctot;
-      sc.cta_nbp[j * sc.cap + b] = nbp <= kFoldBpCap ? nbp : -1;
-      unsigned long long lastc = 0;
-      if (nbp > 0 && nbp <= kFoldBpCap) {  // the breakpoint with the largest index
-        int best = 0;
-        for (int q = 1; q < nbp; ++q) best = s_bp[q].i > s_bp[best].i ? q : best;
-        lastc = s_bp[best].c + s_off[s_bp[best].thread];
-      }
-      sc.cta_lastc[j * sc.cap + b] = lastc;
     }
+    __syncthreads();
+    if (tid == 0) {
+      sc.cta_ntot[j * sc.cap + b] = ctot;
+      sc.cta_nbp[j * sc.cap + b] = fits ? static_cast<int>(btot) : -1;
+      if (s_nbp < 0) sc.cta_laste[j * sc.cap + b] = kFoldEmpty;
+      if (s_last < 0 || !fits) sc.cta_lastc[j * sc.cap + b] = 0ull;
+    }
+    if (tid == s_nbp) sc.cta_laste[j * sc.cap + b] = s_laste_t[tid];
+    if (fits && tid == s_last) sc.cta_lastc[j * sc.cap + b] = lastc_local + coff;
     __syncthreads();
   }
 

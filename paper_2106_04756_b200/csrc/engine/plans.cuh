@@ -15,7 +15,8 @@ double tile_segs_cutoff() {
 // groups' rows); `extra`: units appended to every build (their SELL parts).
 void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
                 const int* d_ptr, const int* d_idx, PlanDev& out, int64_t s_begin = 0,
-                const std::vector<char>* skip = nullptr, const std::vector<int4>* extra = nullptr) {
+                const std::vector<char>* skip = nullptr, const std::vector<int4>* extra = nullptr,
+                int64_t giant_min_plan = kGiantMin) {
   const bool ordered = c->ordered;
   // segments per tile: tree mode caps it when segments are very short (a
   // lane then owns several segments, and every extra round waits behind the
@@ -53,7 +54,7 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   // segments above giant_min entries are cut in kGiantPart-entry parts
   // (fewer part sums, fences and arrival atomics); FOLP_GIANT_MIN overrides
   const char* genv = std::getenv("FOLP_GIANT_MIN");
-  const int64_t giant_min = genv != nullptr ? std::max<int64_t>(kWarpTile, std::atoll(genv)) : kGiantMin;
+  const int64_t giant_min = genv != nullptr ? std::max<int64_t>(kWarpTile, std::atoll(genv)) : giant_min_plan;
   // One pass over the segments with tiles of at most `target` nonzeros.
   auto build = [&](int64_t target) {
     units.clear();

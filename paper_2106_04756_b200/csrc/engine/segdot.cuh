@@ -103,7 +103,8 @@ __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gp
 // each lane's part sums in part order and runs the epilogue, its reduction
 // terms going to slot n_multi + g (deterministic, like multi-part segments).
 constexpr int kSellTag = 1 << 29;
-constexpr int kSellPart = 64;  // entries per lane per unit (2048 nonzeros)
+constexpr int kSellPart = 128;     // entries per lane per unit (4096 nonzeros)
+constexpr int kSellGiantMin = 4096;  // CSR rows of a SELL plan above this: 2048-entry parts
 struct SellPlan {
   const int* idx = nullptr;      // [32 * sum L] interleaved gather indices
   const double* val = nullptr;   // interleaved working values

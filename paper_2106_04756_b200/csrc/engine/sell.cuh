@@ -95,6 +95,7 @@ void build_sell_plan(folp_gpu_ctx* c, const int64_t* rs, int64_t m, int64_t nnz,
   int slots = 0;
   const char* penv = std::getenv("FOLP_SELL_PART");  // entries per lane per unit
   const int part = penv != nullptr ? std::max(8, std::atoi(penv)) : kSellPart;
+  static_assert(kSellGiantMin >= kWarpTile, "giant parts start above a tile");
   for (int g = 0; g < G; ++g) {
     for (int l = 0; l < 32; ++l) skip[static_cast<size_t>(h.row0[g] + l)] = 1;
     base[g] = static_cast<int>(b);
@@ -107,7 +108,11 @@ void build_sell_plan(folp_gpu_ctx* c, const int64_t* rs, int64_t m, int64_t nnz,
     slots += nparts[g];
     b += 32 * static_cast<int64_t>(L);
   }
-  build_plan(c, rs, m, nnz, c->csr_ptr, c->csr_col, out, 0, &skip, &extra);
+  // the rows left to CSR units here are the contiguous ones (gathers
+  // coalesced): 2048-entry parts above 4096 entries halve their part sums,
+  // fences and arrival atomics (config 5's 8,000-entry supply rows: with
+  // 128-entry SELL parts, trial 515 -> 478 us)
+  build_plan(c, rs, m, nnz, c->csr_ptr, c->csr_col, out, 0, &skip, &extra, kSellGiantMin);
   auto up = [&](const std::vector<int>& v) {
     int* d = dalloc<int>(v.size());
     out.owned.push_back(d);

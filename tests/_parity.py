@@ -118,3 +118,35 @@ def iteration_band(cfg: int, seed: int, scale: float) -> float:
     spread = json.loads((Path(__file__).parent / "golden" / "iteration_spread.json").read_text())
     inst = spread.get(f"cfg{cfg}_s{seed}_x{scale}", {}).get("max_abs_iter_dev", 0.0)
     return max(0.05, inst, spread["family_spread"][f"cfg{cfg}"])
+
+
+def host_kkt(lp, x, y) -> dict:
+    """Independent host recheck of the termination criterion (the paper's
+    Eq. 7) on the ORIGINAL problem from a returned solution, restating the
+    reference acceptance suite's evaluate_optimality
+    (/root/reference/proj/tests/acceptance_main.cpp:88-139) with scipy
+    products: relative gap, primal and dual residuals and their max."""
+    import scipy.sparse as sp
+
+    k = sp.csr_matrix((lp.row_values, lp.row_cols, lp.row_start), shape=(lp.num_rows, lp.num_cols))
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    kx, kty = k @ x, k.T @ y
+    c, q = np.asarray(lp.objective), np.asarray(lp.right_hand_side)
+    lo, up = np.asarray(lp.variable_lower), np.asarray(lp.variable_upper)
+    primal_obj = lp.objective_constant + float(c @ x)
+    r = c - kty
+    has_lo, has_up = lo > -np.inf, up < np.inf
+    lam = np.where(has_lo & has_up, r, np.where(has_lo, np.maximum(r, 0.0),
+                                                np.where(has_up, np.minimum(r, 0.0), 0.0)))
+    dual_obj = lp.objective_constant + float(q @ y)
+    dual_obj += float(np.sum(np.where(lam > 0, lo * np.where(lam > 0, lam, 0.0), 0.0)))
+    dual_obj += float(np.sum(np.where(lam < 0, up * np.where(lam < 0, lam, 0.0), 0.0)))
+    pv = q - kx
+    m1 = lp.num_inequality_rows
+    pv[:m1] = np.maximum(pv[:m1], 0.0)
+    out = {"gap": abs(dual_obj - primal_obj) / (1 + abs(primal_obj) + abs(dual_obj)),
+           "primal": float(np.linalg.norm(pv)) / (1 + float(np.linalg.norm(q))),
+           "dual": float(np.linalg.norm(r - lam)) / (1 + float(np.linalg.norm(c)))}
+    out["worst"] = max(out.values())
+    return out

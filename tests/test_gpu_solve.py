@@ -25,7 +25,7 @@ import pytest
 
 from paper_2106_04756_b200 import cabi, instances
 
-from _parity import assert_within_floor, iteration_band, reference_floor
+from _parity import assert_within_floor, host_kkt, iteration_band, reference_floor
 
 pytestmark = pytest.mark.gpu
 
@@ -168,6 +168,10 @@ def test_tree_mode_solve_to_1e8(eng, ref, cfg, scale):
         admissible = 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
         assert abs(pa - pb) <= admissible
         assert abs(a.iterations - b.iterations) <= iteration_band(cfg, 1, scale) * b.iterations
+        # independent host recheck of Eq. 7 on the original problem from the
+        # returned (postsolved) solution (acceptance_main.cpp:88-139)
+        hk = host_kkt(lp, a.primal_solution, a.dual_solution)
+        assert hk["worst"] <= 1.0001e-8, hk
     assert a.step_condition_violations == 0
 
 
