@@ -545,8 +545,16 @@ struct folp_gpu_ctx {
     b.grow = grow_d;
     b.cond = h;
     b.use_cond = use_cond;
+    b.l_const = l_const;
+    b.u_const = u_const;
+    b.l_uni = l_uni;
+    b.u_uni = u_uni;
     return b;
   }
+  // uniform working bounds (LoopBufs l_uni / u_uni), checked once after rescaling
+  bool bounds_checked = false;
+  double l_const = 0.0, u_const = 0.0;
+  int l_uni = 0, u_uni = 0;
 
   ~folp_gpu_ctx() {
     if (ndg_count > 0 && std::getenv("FOLP_TIMING") != nullptr) {
@@ -1244,6 +1252,7 @@ int folp_gpu_run_chunk(folp_gpu_ctx* c, folp_gpu_loop* loop) {
     }
     if (policy != FOLP_STEP_MALITSKY_POCK && !c->kx_valid) refresh_kx(c);
     ensure_blocked(c);  // after rescaling: the working values are final
+    if (!c->bounds_checked) check_uniform_bounds(c);
     if (c->sell && !c->sell_packed) {
       pack_sell(c, c->rows_sell);
       c->sell_packed = true;

@@ -170,3 +170,39 @@ void pack_sell(folp_gpu_ctx* c, PlanDev& p) {
   ++c->launches;
   CK(cudaGetLastError());
 }
+
+// ---------------------------------------------------------------------
+// Uniform working bounds (ops.cuh LoopBufs l_uni / u_uni): one pass per
+// vector comparing bit patterns with the first entry; FOLP_UNIFORM_BOUNDS=0
+// keeps the arrays.
+__global__ void k_uniform_check(const double* __restrict__ v, int64_t n, int* differs) {
+  const long long v0 = __double_as_longlong(v[0]);
+  int d = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    d |= __double_as_longlong(v[i]) != v0;
+  }
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(differs, 1);
+}
+
+void check_uniform_bounds(folp_gpu_ctx* c) {
+  c->bounds_checked = true;
+  const char* env = std::getenv("FOLP_UNIFORM_BOUNDS");
+  if ((env != nullptr && std::atoi(env) == 0) || c->n == 0) return;
+  int* flags = dalloc<int>(2);
+  CK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+  k_uniform_check<<<c->simple_grid(c->n), kBlock, 0, c->stream>>>(c->lw, c->n, flags);
+  k_uniform_check<<<c->simple_grid(c->n), kBlock, 0, c->stream>>>(c->uw, c->n, flags + 1);
+  c->launches += 2;
+  int h[2] = {1, 1};
+  double v[2] = {0.0, 0.0};
+  CK(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&v[0], c->lw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&v[1], c->uw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  block_free(flags);
+  c->l_uni = h[0] == 0 ? 1 : 0;
+  c->u_uni = h[1] == 0 ? 1 : 0;
+  c->l_const = v[0];
+  c->u_const = v[1];
+}
