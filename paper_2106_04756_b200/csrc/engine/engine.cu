@@ -866,7 +866,7 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
     c->partial_cap = kMaxGrid + c->max_giant + 8;
     if (c->ordered) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);
-      c->terms[1] = c->alloc<double>(static_cast<size_t>(kNuCands) * (n + m) + 8);  // 7 bisection norms
+      c->terms[1] = c->alloc<double>(5 * (n + m) + 8);
       // exact parallel folds of the trial sums (exactfold.cuh); FOLP_EXACT_FOLD=0
       // keeps the one-thread sequential folds
       const char* env = std::getenv("FOLP_EXACT_FOLD");

@@ -502,8 +502,8 @@ void enqueue_ndg_init(folp_gpu_ctx* c, int s, int dist_base, double radius, doub
   CK(cudaGetLastError());
 }
 
-// One bisection pass (3 levels; ordered mode: 3 exact levels, then one
-// pass for g'd at the stopping node); a no-op once that scratch set is done.
+// One bisection pass (3 levels in tree mode, 1 in ordered mode); a no-op
+// once the bisection of that scratch set is done.
 void enqueue_ndg_pass(folp_gpu_ctx* c, int s, double omega) {
   OpNdgPass pass{};
   pass.n = c->n;
@@ -517,11 +517,10 @@ void enqueue_ndg_pass(folp_gpu_ctx* c, int s, double omega) {
   c->ew(c->n + c->m, pass, 15);
 }
 
-// Passes before the first look: 42 tree levels / 48 ordered levels (+ the
-// ordered g'd pass) cover a typical evaluation (the bracket starts at
-// ||g|| / r, the stop is 1e-10 r).
-int ndg_first_batch(const folp_gpu_ctx* c) { return c->ordered ? 17 : 14; }
-int ndg_next_batch(const folp_gpu_ctx* c) { return c->ordered ? 6 : 5; }
+// Passes before the first look: 42 tree levels / 48 ordered levels cover
+// a typical evaluation (the bracket starts at ||g|| / r, the stop is 1e-10 r).
+int ndg_first_batch(const folp_gpu_ctx* c) { return c->ordered ? 48 : 14; }
+int ndg_next_batch(const folp_gpu_ctx* c) { return c->ordered ? 16 : 5; }
 
 // Starts the bisections of the wanted scratch sets and queues the readback
 // of their states: tree mode runs them to the end in one cooperative
@@ -537,12 +536,12 @@ void fetch_ndg(folp_gpu_ctx* c) {
 void finish_ndg(folp_gpu_ctx* c, const bool (&want)[2], const double (&omega)[2]) {
   for (int round = 0; round < 256; ++round) {
     bool pending = false;
-    for (int s = 0; s < 2; ++s) pending = pending || (want[s] && c->ndg_h[s].done != 1);
+    for (int s = 0; s < 2; ++s) pending = pending || (want[s] && !c->ndg_h[s].done);
     if (!pending) return;
     const int batch = ndg_next_batch(c);
     for (int i = 0; i < batch; ++i) {
       for (int s = 0; s < 2; ++s) {
-        if (want[s] && c->ndg_h[s].done != 1) enqueue_ndg_pass(c, s, omega[s]);
+        if (want[s] && !c->ndg_h[s].done) enqueue_ndg_pass(c, s, omega[s]);
       }
     }
     fetch_ndg(c);

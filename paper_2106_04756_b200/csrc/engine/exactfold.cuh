@@ -56,7 +56,7 @@ constexpr int kFoldBlock = 256;
 constexpr int kFoldWarps = kFoldBlock / 32;
 constexpr int kFoldMaxJobs = 8;
 constexpr int kFoldMaxFlags = 4;
-constexpr int kFoldBpCap = 128;  // breakpoints per CTA range and job
+constexpr int kFoldBpCap = 512;  // breakpoints per CTA range and job (beyond: folded step by step)
 constexpr int kFoldIrregular = -100000;
 constexpr int kFoldAfterEvent = -100001;
 

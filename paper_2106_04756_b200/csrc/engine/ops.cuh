@@ -1454,13 +1454,9 @@ struct OpNdgPass {
   NdgState* ns;
 
   // the weights come from the bisection state (set by k_ndg_init), so a
-  // captured evaluation graph never bakes a stale omega into the pass.
-  // done: 0 bisecting, 1 finished, 2 (ordered mode) stopped at nu[0] -- one
-  // more pass folds g'd there.
-  int mode = 0;
+  // captured evaluation graph never bakes a stale omega into the pass
   __device__ bool prepare() {
-    mode = ns->done;
-    if (mode == 1) return false;
+    if (ns->done != 0) return false;
     omega = ns->omega;
     winv = ns->winv;
     return true;
@@ -1474,24 +1470,11 @@ struct OpNdgPass {
     const double his = primal ? hi[s] : INFINITY;
     const double* nu = ns->nu;
     if constexpr (Acc::kOrdered) {
-      // exactly the reference's quotient g / (nu * w) (solver.cpp:349), for
-      // the 7 midpoints of the next 3 levels: ||d(nu_p)||_w^2 terms folded
-      // exactly by one 7-job k_exact_fold (3 reference iterations per
-      // pass); g'd only at the node the bisection stops at (mode 2)
-      if (mode == 2) {
-        const double unclamped = gs / (__ldg(&nu[0]) * w);
-        const double d = ref_min(ref_max(unclamped, los), his);
-        acc.add(0, s, gs * d);
-#pragma unroll
-        for (int p = 1; p < kNuCands; ++p) acc.add(p, s, 0.0);
-      } else {
-#pragma unroll
-        for (int p = 0; p < kNuCands; ++p) {
-          const double unclamped = gs / (__ldg(&nu[p]) * w);
-          const double d = ref_min(ref_max(unclamped, los), his);
-          acc.add(p, s, w * d * d);
-        }
-      }
+      // exactly the reference's quotient g / (nu * w) (solver.cpp:349)
+      const double unclamped = gs / (__ldg(&nu[0]) * w);
+      const double d = ref_min(ref_max(unclamped, los), his);
+      acc.add(0, s, w * d * d);
+      acc.add(1, s, gs * d);
     } else {
       // tree mode: g * RN(1 / (nu * w)) -- within 1.5 ulp of the quotient,
       // far below the tree-order noise; no per-element division
@@ -1514,63 +1497,16 @@ struct OpNdgPass {
     ndg_replay(ns, nsq, gd, kNuLevels);
   }
   __device__ void finalize_ordered(const double* t, int64_t tot_n) const {
-    if (ns->done == 2) {
-      finish_gd(fold(0.0, t, tot_n));
-      return;
-    }
-    double nsq[kNuCands];
-    for (int p = 0; p < kNuCands; ++p) nsq[p] = fold(0.0, t + p * tot_n, tot_n);
-    ndg_replay_ordered(ns, nsq);
+    const double norm_sq = fold(0.0, t, tot_n);
+    const double gd = fold(0.0, t + tot_n, tot_n);
+    ndg_replay(ns, &norm_sq, &gd, 1);
   }
   __host__ void fold_plan(const double* t, int64_t tot_n, FoldJobs& f) const {
-    f.count = kNuCands;
-    for (int p = 0; p < kNuCands; ++p) f.job[p] = FoldJob{t + p * tot_n, tot_n, 0.0, -1, 1.0, nullptr, nullptr};
+    f.count = 2;
+    f.job[0] = FoldJob{t, tot_n, 0.0, -1, 1.0, nullptr, nullptr};
+    f.job[1] = FoldJob{t + tot_n, tot_n, 0.0, -1, 1.0, nullptr, nullptr};
   }
-  __device__ void finalize_exact(const double* r, unsigned) const {
-    if (ns->done == 2) {
-      finish_gd(r[0]);
-      return;
-    }
-    ndg_replay_ordered(ns, r);
-  }
-  __device__ void finish_gd(double gd) const {  // return linalg::dot(g, d) / radius (solver.cpp:369)
-    ns->result = gd / ns->radius;
-    ns->done = 1;
-  }
-  // ndg_replay over the 7 exact norms of a 3-level pass; where the
-  // reference returns (converged, or 200 iterations) the node's nu moves to
-  // nu[0] and done = 2: the next pass folds g'd there.
-  __device__ static void ndg_replay_ordered(NdgState* st, const double* norm_sq) {
-    const double r = st->radius;
-    const double r2 = r * r;
-    double lo_ = st->nu_lo, hi_ = st->nu_hi;
-    int node = 0;
-    st->passes += 1;
-    for (int level = 0; level < kNuLevels; ++level) {
-      const int evaluated = node;
-      st->it += 1;
-      if (fabs(sqrt(norm_sq[evaluated]) - r) <= 1e-10 * r) {
-        st->nu[0] = st->nu[evaluated];
-        st->done = 2;
-        return;
-      }
-      if (norm_sq[evaluated] > r2) {
-        lo_ = st->nu[evaluated];
-        node = 2 * node + 2;
-      } else {
-        hi_ = st->nu[evaluated];
-        node = 2 * node + 1;
-      }
-      if (st->it >= 200) {
-        st->nu[0] = st->nu[evaluated];
-        st->done = 2;
-        return;
-      }
-    }
-    st->nu_lo = lo_;
-    st->nu_hi = hi_;
-    ndg_candidates(lo_, hi_, st->nu);
-  }
+  __device__ void finalize_exact(const double* r, unsigned) const { ndg_replay(ns, &r[0], &r[1], 1); }
 };
 
 // ---------------------------------------------------------------------
