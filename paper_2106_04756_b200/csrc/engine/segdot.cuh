@@ -68,14 +68,22 @@ namespace folpgpu {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
+#ifdef FOLP_TILE128  // A/B builds (make variant): smaller tiles, fewer registers
+constexpr int kWarpTile = 128;
+#else
 constexpr int kWarpTile = 256;        // nonzeros per tile / part (8 per lane)
+#endif
 constexpr int kGiantMin = 65536;      // segments above this use kGiantPart parts
 constexpr int kGiantPart = 2048;      // nnz per part of a giant segment
 constexpr int kMaxAcc = 30;           // widest reduction (bisection pass)
 constexpr int kSerialCap = 128;       // tree mode, large axes: longest segment one lane sums
                                       // (with degree-ordered columns: config 2 -1.6 %, config 3 -1.4 % per trial)
 constexpr int kSingleMax = 1024;      // tree mode, large axes: longest one-warp segment
+#ifdef FOLP_MINB
+constexpr int kPlanCtasPerSm = FOLP_MINB;
+#else
 constexpr int kPlanCtasPerSm = 4;     // the loop products' residency (64 registers)
+#endif
 constexpr double kBalanceMin = 1.04;  // round-robin CTA load imbalance worth reordering
 constexpr int kSegdotCarveout = 36;   // % of the unified L1 as shared memory (engine.cu)
 
@@ -460,7 +468,11 @@ template <class Epi, bool ORDERED, bool PROD = false, int STAGE = 0, bool SELLU 
 #ifdef FOLP_WARP_TIMES
 #define FOLP_SEGDOT_BOUNDS __launch_bounds__(kBlock, kPlanCtasPerSm)  // same residency as the product build
 #else
+#ifdef FOLP_MINB  // A/B builds: CTAs per SM the compiler must fit
+#define FOLP_SEGDOT_BOUNDS __launch_bounds__(kBlock, FOLP_MINB)
+#else
 #define FOLP_SEGDOT_BOUNDS __launch_bounds__(kBlock)
+#endif
 #endif
 __global__ void FOLP_SEGDOT_BOUNDS
 segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
