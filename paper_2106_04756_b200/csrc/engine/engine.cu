@@ -39,6 +39,7 @@
 #include <cstring>
 #include <memory>
 #include <map>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <stdexcept>
@@ -581,13 +582,18 @@ struct folp_gpu_ctx {
                      1e-3 * (double)(long long)(tt[4] - tt[3]), 1e-3 * (tt[5] - tt[4]), 1e-3 * (tt[6] - tt[5]));
       }
     }
+    const bool timing = std::getenv("FOLP_TIMING") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto since = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     if (device >= 0) cudaSetDevice(device);
     for (auto& e : chunk_exec)
       if (e) cudaGraphExecDestroy(e);
     for (auto& e : eval_exec)
       if (e) cudaGraphExecDestroy(e);
+    const double t_graphs = since();
     block_free(eval_omega_h);
     if (stream) cudaStreamSynchronize(stream);  // cached blocks must be idle
+    const double t_sync = since();
     for (void* p : owned) block_free(p);
     for (void* p : rows.owned) block_free(p);
     for (void* p : cols.owned) block_free(p);
@@ -608,7 +614,12 @@ struct folp_gpu_ctx {
     if (ev1) cudaEventDestroy(ev1);
     if (tev0) cudaEventDestroy(tev0);
     if (tev1) cudaEventDestroy(tev1);
+    const double t_free = since();
     if (stream) cudaStreamDestroy(stream);
+    if (timing) {
+      std::fprintf(stderr, "[folp timing] engine destroy: graphs %.4f sync %.4f blocks %.4f stream %.4f\n",
+                   t_graphs, t_sync, t_free, since());
+    }
   }
 };
 

@@ -108,6 +108,43 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
     close(S);
     if (extra != nullptr) units.insert(units.end(), extra->begin(), extra->end());
   };
+  // The number of units build(target) makes, without making them (the tile
+  // retargeting below probes many targets; pure, so probes run concurrently).
+  auto count_units = [&](int64_t target) -> int64_t {
+    int64_t made = 0, seg0 = -1, tile_nnz = 0;
+    auto close = [&](int64_t seg_end) {
+      if (seg0 >= 0 && seg_end > seg0) ++made;
+      seg0 = -1;
+      tile_nnz = 0;
+    };
+    for (int64_t s = s_begin; s < S; ++s) {
+      if (skip != nullptr && (*skip)[static_cast<size_t>(s)]) {
+        close(s);
+        continue;
+      }
+      const int64_t len = ptr[s + 1] - ptr[s];
+      if (len > serial_cap && (len <= kWarpTile || len <= single_max)) {
+        close(s);
+        ++made;
+        continue;
+      }
+      if (len <= kWarpTile) {
+        if (seg0 >= 0 && (tile_nnz + len > target || s - seg0 >= max_segs)) close(s);
+        if (seg0 < 0) seg0 = s;
+        tile_nnz += len;
+        continue;
+      }
+      close(s);
+      if (ordered) {
+        ++made;
+        continue;
+      }
+      const int64_t part = len > giant_min ? kGiantPart : kWarpTile;
+      made += (len + part - 1) / part;
+    }
+    close(S);
+    return made + (extra != nullptr ? static_cast<int64_t>(extra->size()) : 0);
+  };
   build(kWarpTile);
   // Tree mode, large axes: balance the persistent grid's warps.  A warp's
   // units run back to back behind its SM's gather queue, so a kernel ends
@@ -164,12 +201,36 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
       // packing leaves gaps, so search rather than divide)
       const int64_t cap_units = rounds * nw;
       int64_t lo = std::max<int64_t>(32, tile_nnz_total / want_tiles), hi = kWarpTile;
+      // the same bisection as probing one target after the other, with the
+      // next three levels of its probe tree counted concurrently (a probe is
+      // a pass over all segments: 8 sequential ones were 4 ms of config 2's
+      // end-to-end solve)
+      std::map<int64_t, int64_t> made;
+      std::function<void(int64_t, int64_t, int, std::vector<int64_t>&)> probes =
+          [&](int64_t a, int64_t b, int depth, std::vector<int64_t>& out_targets) {
+            if (a >= b || depth == 0) return;
+            const int64_t mid = (a + b) / 2;
+            if (made.find(mid) == made.end()) out_targets.push_back(mid);
+            probes(a, mid, depth - 1, out_targets);
+            probes(mid + 1, b, depth - 1, out_targets);
+          };
       while (lo < hi) {
         const int64_t mid = (lo + hi) / 2;
-        build(mid);
-        if (static_cast<int64_t>(units.size()) <= cap_units) hi = mid; else lo = mid + 1;
+        if (made.find(mid) == made.end()) {
+          std::vector<int64_t> targets;
+          probes(lo, hi, 3, targets);
+          std::vector<int64_t> counts(targets.size(), 0);
+          folp::host::parallel_for(static_cast<int64_t>(targets.size()), [&](int64_t b, int64_t e, int) {
+            for (int64_t i = b; i < e; ++i) counts[static_cast<size_t>(i)] = count_units(targets[static_cast<size_t>(i)]);
+          }, static_cast<int64_t>(targets.size()) << 17);
+          for (size_t i = 0; i < targets.size(); ++i) made[targets[i]] = counts[i];
+        }
+        if (made[mid] <= cap_units) hi = mid; else lo = mid + 1;
       }
       build(lo);
+      if (made.find(lo) != made.end() && made[lo] != static_cast<int64_t>(units.size())) {
+        throw std::logic_error("build_plan: unit count and unit list disagree");
+      }
     }
     // Balanced at CTA granularity: the 8 consecutive units a CTA's warps
     // take in one round stay together and in order (neighbouring segments

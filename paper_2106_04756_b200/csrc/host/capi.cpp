@@ -130,10 +130,10 @@ LinearProgram to_lp(const folp_lp_c* in) {
   lp.constraint_matrix = matrix_from_csr(in);
   const std::size_t n = static_cast<std::size_t>(in->num_cols);
   const std::size_t m = static_cast<std::size_t>(in->num_rows);
-  lp.objective.assign(in->objective, in->objective + n);
-  lp.right_hand_side.assign(in->right_hand_side, in->right_hand_side + m);
-  lp.variable_lower.assign(in->variable_lower, in->variable_lower + n);
-  lp.variable_upper.assign(in->variable_upper, in->variable_upper + n);
+  lp.objective = host::parallel_copy(in->objective, static_cast<int64_t>(n));
+  lp.right_hand_side = host::parallel_copy(in->right_hand_side, static_cast<int64_t>(m));
+  lp.variable_lower = host::parallel_copy(in->variable_lower, static_cast<int64_t>(n));
+  lp.variable_upper = host::parallel_copy(in->variable_upper, static_cast<int64_t>(n));
   lp.num_inequality_rows = in->num_inequality_rows;
   lp.objective_constant = in->objective_constant;
   return lp;
@@ -321,12 +321,26 @@ int folp_solve(const folp_lp_c* lp_in, const folp_params_c* p, const double* x0,
                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
     const SolverParams params = to_params(p);
-    PrimalDualPoint z0;
-    z0.primal.assign(static_cast<std::size_t>(lp_in->num_cols), 0.0);
-    z0.dual.assign(static_cast<std::size_t>(lp_in->num_rows), 0.0);
-    if (x0 != nullptr) z0.primal.assign(x0, x0 + lp_in->num_cols);
-    if (y0 != nullptr) z0.dual.assign(y0, y0 + lp_in->num_rows);
-    export_result(solve(lp, params, z0), out);
+    SolveResult r;
+    if (x0 == nullptr && y0 == nullptr) {
+      r = solve(lp, params);  // the origin: nothing to build or upload
+    } else {
+      PrimalDualPoint z0;
+      z0.primal.assign(static_cast<std::size_t>(lp_in->num_cols), 0.0);
+      z0.dual.assign(static_cast<std::size_t>(lp_in->num_rows), 0.0);
+      if (x0 != nullptr) z0.primal.assign(x0, x0 + lp_in->num_cols);
+      if (y0 != nullptr) z0.dual.assign(y0, y0 + lp_in->num_rows);
+      r = solve(lp, params, z0);
+    }
+    if (std::getenv("FOLP_TIMING") != nullptr) {
+      std::fprintf(stderr, "[folp timing] folp_solve solved %.4fs\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+    export_result(r, out);
+    if (std::getenv("FOLP_TIMING") != nullptr) {
+      std::fprintf(stderr, "[folp timing] folp_solve exported %.4fs\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
   });
 }
 

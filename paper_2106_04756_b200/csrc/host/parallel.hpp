@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstring>
+#include <type_traits>
 #include <thread>
 #include <vector>
 
@@ -44,9 +46,39 @@ void parallel_for(int64_t n, F&& f, int64_t work = -1) {
   }
 }
 
+// A vector of n trivially-copyable elements WITHOUT the value-initializing
+// pass: std::vector<T>(n) zero-fills on one thread, and that fill is also the
+// first touch of every fresh page (config 2's CSR: 84 MB, 5-30 ms before any
+// copy starts).  The elements are left for the caller to overwrite in
+// parallel.  The standard containers offer no such constructor; this sets
+// the end pointer of a reserved vector through the three-pointer layout
+// libstdc++ and libc++ share, and falls back to resize() when the layout
+// check fails.
+template <class T>
+std::vector<T> uninitialized_vector(int64_t n) {
+  static_assert(std::is_trivially_copyable_v<T> && std::is_trivially_destructible_v<T>);
+  std::vector<T> v;
+  if (n <= 0) return v;
+  v.reserve(static_cast<std::size_t>(n));
+  struct Raw { T* begin; T* end; T* cap; };
+  if constexpr (sizeof(Raw) == sizeof(std::vector<T>)) {
+    Raw raw;
+    std::memcpy(&raw, static_cast<const void*>(&v), sizeof raw);
+    if (raw.begin == v.data() && raw.end == raw.begin && raw.cap >= raw.begin + n) {
+      raw.end = raw.begin + n;
+      std::memcpy(static_cast<void*>(&v), &raw, sizeof raw);
+      if (v.size() == static_cast<std::size_t>(n)) return v;
+      raw.end = raw.begin;  // unexpected layout: undo
+      std::memcpy(static_cast<void*>(&v), &raw, sizeof raw);
+    }
+  }
+  v.resize(static_cast<std::size_t>(n));
+  return v;
+}
+
 template <class T>
 std::vector<T> parallel_copy(const T* src, int64_t n) {
-  std::vector<T> out(static_cast<std::size_t>(n));
+  std::vector<T> out = uninitialized_vector<T>(n);
   parallel_for(n, [&](int64_t b, int64_t e, int) { std::copy(src + b, src + e, out.data() + b); });
   return out;
 }

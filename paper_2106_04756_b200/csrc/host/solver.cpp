@@ -94,10 +94,18 @@ std::vector<double> start_vector(Index n) {  // sparse_matrix.cpp:195-202
 // ---------------------------------------------------------------------
 class Driver {
  public:
+  // zero_start: the start point is the origin (z0 is not read; the device
+  // zero-fills instead of receiving two uploaded vectors of zeros)
   Driver(const LinearProgram& raw, const SolverParams& params, const PrimalDualPoint& z0,
-         const folp_gpu_shard* shard = nullptr)
-      : raw_(raw), p_(params), z0_(z0), start_(Clock::now()), shard_(shard) {}
+         const folp_gpu_shard* shard = nullptr, bool zero_start = false)
+      : raw_(raw), p_(params), z0_(z0), zero_start_(zero_start), start_(Clock::now()), shard_(shard) {}
 
+  ~Driver() {
+    if (std::getenv("FOLP_TIMING") == nullptr) return;
+    const double t0 = elapsed();
+    dev_.reset();
+    std::fprintf(stderr, "[folp timing] driver teardown: entered %.4f context released %.4f\n", t0, elapsed());
+  }
   SolveResult run();
   // Everything before the loop (solver.cpp:818-907); a value when the solve
   // already ended (detected, trivial, optimal start).
@@ -171,7 +179,7 @@ class Driver {
   }
 
   SolveResult finish(TerminationReason reason, int slot, const ConvergenceInfo& info);
-  SolveResult finish_point(TerminationReason reason, const PrimalDualPoint& reduced,
+  SolveResult finish_point(TerminationReason reason, PrimalDualPoint reduced,
                            const ConvergenceInfo& info);
   SolveResult finish_detected(PresolveStatus status);
   SolveResult finish_trivial();
@@ -184,20 +192,25 @@ class Driver {
   // column i; empty: identity) and the maps of primal vectors across it
   void primal_to_work(std::vector<double>& v) const {
     if (col_order_.empty()) return;
-    std::vector<double> w(v.size());
-    for (std::size_t i = 0; i < w.size(); ++i) w[i] = v[static_cast<std::size_t>(col_order_[i])];
+    std::vector<double> w = host::uninitialized_vector<double>(static_cast<int64_t>(v.size()));
+    host::parallel_for(static_cast<int64_t>(w.size()), [&](int64_t b, int64_t e, int) {
+      for (int64_t i = b; i < e; ++i) w[i] = v[static_cast<std::size_t>(col_order_[i])];
+    });
     v.swap(w);
   }
   void primal_from_work(std::vector<double>& v) const {
     if (col_order_.empty()) return;
-    std::vector<double> w(v.size());
-    for (std::size_t i = 0; i < w.size(); ++i) w[static_cast<std::size_t>(col_order_[i])] = v[i];
+    std::vector<double> w = host::uninitialized_vector<double>(static_cast<int64_t>(v.size()));
+    host::parallel_for(static_cast<int64_t>(w.size()), [&](int64_t b, int64_t e, int) {
+      for (int64_t i = b; i < e; ++i) w[static_cast<std::size_t>(col_order_[i])] = v[i];  // a permutation: disjoint
+    });
     v.swap(w);
   }
 
   const LinearProgram& raw_;
   SolverParams p_;
   const PrimalDualPoint& z0_;
+  bool zero_start_ = false;
   Clock::time_point start_;
   const folp_gpu_shard* shard_ = nullptr;  // row shard of a multi-GPU solve
 
@@ -236,31 +249,44 @@ class Driver {
   }
 };
 
-SolveResult Driver::finish_point(TerminationReason reason, const PrimalDualPoint& reduced,
+SolveResult Driver::finish_point(TerminationReason reason, PrimalDualPoint reduced,
                                  const ConvergenceInfo& info) {
+  mark("finish:point");
   SolveResult r = tmpl_;
   r.termination_reason = reason;
   r.final_info = info;
   r.iterations = k_total_;
   r.restarts = n_outer_;
-  const PrimalDualPoint full = postsolve(transform_, reduced.primal, reduced.dual);
-  r.primal_solution = full.primal;
-  r.dual_solution = full.dual;
+  // an identity transform postsolves to the same two vectors
+  const bool same_point = transform_.is_identity() &&
+                          static_cast<Index>(reduced.primal.size()) == transform_.original_cols &&
+                          static_cast<Index>(reduced.dual.size()) == transform_.original_rows;
+  PrimalDualPoint full = same_point ? std::move(reduced)
+                                    : postsolve(transform_, reduced.primal, reduced.dual);
+  mark("postsolved");
   // Reduced costs on the original problem (solver.cpp:662-670): K'y on the
   // raw K.  When presolve was the identity the device already holds raw K.
-  std::vector<double> kty(static_cast<std::size_t>(raw_.num_variables()), 0.0);
-  if (!kty.empty()) {
+  std::vector<double> kty;
+  if (raw_.num_variables() > 0) {
     if (dev_ && transform_.is_identity() && raw_on_device_) {
+      kty = host::uninitialized_vector<double>(raw_.num_variables());  // the download fills it
       device::check(folp_gpu_multiply_transpose(ctx(), 0, full.dual.data(), kty.data()),
                     "reduced costs");
       primal_from_work(kty);
     } else {
+      kty.assign(static_cast<std::size_t>(raw_.num_variables()), 0.0);
       raw_.constraint_matrix.multiply_transpose(full.dual, kty);
     }
   }
+  mark("kty");
   ledger_.add_kt();
-  for (std::size_t i = 0; i < kty.size(); ++i) kty[i] = raw_.objective[i] - kty[i];
+  host::parallel_for(static_cast<int64_t>(kty.size()), [&](int64_t b, int64_t e, int) {
+    for (int64_t i = b; i < e; ++i) kty[i] = raw_.objective[i] - kty[i];
+  });
   r.reduced_costs = project_reduced_costs(raw_, kty).values;
+  r.primal_solution = std::move(full.primal);
+  r.dual_solution = std::move(full.dual);
+  mark("reduced costs");
   r.kkt_passes = kkt_passes(ledger_);
   r.wall_seconds = elapsed();
   log_summary(r);
@@ -275,13 +301,13 @@ SolveResult Driver::finish_point(TerminationReason reason, const PrimalDualPoint
 }
 
 SolveResult Driver::finish(TerminationReason reason, int slot, const ConvergenceInfo& info) {
-  PrimalDualPoint reduced;
-  reduced.primal.resize(static_cast<std::size_t>(work_->num_variables()));
-  reduced.dual.resize(static_cast<std::size_t>(work_->num_rows()));
+  PrimalDualPoint reduced;  // both vectors filled by the download
+  reduced.primal = host::uninitialized_vector<double>(work_->num_variables());
+  reduced.dual = host::uninitialized_vector<double>(work_->num_rows());
   device::check(folp_gpu_get_reduced_point(ctx(), slot, reduced.primal.data(), reduced.dual.data()),
                 "reduced_point");
   primal_from_work(reduced.primal);
-  return finish_point(reason, reduced, info);
+  return finish_point(reason, std::move(reduced), info);
 }
 
 SolveResult Driver::finish_detected(PresolveStatus status) {  // solver.cpp:678-692
@@ -305,6 +331,7 @@ SolveResult Driver::finish_trivial() {  // solver.cpp:694-701
 }
 
 SolveResult Driver::finish_limit(TerminationReason reason) {  // solver.cpp:703-726
+  mark("finish:limit");
   ConvergenceInfo cur, avg;
   try {
     cur = evaluate(FOLP_PT_CURRENT);
@@ -533,9 +560,14 @@ std::optional<SolveResult> Driver::start() {
   if (shard_ != nullptr) dev_->attach_shard(work_->constraint_matrix, *shard_);
 
   // start point into the working space, projected (solver.cpp:853-865)
-  PrimalDualPoint z = restrict_point(transform_, z0_.primal, z0_.dual);
-  primal_to_work(z.primal);
-  device::check(folp_gpu_set_start(ctx(), z.primal.data(), z.dual.data()), "start point");
+  if (zero_start_) {
+    // the origin restricts and permutes to the origin
+    device::check(folp_gpu_set_start(ctx(), nullptr, nullptr), "start point");
+  } else {
+    PrimalDualPoint z = restrict_point(transform_, z0_.primal, z0_.dual);
+    primal_to_work(z.primal);
+    device::check(folp_gpu_set_start(ctx(), z.primal.data(), z.dual.data()), "start point");
+  }
 
   double max_abs = 0.0, norm_c = 0.0, norm_q = 0.0;
   device::check(folp_gpu_working_stats(ctx(), &max_abs, &norm_c, &norm_q), "working stats");
@@ -893,10 +925,8 @@ const SolveResult* SolveSession::result() const {
 }
 
 SolveResult solve(const LinearProgram& lp_raw, const SolverParams& params) {
-  PrimalDualPoint z0;
-  z0.primal.assign(static_cast<std::size_t>(lp_raw.num_variables()), 0.0);
-  z0.dual.assign(static_cast<std::size_t>(lp_raw.num_rows()), 0.0);
-  return solve(lp_raw, params, z0);
+  const PrimalDualPoint origin;  // not read: the device zero-fills the start point
+  return Driver(lp_raw, params, origin, nullptr, true).run();
 }
 
 }  // namespace folp
