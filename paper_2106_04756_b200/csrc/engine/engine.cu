@@ -158,6 +158,8 @@ struct folp_gpu_ctx {
   double objective_constant = 0.0;
 
   int *csr_ptr = nullptr, *csr_col = nullptr, *csc_ptr = nullptr, *csc_row = nullptr;
+  struct Staged { void* pinned; double* host_dst; size_t bytes; };
+  std::vector<Staged> staged;  // staged vector copies in flight (plans.cuh upload / download)
   double *csr_orig = nullptr, *csc_orig = nullptr, *csr_work = nullptr, *csc_work = nullptr;
   PlanDev rows, cols;
 
@@ -593,6 +595,7 @@ struct folp_gpu_ctx {
     const double t_graphs = since();
     block_free(eval_omega_h);
     if (stream) cudaStreamSynchronize(stream);  // cached blocks must be idle
+    for (const Staged& sg : staged) block_free(sg.pinned);
     const double t_sync = since();
     for (void* p : owned) block_free(p);
     for (void* p : rows.owned) block_free(p);
@@ -950,7 +953,7 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
       if (m) CK(cudaMemsetAsync(c->kx[i], 0, m * sizeof(double), c->stream));
     }
     zero_average(c.get());
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c.get());
     const char* l2env = std::getenv("FOLP_L2_PERSIST");
     if (l2env == nullptr || std::atoi(l2env) > 0) {
       // keep the loop's streams in L2 (persisting lines) across trials
@@ -1032,7 +1035,7 @@ int folp_gpu_rescale(folp_gpu_ctx* c, int64_t ruiz_iterations, int32_t pock_cham
     CK(cudaGetLastError());
     download(c, row_scale, cum1, m);
     download(c, col_scale, cum2, n);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
     c->kx_valid = false;
   });
 }
@@ -1064,7 +1067,7 @@ int folp_gpu_get_working(folp_gpu_ctx* c, double* csr_values, double* csc_values
     download(c, rhs, c->qw, c->m);
     download(c, lower, c->lw, c->n);
     download(c, upper, c->uw, c->n);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 
@@ -1080,7 +1083,7 @@ int folp_gpu_set_start(folp_gpu_ctx* c, const double* x0, const double* y0) {
     CK(cudaGetLastError());
     zero_average(c);
     refresh_kx(c);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 
@@ -1090,7 +1093,7 @@ int folp_gpu_set_point(folp_gpu_ctx* c, int32_t which, const double* x, const do
     upload(c, c->slot_x(which), x, c->n);
     upload(c, c->slot_y(which), y, c->m);
     if (which == FOLP_PT_CURRENT) refresh_kx(c);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 
@@ -1099,7 +1102,7 @@ int folp_gpu_get_point(folp_gpu_ctx* c, int32_t which, double* x, double* y) {
     prep(c);
     download(c, x, c->slot_x(which), c->n);
     download(c, y, c->slot_y(which), c->m);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 
@@ -1113,7 +1116,7 @@ int folp_gpu_get_reduced_point(folp_gpu_ctx* c, int32_t which, double* x, double
     CK(cudaGetLastError());
     download(c, x, c->xr, c->n);
     download(c, y, c->yr, c->m);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 
@@ -1491,6 +1494,7 @@ int folp_gpu_spectral_norm(folp_gpu_ctx* c, const double* v0, double relative_to
     double* w = c->aux_y;
     double* s = c->xr;
     upload(c, v, v0, c->n);
+    sync_transfers(c);
     double lambda = 0.0;
     for (int64_t it = 0; it < max_iterations; ++it) {
       product(c, false, true, v, w);
@@ -1520,7 +1524,7 @@ int folp_gpu_multiply(folp_gpu_ctx* c, int32_t working, const double* xh, double
     upload(c, c->aux_x, xh, c->n);
     product(c, false, working != 0, c->aux_x, c->kx_aux);
     download(c, out, c->kx_aux, c->m);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 
@@ -1530,7 +1534,7 @@ int folp_gpu_multiply_transpose(folp_gpu_ctx* c, int32_t working, const double* 
     upload(c, c->aux_y, yh, c->m);
     product(c, true, working != 0, c->aux_y, c->xr);
     download(c, out, c->xr, c->n);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 
@@ -1555,7 +1559,7 @@ int folp_gpu_axis_norms(folp_gpu_ctx* c, int32_t axis, double p, int32_t working
     (void)ptr;
     axis_pnorm(c, rows, val, p, dst);
     download(c, out, dst, S);
-    CK(cudaStreamSynchronize(c->stream));
+    sync_transfers(c);
   });
 }
 

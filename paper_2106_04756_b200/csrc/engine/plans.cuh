@@ -354,18 +354,56 @@ void upload_index(folp_gpu_ctx* c, const int64_t* src, int* dst, int64_t count, 
   }
 }
 
+// Host <-> device vector copies.  Vectors of at least kStageMin doubles go
+// through a cached pinned block: pageable cudaMemcpyAsync ran at 2-3 GB/s on
+// the B200 hosts (the final point of config 2, 4.8 MB, took 1.8 ms), a DMA
+// from / to pinned memory plus a memcpy on all host cores a fifth of that.
+// A staged copy completes in sync_transfers(), which every entry point that
+// uploads or downloads calls in place of its stream synchronize.
+constexpr int64_t kStageMin = int64_t(1) << 15;
 void upload(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
   if (count <= 0) return;
+  const size_t bytes = static_cast<size_t>(count) * sizeof(double);
   if (src == nullptr) {
-    CK(cudaMemsetAsync(dst, 0, count * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(dst, 0, bytes, c->stream));
+  } else if (count >= kStageMin) {
+    double* h = static_cast<double*>(block_alloc(bytes, true));
+    c->staged.push_back({h, nullptr, bytes});
+    folp::host::parallel_for(count, [&](int64_t b, int64_t e, int) {
+      std::memcpy(h + b, src + b, static_cast<size_t>(e - b) * sizeof(double));
+    });
+    CK(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, c->stream));
   } else {
-    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
   }
 }
 void download(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
-  if (count > 0 && dst != nullptr) {
-    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (count <= 0 || dst == nullptr) return;
+  const size_t bytes = static_cast<size_t>(count) * sizeof(double);
+  if (count >= kStageMin) {
+    double* h = static_cast<double*>(block_alloc(bytes, true));
+    c->staged.push_back({h, dst, bytes});
+    CK(cudaMemcpyAsync(h, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
   }
+}
+// Stream synchronize + the host half of the staged copies.
+void sync_transfers(folp_gpu_ctx* c) {
+  const cudaError_t err = cudaStreamSynchronize(c->stream);
+  for (const auto& s : c->staged) {
+    if (err == cudaSuccess && s.host_dst != nullptr) {
+      const int64_t count = static_cast<int64_t>(s.bytes / sizeof(double));
+      const double* h = static_cast<const double*>(s.pinned);
+      double* d = s.host_dst;
+      folp::host::parallel_for(count, [&](int64_t b, int64_t e, int) {
+        std::memcpy(d + b, h + b, static_cast<size_t>(e - b) * sizeof(double));
+      });
+    }
+    block_free(s.pinned);
+  }
+  c->staged.clear();
+  CK(err);
 }
 void copy_d2d(folp_gpu_ctx* c, double* dst, const double* src, int64_t count) {
   if (count > 0 && dst != src) {

@@ -10,6 +10,11 @@
 #include <cstdint>
 #include <cstring>
 #include <type_traits>
+#include <condition_variable>
+#include <deque>
+#include <exception>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -21,8 +26,105 @@ inline int host_threads(int64_t work) {
   return static_cast<int>(std::min<int64_t>({hw, by_work, 32}));
 }
 
-// f(begin, end, thread) over [0, n) split into contiguous chunks; `work`
-// (default n) sizes the thread count (a row loop passes its nonzeros).
+// Persistent workers for parallel_for.  Starting and joining up to 32
+// std::threads per call cost ~0.5 ms each on the B200 hosts, and config 2's
+// end-to-end solve makes a dozen such calls (ingest, histogram, staging);
+// the workers are started once per process and sleep between calls.  Any
+// number of host threads may submit batches at once; the submitting thread
+// takes chunks itself, so a batch completes even when every worker is busy
+// (or when it is submitted from inside another batch).
+class WorkerPool {
+ public:
+  static WorkerPool& get() {
+    static WorkerPool* pool = new WorkerPool();  // process lifetime: never joined at exit
+    return *pool;
+  }
+  // job(i) for every chunk i in [0, chunks); returns when all have run and
+  // rethrows the first exception a chunk raised.
+  void run(int chunks, const std::function<void(int)>& job) {
+    Batch batch;
+    batch.job = &job;
+    batch.chunks = chunks;
+    batch.left = chunks;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      queue_.push_back(&batch);
+    }
+    cv_.notify_all();
+    for (;;) {  // the submitter works too
+      int i = -1;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        i = claim(&batch);
+      }
+      if (i < 0) break;
+      execute(&batch, i);
+    }
+    std::unique_lock<std::mutex> lk(batch.mu);
+    batch.cv.wait(lk, [&] { return batch.left == 0; });
+    if (batch.err) std::rethrow_exception(batch.err);
+  }
+
+ private:
+  struct Batch {
+    const std::function<void(int)>* job = nullptr;
+    int chunks = 0;
+    int next = 0;   // guarded by the pool mutex
+    int left = 0;   // guarded by mu
+    std::mutex mu;
+    std::condition_variable cv;
+    std::exception_ptr err;
+  };
+  WorkerPool() {
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int workers = std::min(hw, 32) - 1;
+    for (int w = 0; w < workers; ++w) {
+      std::thread([this] { work(); }).detach();
+    }
+  }
+  // pool mutex held: the next chunk of `only` (or of the oldest open batch)
+  int claim(Batch* only, Batch** from = nullptr) {
+    for (auto it = queue_.begin(); it != queue_.end(); ++it) {
+      Batch* b = *it;
+      if (only != nullptr && b != only) continue;
+      const int i = b->next++;
+      if (b->next >= b->chunks) queue_.erase(it);
+      if (from != nullptr) *from = b;
+      return i;
+    }
+    return -1;
+  }
+  static void execute(Batch* b, int i) {
+    std::exception_ptr err;
+    try {
+      (*b->job)(i);
+    } catch (...) {
+      err = std::current_exception();
+    }
+    // the last touch of *b: the submitter may return once left reaches 0
+    std::lock_guard<std::mutex> lk(b->mu);
+    if (err && !b->err) b->err = err;
+    if (--b->left == 0) b->cv.notify_one();
+  }
+  void work() {
+    for (;;) {
+      Batch* b = nullptr;
+      int i = -1;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return !queue_.empty(); });
+        i = claim(nullptr, &b);
+      }
+      if (i >= 0) execute(b, i);
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<Batch*> queue_;
+};
+
+// f(begin, end, chunk) over [0, n) split into contiguous chunks; `work`
+// (default n) sizes the chunk count (a row loop passes its nonzeros).
 template <class F>
 void parallel_for(int64_t n, F&& f, int64_t work = -1) {
   const int t = static_cast<int>(std::min<int64_t>(host_threads(work < 0 ? n : work), std::max<int64_t>(n, 1)));
@@ -30,20 +132,10 @@ void parallel_for(int64_t n, F&& f, int64_t work = -1) {
     f(int64_t(0), n, 0);
     return;
   }
-  // joins on every exit path: a failed thread start must not leave joinable
-  // threads behind (std::terminate in ~thread)
-  struct Pool {
-    std::vector<std::thread> v;
-    ~Pool() {
-      for (auto& th : v)
-        if (th.joinable()) th.join();
-    }
-  } pool;
-  pool.v.reserve(t);
-  for (int i = 0; i < t; ++i) {
-    const int64_t b = n * i / t, e = n * (i + 1) / t;
-    pool.v.emplace_back([&f, b, e, i] { f(b, e, i); });
-  }
+  const std::function<void(int)> job = [&f, n, t](int i) {
+    f(n * i / t, n * (i + 1) / t, i);
+  };
+  WorkerPool::get().run(t, job);
 }
 
 // A vector of n trivially-copyable elements WITHOUT the value-initializing
