@@ -105,6 +105,7 @@ int guarded(F&& f) {
 // ---------------------------------------------------------------------
 struct PlanDev {
   SegPlan sp{};
+  int pair_len = 0;  // 2: every segment holds exactly two entries (pair_kernel)
   std::vector<void*> owned;
   const int* long_segs = nullptr;  // segments above kLongSeq entries (sequential norms)
   int n_long = 0;
@@ -399,6 +400,38 @@ struct folp_gpu_ctx {
     return stage_env != 0 && (&p == &rows || &p == &cols) && p.sp.vec_len > 0 &&
            p.sp.vec_len * static_cast<int64_t>(sizeof(double)) <= kStageMaxBytes;
   }
+  // Axes of two-entry segments (segdot.cuh pair_kernel): the loop's own
+  // products in tree mode; FOLP_PAIRS=0 keeps the warp tiles.
+  int pairs_env = -1;
+  template <class Epi>
+  bool pairs_ok(const PlanDev& p) {
+    if (pairs_env < 0) {
+      const char* env = std::getenv("FOLP_PAIRS");
+      pairs_env = env != nullptr ? std::atoi(env) : 1;
+    }
+    return pairs_env != 0 && TraceSlot<Epi>::v >= 0 && p.pair_len == 2 && (&p == &rows || &p == &cols);
+  }
+  template <class Epi>
+  void launch_pairs(const PlanDev& p, const double* val, const Epi& epi, RedBuf rb) {
+    auto fn = pair_kernel<Epi>;
+    const int64_t need = (static_cast<int64_t>(p.sp.S) + 2 * kBlock - 1) / (2 * kBlock);
+    const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    int na = 0;
+    if (pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    CK(cudaLaunchKernelEx(&cfg, fn, p.sp.S, p.sp.idx, val, p.sp.vec_len, epi, rb));
+  }
   template <class Epi, bool ORD, bool PR, int ST = 0, bool SE = false>
   void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb,
                      int smem = 0) {
@@ -466,6 +499,8 @@ struct folp_gpu_ctx {
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, false, true>(grid, p.sp, prod, epi, rb);
       ++launches;
+    } else if (pairs_ok<Epi>(p)) {
+      if constexpr (TraceSlot<Epi>::v >= 0) launch_pairs(p, val, epi, rb);
     } else if (p.sp.sell.n_groups > 0) {
       // a plan with SELL-32 groups (sell.cuh)
       auto fn = segdot_kernel<Epi, false, false, 0, true>;

@@ -315,9 +315,13 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   };
   {
     std::vector<int> ls;
+    bool pairs = s_begin == 0 && S > 0 && skip == nullptr && ptr[0] == 0;
     for (int64_t sg = s_begin; sg < S; ++sg) {
-      if (ptr[sg + 1] - ptr[sg] > kLongSeq) ls.push_back(static_cast<int>(sg));
+      const int64_t len = ptr[sg + 1] - ptr[sg];
+      if (len > kLongSeq) ls.push_back(static_cast<int>(sg));
+      pairs = pairs && len == 2;
     }
+    out.pair_len = pairs ? 2 : 0;  // every segment s is entries 2s, 2s+1 (pair_kernel)
     out.n_long = static_cast<int>(ls.size());
     if (!ls.empty()) out.long_segs = up(ls);
   }

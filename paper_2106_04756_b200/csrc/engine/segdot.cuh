@@ -723,6 +723,92 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
 #endif
 }
 
+// Two-entry segments, one thread per segment (tree mode, the loop's
+// products).  An axis whose every segment holds exactly two entries -- the
+// columns of a node-arc incidence matrix: transportation, assignment and
+// network-flow LPs; config 5 has 16M of them -- needs no unit plan, segment
+// bounds or shared memory: segment s owns entries 2s and 2s+1, so a thread
+// reads its indices as one int2 and its values as one double2 (consecutive
+// threads, consecutive 8 / 16 bytes), and the kernel is a stream of
+// independent loads, two segments per thread in flight.  Through the warp
+// tiles the same axis ran at 57 % of the HBM peak: a lane owned four
+// segments of a 128-segment tile one after the other, each with its own
+// dependent operand loads behind the tile's shared-memory round trip.
+// The dot is 0 + p0 + p1 in entry order, as in the tiles (bit-identical).
+// The first round's entries are static data and are loaded BEFORE
+// griddepcontrol.wait, under the predecessor's tail.  Plain read-only loads:
+// evict-first (ld.global.cs) streams measured 466 vs 424 us per config-5
+// trial, a 256-byte L2 prefetch hint, 4 or 8 CTAs per SM and a 2.7x larger
+// grid no change (profiles/r2_experiments_s4.md).
+template <class Epi>
+__global__ void __launch_bounds__(kBlock)
+pair_kernel(int S, const int* __restrict__ idx, const double* __restrict__ val, int vec_len, Epi epi,
+            RedBuf rb) {
+  constexpr int K = Epi::K;
+  const int2* __restrict__ idx2 = reinterpret_cast<const int2*>(idx);
+  const double2* __restrict__ val2 = reinterpret_cast<const double2*>(val);
+  const int stride = static_cast<int>(gridDim.x) * kBlock;
+  int s = static_cast<int>(blockIdx.x) * kBlock + threadIdx.x;
+  int2 ia = make_int2(0, 0), ib = make_int2(0, 0);
+  double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
+  if (s < S) {
+    ia = __ldg(&idx2[s]);
+    va = __ldg(&val2[s]);
+  }
+  if (s < S - stride) {
+    ib = __ldg(&idx2[s + stride]);
+    vb = __ldg(&val2[s + stride]);
+  }
+  griddep_wait();
+  griddep_launch();
+  if (!epi.prepare()) return;
+  const double* __restrict__ vec = epi.vec();
+  TreeAcc<K> acc;
+  acc.zero();
+  (void)vec_len;
+  for (; s < S; s += 2 * stride) {
+    const bool two = s < S - stride;
+    const typename Epi::Pre pa = epi.load(s);
+    typename Epi::Pre pb{};
+    if (two) pb = epi.load(s + stride);
+    FOLP_DCHECK(vec_len == 0 || (ia.x >= 0 && ia.x < vec_len && ia.y >= 0 && ia.y < vec_len));
+    FOLP_DCHECK(!two || vec_len == 0 || (ib.x >= 0 && ib.x < vec_len && ib.y >= 0 && ib.y < vec_len));
+    const double ga0 = __ldg(&vec[ia.x]), ga1 = __ldg(&vec[ia.y]);
+    double gb0 = 0.0, gb1 = 0.0;
+    if (two) {
+      gb0 = __ldg(&vec[ib.x]);
+      gb1 = __ldg(&vec[ib.y]);
+    }
+    // the next round's entries, in flight across this round's epilogues
+    const int sn = s + 2 * stride;
+    int2 na = make_int2(0, 0), nb = make_int2(0, 0);
+    double2 wa = make_double2(0.0, 0.0), wb = make_double2(0.0, 0.0);
+    if (sn < S) {
+      na = __ldg(&idx2[sn]);
+      wa = __ldg(&val2[sn]);
+    }
+    if (sn < S - stride) {
+      nb = __ldg(&idx2[sn + stride]);
+      wb = __ldg(&val2[sn + stride]);
+    }
+    double dot = 0.0;
+    dot += va.x * ga0;
+    dot += va.y * ga1;
+    epi.apply(s, dot, pa, acc);
+    if (two) {
+      dot = 0.0;
+      dot += vb.x * gb0;
+      dot += vb.y * gb1;
+      epi.apply(s + stride, dot, pb, acc);
+    }
+    ia = na;
+    ib = nb;
+    va = wa;
+    vb = wb;
+  }
+  if constexpr (Epi::kReduce) reduce_tail(epi, acc.v, rb, 0);
+}
+
 // A warp's unit of one plan held in registers for a whole chunk (small
 // problems: every warp of the cluster owns at most one unit per product, so
 // its descriptor, index stream, values and segment bounds never change
