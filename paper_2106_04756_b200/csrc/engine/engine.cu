@@ -159,6 +159,7 @@ struct folp_gpu_ctx {
   double objective_constant = 0.0;
 
   int *csr_ptr = nullptr, *csr_col = nullptr, *csc_ptr = nullptr, *csc_row = nullptr;
+  bool l2_window = false;  // the loop's streams hold an L2 persisting window
   struct Staged { void* pinned; double* host_dst; size_t bytes; };
   std::vector<Staged> staged;  // staged vector copies in flight (plans.cuh upload / download)
   double *csr_orig = nullptr, *csc_orig = nullptr, *csr_work = nullptr, *csc_work = nullptr;
@@ -654,6 +655,9 @@ struct folp_gpu_ctx {
     if (tev1) cudaEventDestroy(tev1);
     const double t_free = since();
     if (stream) cudaStreamDestroy(stream);
+    // lines this context pinned go back to normal (a later, larger context
+    // would otherwise stream past a carve-out full of dead lines)
+    if (l2_window) cudaCtxResetPersistingL2Cache();
     if (timing) {
       std::fprintf(stderr, "[folp timing] engine destroy: graphs %.4f sync %.4f blocks %.4f stream %.4f\n",
                    t_graphs, t_sync, t_free, since());
@@ -995,7 +999,14 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
       int max_persist = 0, max_window = 0;
       cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device);
       cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
-      if (max_persist > 0 && max_window > 0) {
+      // Only when the block (nearly) fits the persisting carve-out.  A larger
+      // block keeps a random ~max_persist of its lines pinned and leaves the
+      // rest of the L2 to every other stream: measured per trial, config 5
+      // (768 MB block) 426.7 us with the window vs 284.6 us without, config
+      // 3 (480 MB) 306.8 vs 249.7 us; config 2 (84 MB, fits) 56.0 vs 58.0 us.
+      // FOLP_L2_PERSIST=2 forces the window.
+      const bool fits = c->loop_block_bytes <= static_cast<size_t>(max_persist) + (static_cast<size_t>(max_persist) >> 2);
+      if (max_persist > 0 && max_window > 0 && (fits || (l2env != nullptr && std::atoi(l2env) > 1))) {
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
         cudaStreamAttrValue attr{};
         const size_t bytes = std::min(c->loop_block_bytes, static_cast<size_t>(max_window));
@@ -1006,6 +1017,7 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
         attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+        c->l2_window = true;
         cudaGetLastError();
         if (timing) {
           std::fprintf(stderr, "[folp timing] L2 persist: max %d B, window max %d B, block %zu B\n",
