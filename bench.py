@@ -358,9 +358,15 @@ def run_b200(args, world, rank, local):
                      trace_capacity=1, shard=spec)
     e2e_s = time.perf_counter() - t
     e2e_s = allreduce_max(e2e_s, world)
-    # CSR+CSC pointers and int64 indices + values, c/l/u/q, start point
-    h2d = 8 * (m + n + 2) + 32 * nnz + 8 * (3 * n + m) + 8 * (n + m)
-    d2h = 8 * (n + m) + 8 * n
+    # what folp_solve moves over PCIe for one solve: row starts (int64), column
+    # indices (narrowed to int32 on the host), values, c / l / u / q, the
+    # column order and its inverse (int32, degree-ordered contexts), the final
+    # dual for the reduced costs; the CSC is built on the device and a zero
+    # start point is a device memset.  Back: the final point, K'y for the
+    # reduced costs, the column starts the host plans from, and 48 doubles of
+    # evaluation results per period.
+    h2d = 8 * (m + 1) + 12 * nnz + 8 * (3 * n + m) + 8 * n + 8 * m
+    d2h = 8 * (n + m) + 8 * n + 8 * (n + 1) + 48 * 8 * args.steps
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

@@ -410,8 +410,14 @@ struct folp_gpu_ctx {
       const char* env = std::getenv("FOLP_PAIRS");
       pairs_env = env != nullptr ? std::atoi(env) : 1;
     }
-    return pairs_env != 0 && TraceSlot<Epi>::v >= 0 && p.pair_len == 2 && (&p == &rows || &p == &cols);
+    const bool ok = pairs_env != 0 && TraceSlot<Epi>::v >= 0 && p.pair_len == 2 && (&p == &rows || &p == &cols);
+    if (ok && !pairs_said && std::getenv("FOLP_TIMING") != nullptr) {
+      std::fprintf(stderr, "[folp timing] pair kernel on the axis of %d two-entry segments\n", p.sp.S);
+      pairs_said = true;
+    }
+    return ok;
   }
+  bool pairs_said = false;
   template <class Epi>
   void launch_pairs(const PlanDev& p, const double* val, const Epi& epi, RedBuf rb) {
     auto fn = pair_kernel<Epi>;
@@ -437,16 +443,17 @@ struct folp_gpu_ctx {
   void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb,
                      int smem = 0) {
     auto fn = segdot_kernel<Epi, ORD, PR, ST, SE>;
-    // L1 / shared split: for degree-ordered columns (a hot prefix of the
-    // gathered vector), the smallest shared carveout that still holds
-    // kPlanCtasPerSm CTAs leaves the most L1 to the gathers (config 2 59.7
-    // -> 57.6 us per trial); other layouts keep the driver's choice (config
-    // 4's window-blocked products lose 25 % with it, config 5 3 %).
+    // L1 / shared split: the smallest shared carveout that still holds
+    // kPlanCtasPerSm CTAs leaves the most L1 to the gathers (config 2's
+    // degree-ordered hot prefix: 59.7 -> 57.6 us per trial; config 3 250.2
+    // -> 243.2 us; config 5 unchanged); window-blocked contexts keep the
+    // driver's choice (config 4 loses 25 % with the small carveout).
     // FOLP_CARVEOUT=% forces one split everywhere, -1 = driver default.
     // Set per launch (a launch attribute, captured into graph nodes too), so
     // concurrent contexts of both kinds never share mutable state.
     const char* env = std::getenv("FOLP_CARVEOUT");
-    const int want = ST != 0 ? 100 : env != nullptr ? std::atoi(env) : (hot_columns ? kSegdotCarveout : -1);
+    const bool windowed = brows.windows > 0 || bcols.windows > 0;
+    const int want = ST != 0 ? 100 : env != nullptr ? std::atoi(env) : (!windowed ? kSegdotCarveout : -1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kBlock);

@@ -271,3 +271,31 @@ def test_sell_row_groups(eng, ref, cfg, scale, min_len, monkeypatch, capfd):
     pa, pb = a.final_info["primal_objective"], b.final_info["primal_objective"]
     assert abs(pa - pb) <= 1e-8 * (2 + 2 * abs(pa) + 2 * abs(pb))
     assert a.step_condition_violations == 0
+
+
+@pytest.mark.parametrize("scale", [0.05, 0.02])
+def test_two_entry_columns(eng, ref, scale, monkeypatch, capfd):
+    """The loop's K'y over two-entry columns, one thread per column (engine
+    segdot.cuh pair_kernel): config 5's columns are a node-arc incidence
+    structure (one supply row, one demand row).  The first 100 iterates
+    within the reference's noise floor with identical restarts and ledger --
+    with the pair kernel and with the warp tiles it replaces (FOLP_PAIRS=0)
+    -- and the first accepted iterate bit-identical between the two (its
+    primal step does not depend on any reduction order)."""
+    lp = instances.generate(5, 2, scale)
+    p = cabi.params(record_iterate_trace=True, iteration_limit=100)
+    b = ref.solve_lp(lp, p, iterate_capacity=100)
+    floor = reference_floor(lp, p, 100, b)
+    runs = {}
+    for pairs in ("1", "0"):
+        monkeypatch.setenv("FOLP_PAIRS", pairs)
+        monkeypatch.setenv("FOLP_TIMING", "1")
+        a = eng.solve_lp(lp, p, iterate_capacity=100)
+        assert ("pair kernel" in capfd.readouterr().err) == (pairs == "1")
+        assert_within_floor(a.iterate_trace, b.iterate_trace, floor, f"pairs={pairs}")
+        assert a.restart_iterations == b.restart_iterations
+        assert a.kkt_passes == b.kkt_passes
+        runs[pairs] = a
+    (i1, e1, x1, y1), (i0, e0, x0, y0) = runs["1"].iterate_trace[0], runs["0"].iterate_trace[0]
+    assert i1 == i0 == 1 and e1 == e0
+    assert np.array_equal(x1, x0) and np.array_equal(y1, y0)
