@@ -299,6 +299,11 @@ struct folp_gpu_ctx {
     return rb;
   }
   int partial_cap = 0;  // slots (of kMaxAcc doubles) in `partials`
+  // kernel A's deferred sums (segdot.cuh DeferredSums): its own partial
+  // slots, the slot count of its last launch, and the switch launch_slot sets
+  double* partials_a = nullptr;
+  int a_np = 0;
+  bool a_defer = false;
 
   // exact parallel fold (exactfold.cuh) of ordered mode's trial sums
   FoldScratch fold{};
@@ -438,6 +443,7 @@ struct folp_gpu_ctx {
     cfg.attrs = attr;
     cfg.numAttrs = na;
     CK(cudaLaunchKernelEx(&cfg, fn, p.sp.S, p.sp.idx, val, p.sp.vec_len, epi, rb));
+    last_np = grid;
   }
   template <class Epi, bool ORD, bool PR, int ST = 0, bool SE = false>
   void launch_segdot(int grid, const SegPlan& sp, const double* val, const Epi& epi, RedBuf rb,
@@ -480,6 +486,12 @@ struct folp_gpu_ctx {
   void seg(const PlanDev& p, const double* val, const Epi& epi, int counter, int region = 1) {
     RedBuf rb = red(counter);
     const int64_t need = (static_cast<int64_t>(p.sp.n_units) + kWarps - 1) / kWarps;
+    if constexpr (std::is_same_v<Epi, EpiPrimal>) {
+      if (a_defer && !ordered) {
+        rb.partials = partials_a;
+        rb.tree_defer = 1;
+      }
+    }
     if (ordered) {
       rb.terms = terms[region];
       rb.nterm = p.sp.S;
@@ -506,6 +518,7 @@ struct folp_gpu_ctx {
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, false, true>(grid, p.sp, prod, epi, rb);
+      last_np = grid + p.sp.n_multi + p.sp.sell.n_groups;
       ++launches;
     } else if (pairs_ok<Epi>(p)) {
       if constexpr (TraceSlot<Epi>::v >= 0) launch_pairs(p, val, epi, rb);
@@ -515,6 +528,7 @@ struct folp_gpu_ctx {
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, false, false, 0, true>(grid, p.sp, val, epi, rb);
+      last_np = grid + p.sp.n_multi + p.sp.sell.n_groups;
     } else if (stage_ok(p)) {
       // the gathered vector in shared memory (segdot.cuh, staged gathers)
       auto fn = segdot_kernel<Epi, false, false, 1>;
@@ -522,15 +536,21 @@ struct folp_gpu_ctx {
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn), smem);
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, false, false, 1>(grid, p.sp, val, epi, rb, smem);
+      last_np = grid + p.sp.n_multi + p.sp.sell.n_groups;
     } else {
       auto fn = segdot_kernel<Epi, false>;
       const int64_t cap = static_cast<int64_t>(sms) * occupancy(reinterpret_cast<const void*>(fn));
       const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, std::min<int64_t>(cap, kMaxGrid))));
       launch_segdot<Epi, false, false>(grid, p.sp, val, epi, rb);
+      last_np = grid + p.sp.n_multi + p.sp.sell.n_groups;
     }
     ++launches;
     CK(cudaGetLastError());
+    if constexpr (std::is_same_v<Epi, EpiPrimal>) {
+      if (rb.tree_defer) a_np = last_np;
+    }
   }
+  int last_np = 0;  // partial slots of the last tree-mode product launch
 
   template <class Op>
   void ew(int64_t count, const Op& op, int counter, int region = 1) {
@@ -924,6 +944,7 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
     }
     c->partials = c->alloc<double>(static_cast<size_t>(kMaxGrid + c->max_giant + 8) * kMaxAcc);
     c->partial_cap = kMaxGrid + c->max_giant + 8;
+    c->partials_a = c->alloc<double>(static_cast<size_t>(c->partial_cap) * EpiPrimal::K);
     if (c->ordered) {
       c->terms[0] = c->alloc<double>(5 * std::max(n, m) + 8);
       c->terms[1] = c->alloc<double>(5 * (n + m) + 8);

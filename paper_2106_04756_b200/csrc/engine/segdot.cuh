@@ -172,6 +172,8 @@ struct RedBuf {
   double* scratch = nullptr;  // ordered mode: [nnz] products of long segments
                               // (warp_exact_fold); null = one lane folds them
   int cap = 0;                // partial slots allocated (checked build; 0 = unknown)
+  int tree_defer = 0;         // tree mode: store the CTA partials only; the successor
+                              // kernel's last CTA sums them (DeferredSums below)
 };
 
 // Reduction sinks.  Tree mode accumulates in registers (fast, deterministic
@@ -327,6 +329,49 @@ struct StateTail<E, std::void_t<decltype(E::kStateWords)>> {
   static constexpr int words = E::kStateWords;
 };
 
+// The final pass over the per-CTA partials (np slots of K values): a fixed
+// thread -> slot mapping and tree, so the totals depend on the partials and
+// np alone.  Result valid in thread 0.
+template <int K>
+__device__ __forceinline__ void sum_partials(const double* partials, int np, double (*s_vec)[K],
+                                             double (&tot)[K]) {
+  double part[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) part[k] = 0.0;
+  // all of a thread's loads in flight at once (same per-thread order)
+  constexpr int R = K <= 2 ? 4 : 2;
+  for (int base = threadIdx.x; base < np; base += kBlock * R) {
+    double v[R][K];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = base + r * kBlock;
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[r][k] = i < np ? ld_cg(&partials[i * K + k]) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (base + r * kBlock < np) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) part[k] += v[r][k];
+      }
+    }
+  }
+  block_sum_vec<K>(part, s_vec, tot);
+}
+
+// Deferred sums: a kernel whose totals only its successor's decision needs
+// (kernel A's sum omega dx^2 and non-finite flag, consumed by kernel B's
+// step rule) stores its CTA partials and exits -- no ticket, no last-CTA
+// pass, so its successor's griddepcontrol.wait releases that much earlier;
+// the successor's last CTA sums them with the same sum_partials (same bits)
+// next to its own.  An epilogue that consumes such sums provides
+//   static constexpr int kDeferredK;  const double* deferred_partials() const;
+//   int deferred_np() const;  void absorb_deferred(const double (&)[kDeferredK], words) const;
+template <class E, class = void>
+struct DeferredSums { static constexpr int k = 0; };
+template <class E>
+struct DeferredSums<E, std::void_t<decltype(E::kDeferredK)>> { static constexpr int k = E::kDeferredK; };
+
 // Per-block partial + last-block-done final reduction, then epi.finalize().
 template <class Epi>
 __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K], RedBuf rb,
@@ -340,10 +385,14 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) rb.partials[blockIdx.x * K + k] = tot[k];
-    fence_acq_rel();
-    const unsigned ticket = atomicAdd(rb.counter, 1u);
-    s_last = (ticket == gridDim.x - 1) ? 1 : 0;
-    if (s_last) fence_acq_rel();  // acquire; the barrier below extends it to the CTA
+    if (rb.tree_defer) {
+      s_last = 0;  // the successor kernel sums the partials
+    } else {
+      fence_acq_rel();
+      const unsigned ticket = atomicAdd(rb.counter, 1u);
+      s_last = (ticket == gridDim.x - 1) ? 1 : 0;
+      if (s_last) fence_acq_rel();  // acquire; the barrier below extends it to the CTA
+    }
   }
   __syncthreads();
   if (!s_last) return;
@@ -356,28 +405,16 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
     if (threadIdx.x == kBlock - 1) epi.tail_aux(s_rg);
   }
   const int np = static_cast<int>(gridDim.x) + n_extra;
-  double part[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) part[k] = 0.0;
-  // all of a thread's loads in flight at once (same per-thread order)
-  constexpr int R = K <= 2 ? 4 : 2;
-  for (int base = threadIdx.x; base < np; base += kBlock * R) {
-    double v[R][K];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = base + r * kBlock;
-#pragma unroll
-      for (int k = 0; k < K; ++k) v[r][k] = i < np ? ld_cg(&rb.partials[i * K + k]) : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (base + r * kBlock < np) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) part[k] += v[r][k];
-      }
+  sum_partials<K>(rb.partials, np, s_vec, tot);
+  constexpr int DK = DeferredSums<Epi>::k;
+  if constexpr (DK > 0 && SW > 0) {
+    if (epi.deferred_partials() != nullptr) {
+      __shared__ double s_dvec[kWarps][DK];
+      double dtot[DK];
+      sum_partials<DK>(epi.deferred_partials(), epi.deferred_np(), s_dvec, dtot);
+      if (threadIdx.x == 0) epi.absorb_deferred(dtot, s_state);
     }
   }
-  block_sum_vec<K>(part, s_vec, tot);
   trace_tail<Epi>(1);
   if (threadIdx.x == 0) {
     if constexpr (SW > 0) {

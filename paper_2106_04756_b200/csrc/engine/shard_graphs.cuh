@@ -200,19 +200,33 @@ void launch_slot(folp_gpu_ctx* c, int policy, const LoopBufs& b) {
     // ordered mode: the products only store their terms; one cooperative
     // k_exact_fold folds them exactly in the reference's order and decides
     const bool fold = c->ordered && c->fold_grid > 0 && !c->sharded();
+    // tree mode, plain (unsharded, unwindowed) products: kernel A leaves its
+    // two sums as CTA partials for kernel B's last CTA (segdot.cuh
+    // DeferredSums; FOLP_DEFER_A=0 keeps kernel A's own last-CTA pass)
+    const char* denv = std::getenv("FOLP_DEFER_A");
+    const bool defer_a = !c->ordered && !c->sharded() && c->brows.windows == 0 &&
+                         c->bcols.windows == 0 && (denv == nullptr || std::atoi(denv) > 0);
     try {
       c->defer_tail = fold;
+      c->a_defer = defer_a;
       axis_product(c, false, true, EpiPrimal{b}, 2, 0);
+      c->a_defer = false;
+      EpiDual ed{b};
+      if (defer_a) {
+        ed.a_partials = c->partials_a;
+        ed.a_np = c->a_np;
+      }
       if (c->sell && c->sell_packed && !c->sharded() && c->brows.windows == 0) {
-        c->seg(c->rows_sell, c->csr_work, EpiDual{b}, 3, 1);  // SELL-32 groups (sell.cuh)
+        c->seg(c->rows_sell, c->csr_work, ed, 3, 1);  // SELL-32 groups (sell.cuh)
       } else {
-        axis_product(c, true, true, EpiDual{b}, 3, 1);
+        axis_product(c, true, true, ed, 3, 1);
       }
       c->defer_tail = false;
       if (fold) c->launch_trial_fold(b);
     } catch (...) {
       c->pdl = false;
       c->defer_tail = false;
+      c->a_defer = false;
       throw;
     }
     c->pdl = false;
