@@ -143,6 +143,7 @@ int occupancy(const void* fn, int smem = 0) {
   return b;
 }
 
+constexpr double kL2PersistFill = 1.0;  // share of the persisting carve-out the loop's streams may pin
 constexpr int kResSlots = 96;
 constexpr int kCounters = 16;
 constexpr int kMaxGrid = 148 * 8;
@@ -1040,8 +1041,11 @@ int folp_gpu_create_ordered(const folp_gpu_problem* p, const int64_t* col_order,
         const size_t bytes = std::min(c->loop_block_bytes, static_cast<size_t>(max_window));
         attr.accessPolicyWindow.base_ptr = c->loop_block;
         attr.accessPolicyWindow.num_bytes = bytes;
-        attr.accessPolicyWindow.hitRatio =
-            static_cast<float>(std::min(1.0, static_cast<double>(max_persist) / bytes));
+        // the fraction of the window's lines that persist (the rest stream);
+        // FOLP_L2_HIT_RATIO overrides
+        double ratio = std::min(1.0, kL2PersistFill * static_cast<double>(max_persist) / bytes);
+        if (const char* renv = std::getenv("FOLP_L2_HIT_RATIO")) ratio = std::min(1.0, std::max(0.0, std::atof(renv)));
+        attr.accessPolicyWindow.hitRatio = static_cast<float>(ratio);
         attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
