@@ -155,10 +155,16 @@ void build_plan(folp_gpu_ctx* c, const int64_t* ptr, int64_t S, int64_t nnz,
   // least work so far, largest first (LPT).  FOLP_BALANCE=0 disables.
   const char* benv = std::getenv("FOLP_BALANCE");
   const int nw = c->sms * kPlanCtasPerSm * kWarps;
-  auto cost = [](const int4& d) -> int64_t {
-    if (d.x <= -kSellTag) return 32 * static_cast<int64_t>(d.w - d.z) + 64 + 24;
+  // modelled unit cost: entries + kCostSeg per segment + kCostUnit per unit
+  // (FOLP_COST_SEG / FOLP_COST_UNIT override, for tuning)
+  const char* cs_env = std::getenv("FOLP_COST_SEG");
+  const char* cu_env = std::getenv("FOLP_COST_UNIT");
+  const int64_t cost_seg = cs_env != nullptr ? std::atoll(cs_env) : 2;
+  const int64_t cost_unit = cu_env != nullptr ? std::atoll(cu_env) : 24;
+  auto cost = [cost_seg, cost_unit](const int4& d) -> int64_t {
+    if (d.x <= -kSellTag) return 32 * static_cast<int64_t>(d.w - d.z) + 64 + cost_unit;
     const int64_t segs = d.x >= 0 ? d.y - d.x : 1;
-    return (d.w - d.z) + 2 * segs + 24;
+    return (d.w - d.z) + cost_seg * segs + cost_unit;
   };
   // max / mean CTA load of the plain round-robin order: even plans (config
   // 5's equal parts and tiles) are left alone -- reordering them measured

@@ -717,25 +717,40 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
       for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
       if (single) {
         if (lane == 0) epi.apply(-d.y - 2, sum, pre_single, acc);
-      } else if (lane == 0) {
-        p.part_sums[d.y] = sum;
-        fence_acq_rel();
-        const int np = p.multi_parts[multi];
-        const unsigned arrived = atomicAdd(&p.arrivals[multi], 1u);
-        if (arrived == static_cast<unsigned>(np - 1)) {
+      } else {
+        int np = 0;
+        unsigned last = 0;
+        if (lane == 0) {
+          p.part_sums[d.y] = sum;
+          fence_acq_rel();
+          np = p.multi_parts[multi];
+          last = atomicAdd(&p.arrivals[multi], 1u) == static_cast<unsigned>(np - 1) ? 1u : 0u;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          // The last part to arrive sums the segment's part sums with the
+          // whole warp: lane l takes parts l, l + 32, ... in order, then a
+          // fixed shuffle tree (deterministic, arrival order never matters).
+          // One lane walking config 3's 977-part row alone was the kernel's
+          // last straggler: units done p99 113 us, p100 148 us.
+          np = __shfl_sync(0xffffffffu, np, 0);
           fence_acq_rel();
           const int first = p.multi_first[multi];
           double total = 0.0;
-          for (int q = 0; q < np; ++q) total += ld_cg(&p.part_sums[first + q]);
-          const int seg = p.multi_seg[multi];
-          TreeAcc<K> macc;
-          macc.zero();
-          epi.apply(seg, total, epi.load(seg), macc);
-          if constexpr (Epi::kReduce) {
+          for (int q = lane; q < np; q += 32) total += ld_cg(&p.part_sums[first + q]);
 #pragma unroll
-            for (int k = 0; k < K; ++k) rb.partials[(gridDim.x + multi) * K + k] = macc.v[k];
+          for (int off = 16; off > 0; off >>= 1) total += __shfl_down_sync(0xffffffffu, total, off);
+          if (lane == 0) {
+            const int seg = p.multi_seg[multi];
+            TreeAcc<K> macc;
+            macc.zero();
+            epi.apply(seg, total, epi.load(seg), macc);
+            if constexpr (Epi::kReduce) {
+#pragma unroll
+              for (int k = 0; k < K; ++k) rb.partials[(gridDim.x + multi) * K + k] = macc.v[k];
+            }
+            p.arrivals[multi] = 0u;
           }
-          p.arrivals[multi] = 0u;
         }
       }
     }
