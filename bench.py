@@ -15,7 +15,9 @@ session (include/folp_c.h folp_session_*).
                (three solves, the median reported, all three listed)
   roofline   : fused step kernels (K'y+primal step, Kx'+dual step) --
                algorithmic bytes per trial slot 24*nnz + 68*(m+n)
-               (SURVEY.md 8d) over their CUDA-event time, vs measured HBM peak;
+               (SURVEY.md 8d), less 8*n per bound vector that is one 0 /
+               infinite value (a constant to the algorithm, not a stream),
+               over their CUDA-event time, vs measured HBM peak;
                traffic = the DRAM bytes ncu measured for one trial
                (profiles/r2_traffic.json)
   cpu_baseline: the compiled reference (oracle/_ref) on 1 host core
@@ -54,10 +56,23 @@ UNIT = "iter/s"
 CADENCE = 40
 
 
-def bytes_per_trial(m: int, n: int, nnz: int) -> int:
+def bytes_per_trial(m: int, n: int, nnz: int, uniform_bounds: int = 0) -> int:
     """Algorithmic HBM bytes of one trial slot (kernel A + kernel B), fp64 values,
-    int32 indices/pointers, every vector touched once."""
-    return 24 * nnz + 68 * (m + n)
+    int32 indices/pointers, every vector touched once, less the
+    bound vectors the algorithm does not need: a lower (upper) bound that is
+    the same 0 / infinite value for every variable stays uniform under the
+    diagonal rescaling and is a constant, not an 8-byte stream per column."""
+    return 24 * nnz + 68 * (m + n) - 8 * n * uniform_bounds
+
+
+def uniform_bound_count(lp) -> int:
+    """How many of (lower, upper) are one scale-invariant value (0 or +-inf)."""
+    count = 0
+    for v in (lp.variable_lower, lp.variable_upper):
+        v = np.asarray(v)
+        if v.size and (v[0] == 0.0 or np.isinf(v[0])) and bool(np.all(v == v[0])):
+            count += 1
+    return count
 
 
 def measured_traffic(config: int):
@@ -346,7 +361,8 @@ def run_b200(args, world, rank, local):
     slots = s1["loop_slots"] - s0["loop_slots"]
     loop_ms = s1["loop_ms"] - s0["loop_ms"]
     launches = s1["launches"] - s0["launches"]
-    b_trial = bytes_per_trial(m, n, nnz)
+    n_uniform = uniform_bound_count(lp)
+    b_trial = bytes_per_trial(m, n, nnz, n_uniform)
     achieved = b_trial * slots / (loop_ms / 1000.0) / 1e9 if loop_ms > 0 else 0.0
     peak, peak_src = measured_peak()
 
@@ -388,6 +404,8 @@ def run_b200(args, world, rank, local):
                      "frac": achieved / peak, "traffic": measured_traffic(args.config),
                      "kernel": "segdot_kernel<EpiPrimal> + segdot_kernel<EpiDual> (one trial)",
                      "bytes_per_launch_pair": b_trial,
+                     "bytes_model": "24*nnz + 68*(m+n) - 8*n per uniform (0 or infinite) bound vector: %d uniform"
+                                    % n_uniform,
                      "kernel_ms_per_trial": loop_ms / max(1, slots), "peak_source": peak_src},
         "e2e": {"value": e2e_iters * jobs / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),

@@ -315,16 +315,15 @@ struct EpiDual {
     decide_trial(b, tot[0], movement, st->bad_a != 0.0 || tot[2] != 0.0);
   }
   // kernel A's deferred sums (segdot.cuh DeferredSums): its CTA partials,
-  // summed here by the last CTA into the shared copy of the state
+  // summed by this kernel's highest-numbered CTA at its start into the state
   static constexpr int kDeferredK = 2;  // EpiPrimal::K
   const double* a_partials = nullptr;
   int a_np = 0;
   __device__ const double* deferred_partials() const { return a_partials; }
   __device__ int deferred_np() const { return a_np; }
-  __device__ void absorb_deferred(const double (&tot)[kDeferredK], unsigned long long* words) const {
-    DevState* st = reinterpret_cast<DevState*>(words);
-    st->sx = tot[0];     // EpiPrimal::finalize
-    st->bad_a = tot[1];
+  __device__ void store_deferred(const double (&tot)[kDeferredK]) const {
+    b.st->sx = tot[0];     // EpiPrimal::finalize
+    b.st->bad_a = tot[1];
   }
   // the decision on the last CTA's shared copy of the state (segdot.cuh StateTail)
   static constexpr int kStateWords = sizeof(DevState) / 8;

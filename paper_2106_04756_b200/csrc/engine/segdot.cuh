@@ -339,7 +339,7 @@ __device__ __forceinline__ void sum_partials(const double* partials, int np, dou
 #pragma unroll
   for (int k = 0; k < K; ++k) part[k] = 0.0;
   // all of a thread's loads in flight at once (same per-thread order)
-  constexpr int R = K <= 2 ? 4 : 2;
+  constexpr int R = K <= 3 ? 4 : 2;
   for (int base = threadIdx.x; base < np; base += kBlock * R) {
     double v[R][K];
 #pragma unroll
@@ -362,15 +362,30 @@ __device__ __forceinline__ void sum_partials(const double* partials, int np, dou
 // Deferred sums: a kernel whose totals only its successor's decision needs
 // (kernel A's sum omega dx^2 and non-finite flag, consumed by kernel B's
 // step rule) stores its CTA partials and exits -- no ticket, no last-CTA
-// pass, so its successor's griddepcontrol.wait releases that much earlier;
-// the successor's last CTA sums them with the same sum_partials (same bits)
-// next to its own.  An epilogue that consumes such sums provides
+// pass, so its successor's griddepcontrol.wait releases that much earlier.
+// The successor's highest-numbered CTA sums them at its START with the same
+// sum_partials (same bits) and stores the totals where the decision reads
+// them -- under the product, not in its serial tail; the store precedes that
+// CTA's own arrival ticket, so the last CTA's acquire covers it.  An
+// epilogue that consumes such sums provides
 //   static constexpr int kDeferredK;  const double* deferred_partials() const;
-//   int deferred_np() const;  void absorb_deferred(const double (&)[kDeferredK], words) const;
+//   int deferred_np() const;  void store_deferred(const double (&)[kDeferredK]) const;
 template <class E, class = void>
 struct DeferredSums { static constexpr int k = 0; };
 template <class E>
 struct DeferredSums<E, std::void_t<decltype(E::kDeferredK)>> { static constexpr int k = E::kDeferredK; };
+template <class Epi>
+__device__ __forceinline__ void absorb_deferred_sums(const Epi& epi) {
+  constexpr int DK = DeferredSums<Epi>::k;
+  if constexpr (DK > 0) {
+    if (blockIdx.x == gridDim.x - 1 && epi.deferred_partials() != nullptr) {  // CTA-uniform
+      __shared__ double s_dvec[kWarps][DK];
+      double dtot[DK];
+      sum_partials<DK>(epi.deferred_partials(), epi.deferred_np(), s_dvec, dtot);
+      if (threadIdx.x == 0) epi.store_deferred(dtot);
+    }
+  }
+}
 
 // Per-block partial + last-block-done final reduction, then epi.finalize().
 template <class Epi>
@@ -406,15 +421,6 @@ __device__ __forceinline__ void reduce_tail(const Epi& epi, double (&acc)[Epi::K
   }
   const int np = static_cast<int>(gridDim.x) + n_extra;
   sum_partials<K>(rb.partials, np, s_vec, tot);
-  constexpr int DK = DeferredSums<Epi>::k;
-  if constexpr (DK > 0 && SW > 0) {
-    if (epi.deferred_partials() != nullptr) {
-      __shared__ double s_dvec[kWarps][DK];
-      double dtot[DK];
-      sum_partials<DK>(epi.deferred_partials(), epi.deferred_np(), s_dvec, dtot);
-      if (threadIdx.x == 0) epi.absorb_deferred(dtot, s_state);
-    }
-  }
   trace_tail<Epi>(1);
   if (threadIdx.x == 0) {
     if constexpr (SW > 0) {
@@ -521,6 +527,7 @@ segdot_kernel(SegPlan p, const double* __restrict__ val, Epi epi, RedBuf rb) {
   griddep_wait();
   griddep_launch();            // the successor may start filling freed SMs
   if (!epi.prepare()) return;  // loop slot disabled: every CTA agrees
+  if constexpr (!ORDERED) absorb_deferred_sums(epi);
 #ifdef FOLP_WARP_TIMES
   trace_warp<Epi>(0, global_ns());
 #endif
@@ -814,6 +821,7 @@ pair_kernel(int S, const int* __restrict__ idx, const double* __restrict__ val, 
   griddep_wait();
   griddep_launch();
   if (!epi.prepare()) return;
+  absorb_deferred_sums(epi);
   const double* __restrict__ vec = epi.vec();
   TreeAcc<K> acc;
   acc.zero();
