@@ -299,3 +299,23 @@ def test_two_entry_columns(eng, ref, scale, monkeypatch, capfd):
     (i1, e1, x1, y1), (i0, e0, x0, y0) = runs["1"].iterate_trace[0], runs["0"].iterate_trace[0]
     assert i1 == i0 == 1 and e1 == e0
     assert np.array_equal(x1, x0) and np.array_equal(y1, y0)
+
+
+def test_deferred_sums_bit_identical(eng, monkeypatch):
+    """Kernel A's two sums left as CTA partials for kernel B (engine
+    segdot.cuh DeferredSums) against kernel A's own last-CTA reduction
+    (FOLP_DEFER_A=0): the same partials through the same tree, so every bit
+    of a 200-iteration tree-mode solve agrees (members of configs 2 and 5:
+    warp tiles and the pair kernel)."""
+    for cfg, scale in [(2, 0.05), (5, 0.05)]:
+        lp = instances.generate(cfg, 3, scale)
+        p = cabi.params(iteration_limit=200)
+        monkeypatch.delenv("FOLP_DEFER_A", raising=False)
+        a = eng.solve_lp(lp, p)
+        monkeypatch.setenv("FOLP_DEFER_A", "0")
+        b = eng.solve_lp(lp, p)
+        assert np.array_equal(a.primal_solution, b.primal_solution), cfg
+        assert np.array_equal(a.dual_solution, b.dual_solution), cfg
+        assert np.array_equal(a.reduced_costs, b.reduced_costs), cfg
+        assert a.restart_iterations == b.restart_iterations and a.step_trials == b.step_trials
+        assert a.final_info == b.final_info
