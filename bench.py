@@ -402,7 +402,8 @@ def run_b200(args, world, rank, local):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": measured_traffic(args.config),
-                     "kernel": "segdot_kernel<EpiPrimal> + segdot_kernel<EpiDual> (one trial)",
+                     "kernel": "kernel A (K'y + primal step: segdot_kernel<EpiPrimal>, pair_kernel<EpiPrimal> on "
+                               "two-entry columns) + kernel B (K x' + dual step: segdot_kernel<EpiDual>), one trial",
                      "bytes_per_launch_pair": b_trial,
                      "bytes_model": "24*nnz + 68*(m+n) - 8*n per uniform (0 or infinite) bound vector: %d uniform"
                                     % n_uniform,
